@@ -1,0 +1,189 @@
+/*
+ * asicp.h — C-ABI of the B200-native AS-ICP grasp optimiser.
+ *
+ * This is the drop-in boundary for the reference hot path
+ *   graspmatch::GraspSolution graspmatch::optimize_grasp(const GraspProblem&)
+ *   (/root/reference/proj/include/graspmatch/grasp.hpp:141, defined at
+ *    /root/reference/proj/src/grasp.cpp:132-307).
+ * The reference has no FFI layer of its own; its C++ entry point is replaced
+ * at link time by the adapter in paper_2412_08346_b200/csrc/graspmatch_adapter.cpp,
+ * which marshals GraspProblem into the POD structs below.
+ *
+ * Plain C: no torch/Eigen/CUDA types cross this boundary.  All point arrays are
+ * row-major xyz float64 (n x 3); poses are 7-vectors (tx, ty, tz, qw, qx, qy, qz)
+ * exactly like graspmatch::PoseParams::as_vector (types.hpp:24-41).
+ *
+ * Return codes of every int-returning entry point:
+ *   ASICP_OK (0)            success
+ *   ASICP_INVALID_ARGUMENT  contract violation; the message graspmatch would
+ *                           have thrown as InvalidArgument is copied into err
+ *   ASICP_DEVICE_ERROR      CUDA failure (message in err)
+ */
+#ifndef ASICP_H_
+#define ASICP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASICP_ABI_VERSION 1
+
+#define ASICP_OK 0
+#define ASICP_INVALID_ARGUMENT 1
+#define ASICP_DEVICE_ERROR 2
+
+/* graspmatch::GraspStatus (grasp.hpp:76) */
+#define ASICP_STATUS_FOUND 0
+#define ASICP_STATUS_NO_GRASP_FOUND 1
+
+/* graspmatch::BandwidthMode (optim.hpp:56) */
+#define ASICP_BANDWIDTH_MEDIAN 0
+#define ASICP_BANDWIDTH_FIXED 1
+
+/* Context options (asicp_set_option). */
+#define ASICP_OPT_NN_MODE 1        /* 0 = FP32 filter + FP64 certification (default), 1 = FP64 brute force */
+#define ASICP_OPT_USE_GRAPH 2      /* 1 = capture the iteration loop in a CUDA graph (default 1) */
+#define ASICP_OPT_PROFILE 3        /* 1 = record per-kernel CUDA events (asicp_get_stats) */
+
+/* One voxel grid of the stacked gripper SDF (graspmatch::SdfGrid, sdf.hpp:23-39,
+ * plus its StackedSdf offset, sdf.hpp:43-47). */
+typedef struct asicp_sdf_grid {
+  int32_t dims[3];           /* node counts per axis */
+  double origin[3];
+  double voxel;
+  double boundary_max_abs;
+  double offset[3];          /* StackedSdf::offsets[i] */
+  const float* values;       /* dims[0]*dims[1]*dims[2], x-major ((ix*ny)+iy)*nz+iz */
+} asicp_sdf_grid;
+
+/* graspmatch::Preshape (grasp.hpp:16-24). */
+typedef struct asicp_preshape {
+  const double* inner_surface; /* S: n_surface x 3, gripper frame */
+  int64_t n_surface;
+  const double* full_cloud;    /* G: validated non-empty only (grasp.cpp:15) */
+  int64_t n_full;
+  double tcp[3];
+  int64_t sdf_index;
+} asicp_preshape;
+
+/* graspmatch::GraspProblem (grasp.hpp:27-44) with SgdConfig / SteinConfig
+ * (optim.hpp:28-76) flattened.  Caller-owned; never retained after return. */
+typedef struct asicp_problem {
+  const double* object_cloud;  /* R: n_object x 3 */
+  int64_t n_object;
+  const double* scene_cloud;   /* C: n_scene x 3 */
+  int64_t n_scene;
+  const asicp_preshape* preshapes;
+  int64_t n_preshapes;
+  const asicp_sdf_grid* sdf_grids;
+  int64_t n_sdf_grids;
+  double com[3];
+  /* initializations: per preshape p, init_counts[p] poses; rows concatenated
+   * preshape-major (the global particle order of grasp.cpp:135-145). */
+  const double* init_poses;    /* J x 7 */
+  const int64_t* init_counts;  /* n_preshapes entries */
+  /* SgdConfig */
+  double learning_rate;
+  double A[49];                /* row-major 7x7 preconditioner */
+  double convergence_threshold;
+  /* SteinConfig */
+  int32_t bandwidth_mode;
+  double fixed_bandwidth;
+  double prior_t_mean[3];
+  double prior_t_sigma[3];
+  double prior_q_location[4];
+  double prior_q_kappa[4];
+  int64_t anneal_period_total; /* AnnealingSchedule::period_total (T) */
+  int64_t anneal_cycles;       /* C */
+  double anneal_exponent;      /* p */
+  double step_scale;
+  /* GraspProblem scalars */
+  int64_t k_stein;
+  int64_t k_max;
+  double contact_tolerance;
+  uint64_t seed;
+  int32_t workers;             /* accepted and ignored (results are worker-count invariant) */
+  int32_t record_trace;
+} asicp_problem;
+
+/* graspmatch::GraspSolution (grasp.hpp:78-86).  Scalars are filled by the
+ * library; every array pointer is caller-allocated and may be NULL. */
+typedef struct asicp_solution {
+  int32_t status;              /* ASICP_STATUS_* */
+  double theta[7];
+  int64_t preshape_id;
+  double final_loss;
+  int32_t converged;
+  int64_t n_particles;         /* J (filled) */
+  /* ParticleSummary (grasp.hpp:67-74), global particle order, J entries */
+  double* particle_theta;      /* J x 7 */
+  double* particle_loss;       /* J: full_cloud_loss */
+  int32_t* particle_collision_free;
+  int32_t* particle_converged;
+  int64_t* particle_preshape;
+  /* TraceRecord (grasp.hpp:57-65), row-major iteration x particle, k_max*J
+   * entries, written only when record_trace != 0.  iteration / particle /
+   * preshape / phase follow from the row index and the problem. */
+  double* trace_theta;         /* (k_max*J) x 7, pre-update pose */
+  double* trace_loss;          /* k_max*J */
+  int32_t* trace_in_collision; /* k_max*J */
+  /* Diagnostics (not part of the reference contract). */
+  int64_t nn_queries;          /* nearest-neighbour queries resolved */
+  int64_t nn_uncertified;      /* queries the FP32 filter could not certify alone */
+  int64_t nn_full_refines;     /* queries that needed a full FP64 rescan */
+  int64_t nn_pool_ties;        /* exact FP64 ties between distinct points resolved by canonical order */
+  double nn_pairs;             /* (query, candidate) pairs evaluated by the NN kernels */
+} asicp_solution;
+
+/* Per-kernel device timing collected when ASICP_OPT_PROFILE is set. */
+typedef struct asicp_stats {
+  double solve_ms;             /* device time of the last asicp_run (events on the ctx stream) */
+  double nn_ms;                /* summed device time of NN filter launches */
+  int64_t nn_launches;
+  double nn_pairs;             /* candidate pairs processed by those launches */
+  double collide_ms;
+  double minibatch_ms;
+  double cost_ms;
+  double svgd_ms;
+  int64_t kernel_launches;     /* kernels enqueued by the last asicp_run */
+} asicp_stats;
+
+typedef struct asicp_ctx asicp_ctx;
+
+/* ABI version check. */
+int asicp_abi_version(void);
+
+/* Create a context on CUDA device `device`.  `stream` is a cudaStream_t to
+ * launch on (NULL: the context creates its own non-blocking stream).
+ * Device buffers persist across calls. Returns NULL on failure (message in err). */
+asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen);
+void asicp_destroy(asicp_ctx* ctx);
+
+int asicp_set_option(asicp_ctx* ctx, int option, int64_t value);
+
+/* Validate (GraspProblem::validate, grasp.cpp:20-31, plus the in-loop
+ * requires) and upload the problem into device memory. */
+int asicp_prepare(asicp_ctx* ctx, const asicp_problem* problem, char* err, size_t errlen);
+
+/* Run optimize_grasp on the prepared, device-resident problem and fill the
+ * solution (synchronous with respect to the host). */
+int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen);
+
+/* prepare + run: the drop-in for graspmatch::optimize_grasp. */
+int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution,
+                         char* err, size_t errlen);
+
+int asicp_get_stats(asicp_ctx* ctx, asicp_stats* stats);
+
+/* Host-side reference helpers used by the adapter/tests (pure functions). */
+int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref); /* spatial_index.cpp:133-139 */
+double asicp_annealing(int64_t t, int64_t T, int64_t C, double p);        /* optim.cpp:158-164 */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ASICP_H_ */
