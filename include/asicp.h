@@ -84,7 +84,8 @@ typedef struct asicp_problem {
   /* initializations: per preshape p, init_counts[p] poses; rows concatenated
    * preshape-major (the global particle order of grasp.cpp:135-145). */
   const double* init_poses;    /* J x 7 */
-  const int64_t* init_counts;  /* n_preshapes entries */
+  const int64_t* init_counts;  /* n_init_lists entries */
+  int64_t n_init_lists;        /* GraspProblem::initializations.size(); must equal n_preshapes */
   /* SgdConfig */
   double learning_rate;
   double A[49];                /* row-major 7x7 preconditioner */

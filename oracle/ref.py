@@ -1,0 +1,155 @@
+"""Parity oracle — TEST INFRASTRUCTURE ONLY.
+
+ctypes access to oracle/_ref/libgraspmatch_ref.so: the UNMODIFIED reference
+(/root/reference/proj/src/*.cpp, built by oracle/Makefile against the Eigen /
+doctest subset shims) plus a bridge taking the product's asicp_problem struct
+(oracle/ref_bridge.cpp).  Only tests/, __graft_entry__.smoke() and bench.py's
+CPU-baseline legs use this module — it is the checker, never the product.
+
+Pinning (tests/test_oracle.py): the reference's own 103 unit tests and 9/9
+acceptance criteria pass on this build, and the desk seed-0 solve reproduces
+proj/README.md:43-46 to every printed digit.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from paper_2412_08346_b200 import _lib as L
+from paper_2412_08346_b200.grasp import (CProblem, GraspProblem, GraspSolution, InvalidArgument, SolutionBuffers,
+                                         problem_from_c)
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "_ref" / "libgraspmatch_ref.so"
+_LIB = None
+
+
+def available() -> bool:
+    return LIB_PATH.exists()
+
+
+def load() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} missing: run `make -C oracle` where /root/reference exists")
+        lib = C.CDLL(str(LIB_PATH))
+        lib.ref_optimize_grasp.argtypes = [C.POINTER(L.Problem), C.POINTER(L.Solution), C.c_char_p, C.c_size_t]
+        lib.ref_desk_problem.restype = C.c_void_p
+        lib.ref_desk_problem.argtypes = [C.c_uint64, C.c_int, C.c_int64, C.c_int64]
+        lib.ref_self_matching_problem.restype = C.c_void_p
+        lib.ref_problem_view.restype = C.POINTER(L.Problem)
+        lib.ref_problem_view.argtypes = [C.c_void_p]
+        lib.ref_problem_free.argtypes = [C.c_void_p]
+        lib.ref_cylinder_cloud.argtypes = [C.c_double, C.c_double, C.c_int, C.c_uint64, L.c_double_p]
+        lib.ref_sample_minibatch_indices.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, L.c_i64_p]
+        lib.ref_nearest.restype = C.c_int64
+        lib.ref_nearest.argtypes = [L.c_double_p, C.c_int64, L.c_double_p, L.c_double_p]
+        lib.ref_colliding_flags.restype = C.c_int64
+        lib.ref_colliding_flags.argtypes = [C.POINTER(L.Problem), C.c_int64, L.c_double_p, L.c_i32_p]
+        lib.ref_sdf_query.restype = C.c_double
+        lib.ref_sdf_query.argtypes = [C.POINTER(L.Problem), C.c_int64, L.c_double_p]
+        lib.ref_build_sdf.restype = C.c_int64
+        lib.ref_build_sdf.argtypes = [L.c_double_p, C.c_int64, C.c_double, C.c_double, C.c_double, L.c_i32_p,
+                                      L.c_double_p, L.c_float_p]
+        _LIB = lib
+    return _LIB
+
+
+def optimize_grasp(problem) -> GraspSolution:
+    """Reference graspmatch::optimize_grasp on a GraspProblem / CProblem / Fixture."""
+    lib = load()
+    cp = problem if hasattr(problem, "ptr") else CProblem(problem)
+    bufs = SolutionBuffers(cp.J, cp.k_max, cp.record_trace)
+    err = C.create_string_buffer(512)
+    rc = lib.ref_optimize_grasp(cp.ptr(), C.byref(bufs.struct), err, 512)
+    if rc == L.ASICP_INVALID_ARGUMENT:
+        raise InvalidArgument(err.value.decode())
+    if rc != L.ASICP_OK:
+        raise RuntimeError(err.value.decode())
+    return bufs.solution(cp.k_stein)
+
+
+class RefFixture:
+    def __init__(self, handle):
+        self.lib = load()
+        self.handle = handle
+        self._view = self.lib.ref_problem_view(handle)
+
+    @property
+    def struct(self):
+        return self._view.contents
+
+    def ptr(self):
+        return self._view
+
+    @property
+    def J(self):
+        v = self.struct
+        return int(sum(v.init_counts[i] for i in range(v.n_init_lists)))
+
+    @property
+    def k_max(self):
+        return int(self.struct.k_max)
+
+    @property
+    def k_stein(self):
+        return int(self.struct.k_stein)
+
+    @property
+    def record_trace(self):
+        return bool(self.struct.record_trace)
+
+    def set(self, **fields):
+        for k, v in fields.items():
+            setattr(self.struct, k, v)
+        return self
+
+    def problem(self) -> GraspProblem:
+        return problem_from_c(self.struct)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.ref_problem_free(self.handle)
+        except Exception:
+            pass
+
+
+def desk(seed: int = 0, workers: int = 0, n_init: int = 100, n_top: int = 6) -> RefFixture:
+    return RefFixture(load().ref_desk_problem(seed, workers, n_init, n_top))
+
+
+def self_matching() -> RefFixture:
+    return RefFixture(load().ref_self_matching_problem())
+
+
+def sample_minibatch_indices(seed: int, n: int, m: int, skip: int = 0) -> np.ndarray:
+    out = np.zeros(m, dtype=np.int64)
+    rc = load().ref_sample_minibatch_indices(seed, skip, n, m, out.ctypes.data_as(L.c_i64_p))
+    if rc != 0:
+        raise InvalidArgument("sample_minibatch: m out of range")
+    return out
+
+
+def cylinder_cloud(radius=0.03, height=0.12, n=1500, seed=1) -> np.ndarray:
+    out = np.zeros((n, 3))
+    load().ref_cylinder_cloud(radius, height, n, seed, out.ctypes.data_as(L.c_double_p))
+    a_side = 2.0 * np.pi * radius * height
+    a_cap = np.pi * radius * radius
+    n_side = int(n * a_side / (a_side + 2.0 * a_cap))
+    return out[: n_side + 2 * ((n - n_side) // 2)]
+
+
+def build_sdf(cloud, voxel, padding=-1.0, band=0.003):
+    cloud = np.ascontiguousarray(cloud, dtype=np.float64)
+    dims = (C.c_int32 * 3)()
+    meta = (C.c_double * 5)()
+    lib = load()
+    n = lib.ref_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta, None)
+    vals = np.zeros(n, dtype=np.float32)
+    lib.ref_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta,
+                      vals.ctypes.data_as(L.c_float_p))
+    return tuple(dims), np.array(meta[:3]), meta[3], meta[4], vals

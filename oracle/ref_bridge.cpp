@@ -66,7 +66,7 @@ GraspProblem to_problem(const asicp_problem& p) {
   g.sdf.epsilon = eps;
   g.com = Vec3(p.com[0], p.com[1], p.com[2]);
   int64_t row = 0;
-  for (int64_t i = 0; i < p.n_preshapes; ++i) {
+  for (int64_t i = 0; i < p.n_init_lists; ++i) {
     std::vector<PoseParams> poses;
     for (int64_t k = 0; k < p.init_counts[i]; ++k, ++row) {
       Vec7 v;
@@ -177,6 +177,7 @@ Holder* hold(const GraspProblem& g) {
   for (int a = 0; a < 3; ++a) v.com[a] = g.com[a];
   v.init_poses = h->inits.data();
   v.init_counts = h->counts.data();
+  v.n_init_lists = static_cast<int64_t>(h->counts.size());
   v.learning_rate = g.sgd.learning_rate;
   for (int r = 0; r < 7; ++r)
     for (int c = 0; c < 7; ++c) v.A[7 * r + c] = g.sgd.A(r, c);

@@ -1,0 +1,26 @@
+"""B200-native AS-ICP grasp optimiser (arXiv 2412.08346).
+
+Drop-in for graspmatch::optimize_grasp (proj/include/graspmatch/grasp.hpp:141):
+the CUDA library libasicp.so (csrc/, sm_100a) behind the C-ABI of
+include/asicp.h, with a Python mirror of the reference API in grasp.py.
+"""
+from .grasp import (  # noqa: F401
+    AnnealingSchedule,
+    BandwidthMode,
+    DeviceError,
+    GraspProblem,
+    GraspSolution,
+    GraspStatus,
+    InvalidArgument,
+    ParticlePhase,
+    PosePrior,
+    Preshape,
+    SdfGrid,
+    SgdConfig,
+    Solver,
+    StackedSdf,
+    SteinConfig,
+    annealing,
+    minibatch_schedule,
+    optimize_grasp,
+)

@@ -1,0 +1,739 @@
+// Deterministic synthetic problems (include/asicp_fixtures.h).
+//
+// Host-side C++ (no device code).  The desk scenario reproduces
+// proj/src/synthetic.cpp bit for bit (same std::mt19937_64 streams, same
+// arithmetic order: checked against the reference fixtures in
+// tests/test_fixtures.py); build_sdf follows proj/src/sdf.cpp:48-175 with an
+// exact grid-bucket nearest-neighbour search instead of the kd-tree (the
+// distance is a minimum, so the float values are identical).  The KG3 gripper
+// and the cfg1-3 workloads are new fixtures defined in SURVEY.md §8(d).
+#include "asicp.h"
+#include "asicp_fixtures.h"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <queue>
+#include <random>
+#include <stdexcept>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+namespace {
+
+struct P3 {
+  double x, y, z;
+  double operator[](int a) const { return a == 0 ? x : (a == 1 ? y : z); }
+  double& operator[](int a) { return a == 0 ? x : (a == 1 ? y : z); }
+};
+using Cloud = std::vector<P3>;
+
+double sqn(const P3& a) { return (a.x * a.x + a.y * a.y) + a.z * a.z; }
+P3 sub(const P3& a, const P3& b) { return P3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+
+// graspmatch::Rng (rng.hpp:16-70).
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) : e_(seed) {}
+  uint64_t next_u64() { return e_(); }
+  double uniform01() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform01(); }
+  double normal() {
+    if (have_spare_) {
+      have_spare_ = false;
+      return spare_;
+    }
+    double u1 = uniform01();
+    double u2 = uniform01();
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 2.0 * M_PI * u2;
+    spare_ = r * std::sin(a);
+    have_spare_ = true;
+    return r * std::cos(a);
+  }
+
+ private:
+  std::mt19937_64 e_;
+  bool have_spare_ = false;
+  double spare_ = 0.0;
+};
+
+P3 centroid(const Cloud& c) {
+  P3 s{0.0, 0.0, 0.0};
+  for (const P3& p : c) s = P3{s.x + p.x, s.y + p.y, s.z + p.z};
+  const double n = static_cast<double>(c.size());
+  return P3{s.x / n, s.y / n, s.z / n};
+}
+
+// synthetic.cpp:11-32
+Cloud cylinder_cloud(double radius, double height, int n, uint64_t seed) {
+  Rng rng(seed);
+  const double a_side = 2.0 * M_PI * radius * height;
+  const double a_cap = M_PI * radius * radius;
+  const int n_side = static_cast<int>(n * a_side / (a_side + 2.0 * a_cap));
+  const int n_cap = (n - n_side) / 2;
+  Cloud cloud;
+  cloud.reserve(n);
+  for (int i = 0; i < n_side; ++i) {
+    const double th = rng.uniform(0.0, 2.0 * M_PI);
+    const double z = rng.uniform(0.0, height);
+    cloud.push_back(P3{radius * std::cos(th), radius * std::sin(th), z});
+  }
+  for (double zc : {0.0, height}) {
+    for (int i = 0; i < n_cap; ++i) {
+      const double th = rng.uniform(0.0, 2.0 * M_PI);
+      const double rr = radius * std::sqrt(rng.uniform01());
+      cloud.push_back(P3{rr * std::cos(th), rr * std::sin(th), zc});
+    }
+  }
+  return cloud;
+}
+
+// synthetic.cpp:34-51
+Cloud box_surface_cloud(int n, const P3& half, uint64_t seed) {
+  Rng rng(seed);
+  const double areas[3] = {half.y * half.z, half.x * half.z, half.x * half.y};
+  const double total = (areas[0] + areas[1]) + areas[2];
+  Cloud cloud;
+  for (int i = 0; i < n; ++i) {
+    const double u = rng.uniform01() * total;
+    const int axis = u < areas[0] ? 0 : (u < areas[0] + areas[1] ? 1 : 2);
+    const double sign = rng.uniform01() < 0.5 ? -1.0 : 1.0;
+    P3 p;
+    for (int a = 0; a < 3; ++a) p[a] = rng.uniform(-half[a], half[a]);
+    p[axis] = sign * half[axis];
+    cloud.push_back(p);
+  }
+  return cloud;
+}
+
+// synthetic.cpp:85-91
+Cloud table_cloud(double half_extent = 0.12, double pitch = 0.01, double cutout_radius = 0.035) {
+  Cloud cloud;
+  for (double x = -half_extent; x <= half_extent + 1e-9; x += pitch)
+    for (double y = -half_extent; y <= half_extent + 1e-9; y += pitch)
+      if (std::hypot(x, y) > cutout_radius) cloud.push_back(P3{x, y, 0.0});
+  return cloud;
+}
+
+// geometry.cpp:106-128 voxel_downsample (first-occurrence order).
+struct Key {
+  int64_t x, y, z;
+  bool operator==(const Key& o) const { return x == o.x && y == o.y && z == o.z; }
+};
+struct KeyHash {
+  size_t operator()(const Key& k) const {
+    uint64_t h = 1469598103934665603ull;
+    for (int64_t v : {k.x, k.y, k.z}) {
+      h ^= static_cast<uint64_t>(v);
+      h *= 1099511628211ull;
+    }
+    return static_cast<size_t>(h);
+  }
+};
+Cloud voxel_downsample(const Cloud& cloud, double voxel) {
+  std::unordered_map<Key, size_t, KeyHash> bins;
+  std::vector<P3> sums;
+  std::vector<int> counts;
+  for (const P3& p : cloud) {
+    const Key key{static_cast<int64_t>(std::floor(p.x / voxel)), static_cast<int64_t>(std::floor(p.y / voxel)),
+                  static_cast<int64_t>(std::floor(p.z / voxel))};
+    auto [it, inserted] = bins.try_emplace(key, sums.size());
+    if (inserted) {
+      sums.push_back(p);
+      counts.push_back(1);
+    } else {
+      P3& s = sums[it->second];
+      s = P3{s.x + p.x, s.y + p.y, s.z + p.z};
+      ++counts[it->second];
+    }
+  }
+  Cloud out;
+  for (size_t i = 0; i < sums.size(); ++i) {
+    const double c = counts[i];
+    out.push_back(P3{sums[i].x / c, sums[i].y / c, sums[i].z / c});
+  }
+  return out;
+}
+
+struct Box {
+  P3 lo, hi;
+};
+
+// synthetic.cpp:119-137 (dense face sampling).
+void sample_box_surface(const Box& box, double pitch, Cloud& out) {
+  const P3 size = sub(box.hi, box.lo);
+  for (int axis = 0; axis < 3; ++axis) {
+    const int u = (axis + 1) % 3, v = (axis + 2) % 3;
+    const int nu = std::max(1, static_cast<int>(std::round(size[u] / pitch)));
+    const int nv = std::max(1, static_cast<int>(std::round(size[v] / pitch)));
+    for (double side : {box.lo[axis], box.hi[axis]}) {
+      for (int iu = 0; iu <= nu; ++iu)
+        for (int iv = 0; iv <= nv; ++iv) {
+          P3 p;
+          p[axis] = side;
+          p[u] = box.lo[u] + size[u] * iu / nu;
+          p[v] = box.lo[v] + size[v] * iv / nv;
+          out.push_back(p);
+        }
+    }
+  }
+}
+
+struct Gripper {
+  Cloud inner, full;
+  P3 tcp;
+};
+
+// synthetic.cpp:141-166 two_finger_preshape.
+Gripper two_finger() {
+  constexpr double kGap = 0.068, kThick = 0.012, kWidth = 0.04, kZMin = -0.08, kZMax = 0.02, kPalm = 0.032;
+  const double pitch = 0.005;
+  Gripper g;
+  for (double y : {kGap / 2, -kGap / 2})
+    for (double x = -kWidth / 2 + pitch / 2; x < kWidth / 2; x += pitch)
+      for (double z = kZMin + pitch / 2; z < kZMax; z += pitch) g.inner.push_back(P3{x, y, z});
+  g.inner = voxel_downsample(g.inner, 0.005);
+  const Box boxes[3] = {
+      {P3{-kWidth / 2, kGap / 2, kZMin}, P3{kWidth / 2, kGap / 2 + kThick, kZMax}},
+      {P3{-kWidth / 2, -kGap / 2 - kThick, kZMin}, P3{kWidth / 2, -kGap / 2, kZMax}},
+      {P3{-kWidth / 2, -kGap / 2 - kThick, kZMax}, P3{kWidth / 2, kGap / 2 + kThick, kPalm}},
+  };
+  for (const Box& b : boxes) sample_box_surface(b, 0.002, g.full);
+  g.tcp = centroid(g.inner);
+  return g;
+}
+
+// KG3: three-finger gripper (a thumb on +y opposing two fingers on -y),
+// approach axis -z like the two-finger model; `gap` is the closure (distance
+// between the thumb and finger contact faces).  Contact surface: the inner
+// faces sampled at 2.5 mm (432 + 2 x 288 = 1008 points); collision body: all
+// faces of the four boxes at 2 mm.
+Gripper kg3(double gap) {
+  constexpr double kThick = 0.012, kZMin = -0.09, kZMax = 0.0, kPalm = 0.015;
+  constexpr double kThumbHalf = 0.015, kFingerHalf = 0.01, kFingerX = 0.02;
+  const double pitch = 0.0025;
+  Gripper g;
+  auto face = [&](double x0, double x1, double y) {
+    for (double x = x0 + pitch / 2; x < x1; x += pitch)
+      for (double z = kZMin + pitch / 2; z < kZMax; z += pitch) g.inner.push_back(P3{x, y, z});
+  };
+  face(-kThumbHalf, kThumbHalf, gap / 2);
+  face(-kFingerX - kFingerHalf, -kFingerX + kFingerHalf, -gap / 2);
+  face(kFingerX - kFingerHalf, kFingerX + kFingerHalf, -gap / 2);
+  const Box boxes[4] = {
+      {P3{-kThumbHalf, gap / 2, kZMin}, P3{kThumbHalf, gap / 2 + kThick, kZMax}},
+      {P3{-kFingerX - kFingerHalf, -gap / 2 - kThick, kZMin}, P3{-kFingerX + kFingerHalf, -gap / 2, kZMax}},
+      {P3{kFingerX - kFingerHalf, -gap / 2 - kThick, kZMin}, P3{kFingerX + kFingerHalf, -gap / 2, kZMax}},
+      {P3{-kFingerX - kFingerHalf, -gap / 2 - kThick, kZMax}, P3{kFingerX + kFingerHalf, gap / 2 + kThick, kPalm}},
+  };
+  for (const Box& b : boxes) sample_box_surface(b, 0.002, g.full);
+  g.tcp = centroid(g.inner);
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// build_sdf (sdf.cpp:48-175)
+// ---------------------------------------------------------------------------
+// Exact nearest-neighbour distance over a bucket grid: returns the minimum
+// of the reference's FP64 expression (p - q).squaredNorm() over the cloud.
+class Buckets {
+ public:
+  Buckets(const Cloud& c, double h) : c_(c), h_(h) {
+    lo_ = c.front();
+    P3 hi = c.front();
+    for (const P3& p : c)
+      for (int a = 0; a < 3; ++a) {
+        lo_[a] = std::min(lo_[a], p[a]);
+        hi[a] = std::max(hi[a], p[a]);
+      }
+    for (int a = 0; a < 3; ++a) n_[a] = std::max(1, static_cast<int>(std::floor((hi[a] - lo_[a]) / h_)) + 1);
+    const size_t cells = static_cast<size_t>(n_[0]) * n_[1] * n_[2];
+    start_.assign(cells + 1, 0);
+    std::vector<size_t> cell_of(c.size());
+    for (size_t i = 0; i < c.size(); ++i) {
+      cell_of[i] = cell_index(c[i]);
+      ++start_[cell_of[i] + 1];
+    }
+    for (size_t k = 0; k < cells; ++k) start_[k + 1] += start_[k];
+    items_.resize(c.size());
+    std::vector<size_t> fill(start_.begin(), start_.end() - 1);
+    for (size_t i = 0; i < c.size(); ++i) items_[fill[cell_of[i]]++] = static_cast<uint32_t>(i);
+  }
+  double nearest_d2(const P3& q) const {
+    int qc[3];
+    for (int a = 0; a < 3; ++a) qc[a] = static_cast<int>(std::floor((q[a] - lo_[a]) / h_));
+    int rmax = 0;
+    for (int a = 0; a < 3; ++a) rmax = std::max({rmax, std::abs(qc[a]), std::abs(qc[a] - (n_[a] - 1))});
+    double best = std::numeric_limits<double>::infinity();
+    for (int r = 0; r <= rmax + 1; ++r) {
+      if (r >= 2) {
+        const double bound = (r - 1) * h_;
+        if (best < bound * bound * (1.0 - 1e-9)) break;
+      }
+      for (int dx = -r; dx <= r; ++dx) {
+        const int x = qc[0] + dx;
+        if (x < 0 || x >= n_[0]) continue;
+        for (int dy = -r; dy <= r; ++dy) {
+          const int y = qc[1] + dy;
+          if (y < 0 || y >= n_[1]) continue;
+          const bool edge_xy = std::abs(dx) == r || std::abs(dy) == r;
+          for (int dz = -r; dz <= r; ++dz) {
+            if (!edge_xy && std::abs(dz) != r) continue;
+            const int z = qc[2] + dz;
+            if (z < 0 || z >= n_[2]) continue;
+            const size_t cell = (static_cast<size_t>(x) * n_[1] + y) * n_[2] + z;
+            for (size_t k = start_[cell]; k < start_[cell + 1]; ++k) {
+              const double d2 = sqn(sub(c_[items_[k]], q));
+              if (d2 < best) best = d2;
+            }
+          }
+        }
+      }
+    }
+    return best;
+  }
+
+ private:
+  size_t cell_index(const P3& p) const {
+    int ci[3];
+    for (int a = 0; a < 3; ++a)
+      ci[a] = std::clamp(static_cast<int>(std::floor((p[a] - lo_[a]) / h_)), 0, n_[a] - 1);
+    return (static_cast<size_t>(ci[0]) * n_[1] + ci[1]) * n_[2] + ci[2];
+  }
+  const Cloud& c_;
+  double h_;
+  P3 lo_;
+  int n_[3];
+  std::vector<size_t> start_;
+  std::vector<uint32_t> items_;
+};
+
+struct Sdf {
+  P3 origin;
+  double voxel = 0.0;
+  int32_t dims[3] = {0, 0, 0};
+  std::vector<float> values;
+  double boundary_max_abs = 0.0;
+};
+
+// sdf.cpp:21-35 sample_spacing (95th percentile NN spacing on a subsample).
+double sample_spacing(const Cloud& cloud) {
+  std::vector<double> nn;
+  const size_t stride = std::max<size_t>(1, cloud.size() / 512);
+  for (size_t i = 0; i < cloud.size(); i += stride) {
+    double best = std::numeric_limits<double>::infinity();
+    for (size_t j = 0; j < cloud.size(); ++j) {
+      if (j == i) continue;
+      best = std::min(best, sqn(sub(cloud[i], cloud[j])));
+    }
+    nn.push_back(std::sqrt(best));
+  }
+  std::sort(nn.begin(), nn.end());
+  return nn.empty() ? 0.0 : nn[static_cast<size_t>(0.95 * (nn.size() - 1))];
+}
+
+Sdf build_sdf(const Cloud& cloud, double voxel, double padding_opt = -1.0, double band = 0.003) {
+  if (!(voxel > 0.0)) throw std::invalid_argument("build_sdf: voxel must be positive");
+  if (cloud.size() < 4) throw std::invalid_argument("build_sdf: need >= 4 non-coplanar points");
+  const double padding = padding_opt >= 0.0 ? padding_opt : 4.0 * voxel;
+  P3 lo = cloud.front(), hi = cloud.front();
+  for (const P3& p : cloud)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = p[a] < lo[a] ? p[a] : lo[a];
+      hi[a] = hi[a] < p[a] ? p[a] : hi[a];
+    }
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = lo[a] - padding;
+    hi[a] = hi[a] + padding;
+  }
+  Sdf g;
+  g.origin = lo;
+  g.voxel = voxel;
+  for (int a = 0; a < 3; ++a) g.dims[a] = static_cast<int32_t>(std::ceil((hi[a] - lo[a]) / voxel)) + 1;
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+  const size_t total = static_cast<size_t>(nx) * ny * nz;
+  g.values.resize(total);
+  const double spacing = sample_spacing(cloud);
+  const double closure = 1.05 * std::sqrt(0.25 * voxel * voxel + 0.5 * spacing * spacing);
+  const double skin = std::max(band, closure);
+  const Buckets buckets(cloud, std::max(voxel, 2.0 * spacing));
+  std::vector<float> dist(total);
+  auto node_index = [&](int ix, int iy, int iz) { return (static_cast<size_t>(ix) * ny + iy) * nz + iz; };
+  for (int ix = 0; ix < nx; ++ix)
+    for (int iy = 0; iy < ny; ++iy)
+      for (int iz = 0; iz < nz; ++iz) {
+        const P3 q{g.origin.x + voxel * static_cast<double>(ix), g.origin.y + voxel * static_cast<double>(iy),
+                   g.origin.z + voxel * static_cast<double>(iz)};
+        dist[node_index(ix, iy, iz)] = static_cast<float>(std::sqrt(buckets.nearest_d2(q)));
+      }
+  // Widest-path clearance from the boundary (sdf.cpp:96-142); the max-min
+  // value is unique, so any correct processing order yields the same floats.
+  std::vector<float> clearance(total, 0.0f);
+  std::priority_queue<std::pair<float, size_t>> heap;
+  auto seed = [&](int ix, int iy, int iz) {
+    const size_t id = node_index(ix, iy, iz);
+    if (clearance[id] < dist[id]) {
+      clearance[id] = dist[id];
+      heap.emplace(clearance[id], id);
+    }
+  };
+  for (int ix = 0; ix < nx; ++ix)
+    for (int iy = 0; iy < ny; ++iy) {
+      seed(ix, iy, 0);
+      seed(ix, iy, nz - 1);
+    }
+  for (int ix = 0; ix < nx; ++ix)
+    for (int iz = 0; iz < nz; ++iz) {
+      seed(ix, 0, iz);
+      seed(ix, ny - 1, iz);
+    }
+  for (int iy = 0; iy < ny; ++iy)
+    for (int iz = 0; iz < nz; ++iz) {
+      seed(0, iy, iz);
+      seed(nx - 1, iy, iz);
+    }
+  while (!heap.empty()) {
+    const auto [c, id] = heap.top();
+    heap.pop();
+    if (c < clearance[id]) continue;
+    const int iz = static_cast<int>(id % nz);
+    const int iy = static_cast<int>((id / nz) % ny);
+    const int ix = static_cast<int>(id / (static_cast<size_t>(ny) * nz));
+    const int nb[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+    for (const auto& d : nb) {
+      const int jx = ix + d[0], jy = iy + d[1], jz = iz + d[2];
+      if (jx < 0 || jy < 0 || jz < 0 || jx >= nx || jy >= ny || jz >= nz) continue;
+      const size_t jd = node_index(jx, jy, jz);
+      const float cand = std::min(c, dist[jd]);
+      if (cand > clearance[jd]) {
+        clearance[jd] = cand;
+        heap.emplace(cand, jd);
+      }
+    }
+  }
+  constexpr float kEscapeRatio = 0.9f;
+  for (size_t id = 0; id < total; ++id) {
+    const bool exterior = clearance[id] >= kEscapeRatio * dist[id];
+    g.values[id] = exterior ? -dist[id] : dist[id] - static_cast<float>(skin);
+  }
+  double boundary_max = 0.0;
+  for (int ix = 0; ix < nx; ++ix)
+    for (int iy = 0; iy < ny; ++iy)
+      for (int iz = 0; iz < nz; ++iz) {
+        if (ix != 0 && iy != 0 && iz != 0 && ix != nx - 1 && iy != ny - 1 && iz != nz - 1) continue;
+        boundary_max = std::max(boundary_max, std::abs(static_cast<double>(g.values[node_index(ix, iy, iz)])));
+      }
+  g.boundary_max_abs = boundary_max;
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// Pose initialisers (geometry.cpp:132-181)
+// ---------------------------------------------------------------------------
+using Pose = std::array<double, 7>;
+
+void normalize4(double q[4]) {
+  const double n = std::sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+  for (int i = 0; i < 4; ++i) q[i] = q[i] / n;
+}
+
+// shortest_arc(a, b) (geometry.cpp:132-142)
+void shortest_arc(const P3& a, const P3& b, double q[4]) {
+  const P3 c{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+  const double d = (a.x * b.x + a.y * b.y) + a.z * b.z;
+  if (d < -1.0 + 1e-12) {
+    P3 axis{a.y * 0.0 - a.z * 0.0, a.z * 1.0 - a.x * 0.0, a.x * 0.0 - a.y * 1.0};
+    if (std::sqrt(sqn(axis)) < 1e-6) axis = P3{a.y * 0.0 - a.z * 1.0, a.z * 0.0 - a.x * 0.0, a.x * 1.0 - a.y * 0.0};
+    const double n = std::sqrt(sqn(axis));
+    q[0] = 0.0;
+    q[1] = axis.x / n;
+    q[2] = axis.y / n;
+    q[3] = axis.z / n;
+    return;
+  }
+  q[0] = 1.0 + d;
+  q[1] = c.x;
+  q[2] = c.y;
+  q[3] = c.z;
+  normalize4(q);
+}
+
+std::vector<Pose> fibonacci_quarter_sphere(int n, double radius, const P3& center) {
+  const double golden = (std::sqrt(5.0) - 1.0) / 2.0;
+  std::vector<Pose> poses;
+  for (int i = 0; i < n; ++i) {
+    const double z = 1.0 - (i + 0.5) / n;
+    const double phi = -M_PI / 2.0 + M_PI * std::fmod(i * golden, 1.0);
+    const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    const P3 dir{r * std::cos(phi), r * std::sin(phi), z};
+    Pose p;
+    p[0] = center.x + radius * dir.x;
+    p[1] = center.y + radius * dir.y;
+    p[2] = center.z + radius * dir.z;
+    double q[4];
+    shortest_arc(P3{0.0, 0.0, -1.0}, P3{-dir.x, -dir.y, -dir.z}, q);
+    for (int a = 0; a < 4; ++a) p[3 + a] = q[a];
+    poses.push_back(p);
+  }
+  return poses;
+}
+
+std::vector<Pose> top_down_ring(int n, double radius, const P3& center) {
+  std::vector<Pose> poses;
+  for (int k = 0; k < n; ++k) {
+    const double a = 2.0 * M_PI * k / std::max(1, n);
+    Pose p;
+    p[0] = center.x + radius * 0.0;
+    p[1] = center.y + radius * 0.0;
+    p[2] = center.z + radius * 1.0;
+    p[3] = std::cos(a / 2.0);
+    p[4] = 0.0;
+    p[5] = 0.0;
+    p[6] = std::sin(a / 2.0);
+    poses.push_back(p);
+  }
+  return poses;
+}
+
+// io.cpp:582-591 make_initializations (fibonacci mode).
+std::vector<Pose> fib_inits(size_t count, size_t top_down, double radius, const P3& com) {
+  const size_t top = std::min(top_down, count);
+  std::vector<Pose> poses = fibonacci_quarter_sphere(static_cast<int>(count - top), radius, com);
+  const auto ring = top_down_ring(static_cast<int>(top), radius, com);
+  poses.insert(poses.end(), ring.begin(), ring.end());
+  return poses;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Owning problem + asicp_problem view
+// ---------------------------------------------------------------------------
+struct asicp_fixture {
+  std::vector<double> object, scene, inits;
+  std::vector<std::vector<double>> surf, full;
+  std::vector<Sdf> sdfs;
+  std::vector<int64_t> counts;
+  std::vector<asicp_preshape> pre;
+  std::vector<asicp_sdf_grid> grids;
+  asicp_problem view{};
+};
+
+namespace {
+
+std::vector<double> flat(const Cloud& c) {
+  std::vector<double> out;
+  out.reserve(3 * c.size());
+  for (const P3& p : c) {
+    out.push_back(p.x);
+    out.push_back(p.y);
+    out.push_back(p.z);
+  }
+  return out;
+}
+
+struct Spec {
+  Cloud object, scene;
+  P3 com;
+  std::vector<Gripper> grippers;
+  std::vector<double> voxels;
+  double stack_eps = 0.05;
+  std::vector<std::vector<Pose>> inits;
+  int64_t k_stein = 15, k_max = 40;
+  double conv = 0.0002;
+  uint64_t seed = 0;
+  double contact_tolerance = 0.0;
+};
+
+asicp_fixture* assemble(const Spec& s) {
+  auto* f = new asicp_fixture();
+  f->object = flat(s.object);
+  f->scene = flat(s.scene);
+  double max_diag = 0.0;
+  for (size_t i = 0; i < s.grippers.size(); ++i) {
+    f->surf.push_back(flat(s.grippers[i].inner));
+    f->full.push_back(flat(s.grippers[i].full));
+    f->sdfs.push_back(build_sdf(s.grippers[i].full, s.voxels[i]));
+    const Sdf& g = f->sdfs.back();
+    // stack_preshapes (sdf.cpp:205-218): (max_corner - origin).norm()
+    P3 d;
+    for (int a = 0; a < 3; ++a) d[a] = (g.origin[a] + g.voxel * static_cast<double>(g.dims[a] - 1)) - g.origin[a];
+    max_diag = std::max(max_diag, std::sqrt(sqn(d)));
+  }
+  for (size_t i = 0; i < s.grippers.size(); ++i) {
+    asicp_preshape p{};
+    p.inner_surface = f->surf[i].data();
+    p.n_surface = static_cast<int64_t>(s.grippers[i].inner.size());
+    p.full_cloud = f->full[i].data();
+    p.n_full = static_cast<int64_t>(s.grippers[i].full.size());
+    p.tcp[0] = s.grippers[i].tcp.x;
+    p.tcp[1] = s.grippers[i].tcp.y;
+    p.tcp[2] = s.grippers[i].tcp.z;
+    p.sdf_index = static_cast<int64_t>(i);
+    f->pre.push_back(p);
+    const Sdf& g = f->sdfs[i];
+    asicp_sdf_grid gr{};
+    for (int a = 0; a < 3; ++a) {
+      gr.dims[a] = g.dims[a];
+      gr.origin[a] = g.origin[a];
+    }
+    gr.offset[0] = static_cast<double>(i) * (max_diag + s.stack_eps);
+    gr.offset[1] = 0.0;
+    gr.offset[2] = 0.0;
+    gr.voxel = g.voxel;
+    gr.boundary_max_abs = g.boundary_max_abs;
+    gr.values = g.values.data();
+    f->grids.push_back(gr);
+  }
+  for (const auto& list : s.inits) {
+    f->counts.push_back(static_cast<int64_t>(list.size()));
+    for (const Pose& p : list) f->inits.insert(f->inits.end(), p.begin(), p.end());
+  }
+  asicp_problem& v = f->view;
+  v.object_cloud = f->object.data();
+  v.n_object = static_cast<int64_t>(s.object.size());
+  v.scene_cloud = f->scene.data();
+  v.n_scene = static_cast<int64_t>(s.scene.size());
+  v.preshapes = f->pre.data();
+  v.n_preshapes = static_cast<int64_t>(f->pre.size());
+  v.sdf_grids = f->grids.data();
+  v.n_sdf_grids = static_cast<int64_t>(f->grids.size());
+  v.com[0] = s.com.x;
+  v.com[1] = s.com.y;
+  v.com[2] = s.com.z;
+  v.init_poses = f->inits.data();
+  v.init_counts = f->counts.data();
+  v.n_init_lists = static_cast<int64_t>(f->counts.size());
+  v.learning_rate = 1.0;
+  for (int i = 0; i < 49; ++i) v.A[i] = (i % 8 == 0) ? 1.0 : 0.0;
+  v.convergence_threshold = s.conv;
+  v.bandwidth_mode = ASICP_BANDWIDTH_MEDIAN;
+  v.fixed_bandwidth = 1.0;
+  for (int a = 0; a < 3; ++a) {
+    v.prior_t_mean[a] = 0.0;
+    v.prior_t_sigma[a] = 1.0;
+  }
+  v.prior_q_location[0] = 1.0;
+  for (int a = 1; a < 4; ++a) v.prior_q_location[a] = 0.0;
+  for (int a = 0; a < 4; ++a) v.prior_q_kappa[a] = 0.0;
+  v.anneal_period_total = s.k_max;
+  v.anneal_cycles = 5;
+  v.anneal_exponent = 2.0;
+  v.step_scale = 1.0;
+  v.k_stein = s.k_stein;
+  v.k_max = s.k_max;
+  v.contact_tolerance = s.contact_tolerance;
+  v.seed = s.seed;
+  v.workers = 0;
+  v.record_trace = 0;
+  return f;
+}
+
+Cloud with_table(const Cloud& object) {
+  Cloud scene = object;
+  const Cloud table = table_cloud();
+  scene.insert(scene.end(), table.begin(), table.end());
+  return scene;
+}
+
+// Voxel such that the largest padded grid axis has 64 nodes:
+// ceil(E / v) + 8 + 1 = 64 with 4-voxel padding on both sides.
+double voxel_for_64(const Cloud& full) {
+  P3 lo = full.front(), hi = full.front();
+  for (const P3& p : full)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], p[a]);
+      hi[a] = std::max(hi[a], p[a]);
+    }
+  double e = 0.0;
+  for (int a = 0; a < 3; ++a) e = std::max(e, hi[a] - lo[a]);
+  return e / 54.5;
+}
+
+}  // namespace
+
+extern "C" {
+
+asicp_fixture* asicp_fx_desk(uint64_t seed, int64_t n_init, int64_t n_top) {
+  Spec s;
+  s.object = cylinder_cloud(0.03, 0.12, 1500, 1);
+  s.com = centroid(s.object);
+  s.scene = with_table(s.object);
+  s.grippers = {two_finger()};
+  s.voxels = {0.005};
+  auto poses = fibonacci_quarter_sphere(static_cast<int>(n_init - n_top), 0.25, s.com);
+  const auto top = top_down_ring(static_cast<int>(n_top), 0.25, s.com);
+  poses.insert(poses.end(), top.begin(), top.end());
+  s.inits = {poses};
+  s.k_stein = 15;
+  s.k_max = 40;
+  s.seed = seed;
+  return assemble(s);
+}
+
+asicp_fixture* asicp_fx_config(int cfg, uint64_t seed, int64_t ppp, int64_t n_object) {
+  Spec s;
+  s.seed = seed;
+  if (cfg == 1) {
+    s.object = cylinder_cloud(0.03, 0.12, n_object > 0 ? static_cast<int>(n_object) : 2000, 1);
+    s.com = centroid(s.object);
+    s.scene = with_table(s.object);
+    s.grippers = {kg3(0.08)};
+    s.voxels = {0.005};
+    const size_t count = ppp > 0 ? static_cast<size_t>(ppp) : 64;
+    s.inits = {fib_inits(count, 6, 0.25, s.com)};
+    s.k_stein = 15;
+    s.k_max = 50;
+  } else if (cfg == 2) {
+    s.object = cylinder_cloud(0.04, 0.15, n_object > 0 ? static_cast<int>(n_object) : 10000, 1);
+    s.com = centroid(s.object);
+    s.scene = with_table(s.object);
+    const double gaps[3] = {0.09, 0.10, 0.11};
+    const size_t count = ppp > 0 ? static_cast<size_t>(ppp) : 256;
+    for (double gap : gaps) {
+      s.grippers.push_back(kg3(gap));
+      s.voxels.push_back(voxel_for_64(s.grippers.back().full));
+      s.inits.push_back(fib_inits(count, 6, 0.25, s.com));
+    }
+    s.k_stein = 38;
+    s.k_max = 100;
+  } else {
+    return nullptr;
+  }
+  return assemble(s);
+}
+
+asicp_problem* asicp_fx_view(asicp_fixture* fx) { return fx ? &fx->view : nullptr; }
+void asicp_fx_free(asicp_fixture* fx) { delete fx; }
+
+void asicp_fx_cylinder_cloud(double radius, double height, int n, uint64_t seed, double* out) {
+  const Cloud c = cylinder_cloud(radius, height, n, seed);
+  for (size_t i = 0; i < c.size(); ++i) {
+    out[3 * i] = c[i].x;
+    out[3 * i + 1] = c[i].y;
+    out[3 * i + 2] = c[i].z;
+  }
+}
+
+int64_t asicp_fx_build_sdf(const double* cloud, int64_t n, double voxel, double padding, double band, int32_t* dims,
+                           double* meta, float* values) {
+  Cloud c(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) c[i] = P3{cloud[3 * i], cloud[3 * i + 1], cloud[3 * i + 2]};
+  const Sdf g = build_sdf(c, voxel, padding, band);
+  for (int a = 0; a < 3; ++a) {
+    dims[a] = g.dims[a];
+    meta[a] = g.origin[a];
+  }
+  meta[3] = g.voxel;
+  meta[4] = g.boundary_max_abs;
+  if (values) std::memcpy(values, g.values.data(), g.values.size() * sizeof(float));
+  return static_cast<int64_t>(g.values.size());
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Device-side problem / state layout of the B200 AS-ICP solver and the host
+// launchers of its kernels (kernels.cu).  See DESIGN.md §3 for the HBM layout.
+#pragma once
+
+#include "dmath.cuh"
+#include "nn.cuh"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace asicp {
+
+// Read-only problem data (uploaded once per asicp_prepare).
+struct DevProblem {
+  int J;            // particles (all preshapes, preshape-major)
+  int n_obj;        // |R|
+  int n_scene;      // |C|
+  int n_pop;        // Stein populations (= preshapes)
+  const double* obj64;      // R, n_obj x 3
+  const float4* obj_cand;   // R as FP32 NN candidates (-2b, |b|^2), b = r - center
+  const double* scene64;    // C, n_scene x 3
+  const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
+  const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
+  const double* pre_tcp;    // preshape tcp, 3 per preshape
+  const int* pre_sdf;       // preshape -> grid index
+  const Grid* grids;
+  const float* sdf_values;
+  const int* part_pre;      // particle -> preshape
+  const int64_t* part_surf_off;  // particle -> offset of its surface rows (J + 1)
+  const int* part_pop;      // particle -> population
+  const int* pop_off;       // population -> first particle (n_pop + 1)
+  const double* pop_logk1;  // log(K + 1) per population (host std::log)
+  double center[3];         // FP32 re-centring origin (object centroid)
+  double B_obj;             // max |r - center| over R (with slack)
+  double com[3];
+  double contact_tolerance;
+  double prior_t_mean[3];
+  double prior_t_sigma[3];
+  double prior_q_location[4];
+  double prior_q_kappa[4];
+  int bandwidth_mode;
+  double fixed_bandwidth;
+  double A[49];
+  double lr;
+  double conv_thr;
+};
+
+// Mutable solver state (device pointers).
+struct DevState {
+  double* theta;       // J x 7
+  double* theta_next;  // J x 7 (SVGD double buffer)
+  double* loss;
+  double* prev_loss;
+  int* in_col;
+  int* converged;
+  int* active;
+  int* n_col;
+  double* grad;        // J x 7 likelihood gradient
+  double* prior;       // J x 7 prior log-gradient
+  double* drift;       // J x 7
+  double* h;           // per population bandwidth
+  double* S64;         // transformed contact surface, sum_j N_s(j) x 3
+  float4* Sq32;        // its FP32 queries (x, y, z, margin)
+  float4* Sc32;        // its FP32 candidates (-2x, -2y, -2z, |b|^2)
+  double* Bs;          // per particle max |s - center|
+  int* col_idx;        // J x n_scene colliding scene indices (scene order)
+  float4* col_q;       // J x n_scene FP32 reverse queries
+  int* res_fwd;        // per surface row: NN position in the candidate set
+  int* res_rev;        // J x n_scene: nearest surface index per colliding point
+  uint64_t* rng_state; // J x 312
+  int* rng_mti;        // J
+  int* pool_idx;       // J x n_obj minibatch object indices (sample order)
+  float4* pool32;      // J x n_obj gathered FP32 candidates
+  int* fy_scratch;     // J x n_obj Fisher-Yates scratch (large clouds only)
+  const int* pool_map; // = pool_idx when this iteration's forward match is pooled
+  NnItem* items;
+  int* item_count;     // J + 1
+  int* item_off;       // J + 1
+  int* item_counter;
+  void* scan_tmp;
+  size_t scan_tmp_bytes;
+  NnPartial* partials; // sum_j N_s(j) x max chunks
+  int4* refine_list;
+  int* refine_count;
+  int refine_cap;
+  unsigned long long* stats;  // [0] windows > 1, [1] full refines, [2] queries, [3] canonical-order ties
+  double* trace_theta;
+  double* trace_loss;
+  int* trace_col;
+  double* final_loss;
+  int* final_free;
+};
+
+struct NnPlan {
+  int kind;      // 0 iteration match, 2 final ranking
+  int pooled;    // forward candidates are the particle's minibatch pool
+  int m;         // forward candidate count
+  int nchunks;   // forward candidate chunks (split-K)
+  int chunk;     // candidates per chunk (multiple of kNnTile)
+  int fp64_mode; // resolve every query by FP64 brute force (validation mode)
+};
+
+void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st);
+void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
+void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);
+void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);
+void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
+int minibatch_smem_cap();
+void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st);
+size_t scan_temp_bytes(int n);
+int nn_smem_bytes();
+void nn_set_attrs();
+int nn_blocks_per_sm();
+void launch_nn_filter(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st);
+void launch_nn_merge(const DevProblem& P, DevState& S, const NnPlan& plan, int max_ns, cudaStream_t st);
+void launch_nn_refine(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st);
+void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
+void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
+void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, cudaStream_t st);
+void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
+void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
+
+}  // namespace asicp

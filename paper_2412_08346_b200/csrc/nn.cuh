@@ -1,0 +1,57 @@
+// Certified brute-force nearest-neighbour search (the hot loop of
+// optimize_grasp: match_surface_to_pool grasp.cpp:92-106 /
+// collision_loss_and_gradients grasp.cpp:68-84 / final ranking
+// grasp.cpp:263-281, replacing the kd-tree of spatial_index.cpp:14-105).
+//
+// FP32 filter, FP64 decision:
+//   * candidates are staged tile by tile into shared memory with TMA bulk
+//     copies (cp.async.bulk + mbarrier, 4-stage ring); every thread reads each
+//     candidate with one broadcast LDS.128;
+//   * each thread owns Q queries in registers; a (query, candidate) pair costs
+//     3 FFMA in the expansion form d = |b|^2 - 2 a.b (a, b re-centred at the
+//     object centroid) plus one FSETP against the query's running threshold;
+//   * the threshold is b1 + margin, where margin = 2E bounds the FP32 error of
+//     d (see DESIGN.md §NN certification); every candidate within the margin of
+//     the running minimum is kept in a per-query window list (shared memory);
+//   * the reference's answer (min FP64 (p - q).squaredNorm(), ties -> lowest
+//     position, spatial_index.cpp:70,83) is provably inside that window, so a
+//     window of one is certified and larger windows are decided in FP64 with
+//     the reference formula.  Overflowing windows fall back to a full FP64
+//     rescan.
+#pragma once
+
+#include <cstdint>
+
+namespace asicp {
+
+constexpr int kNnThreads = 128;
+constexpr int kNnQ = 8;                         // queries per thread
+constexpr int kNnQB = kNnThreads * kNnQ;        // queries per work item
+constexpr int kNnTile = 256;                    // candidates per TMA tile (4 KB)
+constexpr int kNnStages = 4;
+constexpr int kNnL = 4;                         // window list entries per query
+
+// One NN work item: a block of <= kNnQB queries against a contiguous
+// candidate chunk.
+struct NnItem {
+  const float4* q;   // queries (x, y, z, margin), re-centred FP32
+  const float4* c;   // candidates (-2x, -2y, -2z, |b|^2)
+  int nq;
+  int nc;
+  int c_base;        // position of c[0] in the full candidate set
+  int kind;          // 0 forward, 1 reverse, 2 final
+  int owner;         // particle index
+  int q_first;       // index of q[0] in the kind's query numbering
+  int chunk;         // chunk index (0..S-1)
+  int nchunks;       // S
+};
+
+// Per (query, chunk) partial window.
+struct NnPartial {
+  float b1;
+  int count;         // entries kept; -1 = window overflowed
+  int pos[kNnL];
+  float d[kNnL];
+};
+
+}  // namespace asicp

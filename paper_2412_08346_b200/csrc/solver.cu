@@ -1,0 +1,767 @@
+// Host orchestration of the B200 AS-ICP solver and the C-ABI (include/asicp.h).
+//
+// asicp_prepare mirrors GraspProblem::validate (grasp.cpp:20-31) and the
+// requires the reference raises inside its loop, then uploads the problem;
+// asicp_run replays optimize_grasp (grasp.cpp:132-307) as a fixed sequence
+// of kernels per iteration (optionally captured once into a CUDA graph:
+// every size that varies with k — the minibatch ramp m(k), the annealing
+// gamma(k), the phase — is a host-side function of k, and every data-
+// dependent branch is resolved on the device through work lists).
+#include "asicp.h"
+#include "kernels.cuh"
+#include "mt64.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+using namespace asicp;
+
+struct InvalidArgument : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void require(bool cond, const char* msg) {
+  if (!cond) throw InvalidArgument(msg);
+}
+
+#define CUDA_OK(expr)                                                                             \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw DeviceError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " @" + __FILE__ + \
+                        ":" + std::to_string(__LINE__));                                          \
+  } while (0)
+
+void copy_err(const std::string& msg, char* err, size_t errlen) {
+  if (err && errlen) {
+    std::strncpy(err, msg.c_str(), errlen - 1);
+    err[errlen - 1] = '\0';
+  }
+}
+
+// spatial_index.cpp:133-139
+int64_t minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
+  const double saturation = 2.0 * static_cast<double>(k_max) / 3.0;
+  const double ramp = std::min(static_cast<double>(k), saturation) / saturation;
+  const auto m = static_cast<int64_t>(std::llround(static_cast<double>(n_ref) * ramp));
+  return std::clamp<int64_t>(m, 1, n_ref);
+}
+
+// optim.cpp:158-164
+double annealing(int64_t t, int64_t T, int64_t C, double p) {
+  const double period = static_cast<double>(T) / static_cast<double>(C);
+  const double phase = std::fmod(static_cast<double>(t), period) / period;
+  return std::pow(phase, p);
+}
+
+// A device allocation that grows on demand.
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (n == 0) return;
+    CUDA_OK(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct asicp_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nn_mode = 0;
+  int use_graph = 1;
+  int profile = 0;
+  int num_sms = 148;
+  int nn_grid = 296;
+
+  // Prepared problem (host side).
+  bool prepared = false;
+  int J = 0, n_obj = 0, n_scene = 0, n_pre = 0, k_max = 0, k_stein = 0;
+  int max_ns = 0;
+  int64_t total_surf = 0;
+  int record_trace = 0;
+  double n_ref = 0, eta_stein = 0;
+  std::vector<double> gammas;
+  std::vector<int64_t> ms;
+  std::vector<int> part_pre;
+  std::vector<double> init_theta;
+  uint64_t seed = 0;
+  int nchunks_max = 1;
+
+  DevProblem P{};
+  DevState S{};
+
+  // Device buffers.
+  Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
+      part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d;
+  Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
+      Bs, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items, item_count,
+      item_off, item_counter, scan_tmp, partials, refine_list, refine_count, stats, trace_theta, trace_loss, trace_col,
+      final_loss, final_free;
+
+  cudaGraphExec_t graph_exec = nullptr;
+  bool graph_valid = false;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> nn_events;
+  asicp_stats last_stats{};
+  double nn_pairs_planned = 0.0;
+  int64_t launches = 0;
+
+  ~asicp_ctx() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    for (auto& e : nn_events) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    Buf* all[] = {&obj64, &obj_cand, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
+                  &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d, &theta,
+                  &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
+                  &S64, &Sq32, &Sc32, &Bs, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
+                  &pool_idx, &pool32, &fy_scratch, &items, &item_count, &item_off, &item_counter, &scan_tmp,
+                  &partials, &refine_list, &refine_count, &stats, &trace_theta, &trace_loss, &trace_col,
+                  &final_loss, &final_free};
+    for (Buf* b : all) b->release();
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+template <typename T>
+void upload(Buf& b, const T* src, size_t n, cudaStream_t st) {
+  b.ensure(std::max<size_t>(n, 1) * sizeof(T));
+  if (n) CUDA_OK(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+}
+
+// GraspProblem::validate (grasp.cpp:20-31) + Preshape::validate (:13-18),
+// then the requires the reference hits inside its first iteration.
+void validate(const asicp_problem& p) {
+  require(p.n_object > 0, "GraspProblem: empty object cloud");
+  require(p.n_scene > 0, "GraspProblem: empty scene cloud");
+  require(p.n_preshapes > 0, "GraspProblem: no preshapes");
+  require(p.n_init_lists == p.n_preshapes, "GraspProblem: one initialization list per preshape required");
+  require(p.k_stein <= p.k_max, "GraspProblem: k_stein must not exceed k_max");
+  for (int64_t i = 0; i < p.n_preshapes; ++i) {
+    const asicp_preshape& s = p.preshapes[i];
+    require(s.n_surface > 0, "Preshape: empty inner surface cloud");
+    require(s.n_full > 0, "Preshape: empty full cloud");
+    // tool_centre_point = centroid (geometry.cpp:86-96): sum in order, / n.
+    double c[3] = {0.0, 0.0, 0.0};
+    for (int64_t k = 0; k < s.n_surface; ++k)
+      for (int a = 0; a < 3; ++a) c[a] = c[a] + s.inner_surface[3 * k + a];
+    double d[3];
+    for (int a = 0; a < 3; ++a) d[a] = s.tcp[a] - c[a] / static_cast<double>(s.n_surface);
+    require(std::sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2]) <= 1e-9,
+            "Preshape: tcp must be the contact-surface centroid");
+    require(s.sdf_index >= 0 && s.sdf_index < p.n_sdf_grids, "GraspProblem: preshape sdf_index out of range");
+  }
+  int64_t J = 0;
+  for (int64_t i = 0; i < p.n_init_lists; ++i) J += p.init_counts[i];
+  require(J >= 1, "optimize_grasp: no initial poses");
+  // First evaluation of particle 0 (grasp.cpp:171-194): unit quaternion
+  // (geometry.cpp:19), then the prior (optim.cpp:150); then the others.
+  auto unit_ok = [&](int64_t j) {
+    const double* q = p.init_poses + 7 * j + 3;
+    const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    return std::abs(std::sqrt(n2) - 1.0) <= 1e-6;
+  };
+  if (p.k_max > 0) {
+    require(unit_ok(0), "rotation_matrix: quaternion is not unit-norm");
+    for (int a = 0; a < 3; ++a)
+      require(p.prior_t_sigma[a] * p.prior_t_sigma[a] > 0.0, "prior_log_gradient: t_sigma must be positive");
+    for (int64_t j = 1; j < J; ++j) require(unit_ok(j), "rotation_matrix: quaternion is not unit-norm");
+    if (p.k_stein > 0) {
+      require(p.anneal_cycles >= 1 && p.anneal_period_total >= p.anneal_cycles, "annealing: need T >= C >= 1");
+      require(p.anneal_exponent > 0.0, "annealing: exponent must be positive");
+      bool coupled = false;
+      for (int64_t i = 0; i < p.n_init_lists; ++i) coupled = coupled || p.init_counts[i] >= 2;
+      if (coupled && p.bandwidth_mode == ASICP_BANDWIDTH_FIXED)
+        require(p.fixed_bandwidth > 0.0, "rbf_kernel: bandwidth must be positive");
+    }
+  } else {
+    // Final ranking still transforms every particle (grasp.cpp:271-277).
+    for (int64_t j = 0; j < J; ++j) require(unit_ok(j), "rotation_matrix: quaternion is not unit-norm");
+  }
+  for (int64_t g = 0; g < p.n_sdf_grids; ++g)
+    for (int a = 0; a < 3; ++a) require(p.sdf_grids[g].dims[a] >= 2, "asicp: SDF grid needs >= 2 nodes per axis");
+  require(p.n_object < (1ll << 30) && p.n_scene < (1ll << 30), "asicp: cloud too large");
+}
+
+void prepare(asicp_ctx* c, const asicp_problem& p) {
+  validate(p);
+  CUDA_OK(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  if (c->graph_exec) {
+    cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+  }
+  c->graph_valid = false;
+  const int n_pre = static_cast<int>(p.n_preshapes);
+  c->n_pre = n_pre;
+  c->n_obj = static_cast<int>(p.n_object);
+  c->n_scene = static_cast<int>(p.n_scene);
+  c->k_max = static_cast<int>(p.k_max);
+  c->k_stein = static_cast<int>(p.k_stein);
+  c->record_trace = p.record_trace ? 1 : 0;
+  c->seed = p.seed;
+  c->n_ref = static_cast<double>(p.n_object);
+  c->eta_stein = p.step_scale / c->n_ref;  // grasp.cpp:154
+
+  // Object cloud: FP64 + re-centred FP32 candidates.
+  std::vector<double> obj(p.object_cloud, p.object_cloud + 3 * p.n_object);
+  double center[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = 0; i < p.n_object; ++i)
+    for (int a = 0; a < 3; ++a) center[a] += obj[3 * i + a];
+  for (int a = 0; a < 3; ++a) center[a] /= static_cast<double>(p.n_object);
+  std::vector<float4> cand(p.n_object);
+  double bmax = 0.0;
+  for (int64_t i = 0; i < p.n_object; ++i) {
+    const double bx = obj[3 * i] - center[0], by = obj[3 * i + 1] - center[1], bz = obj[3 * i + 2] - center[2];
+    const float fx = static_cast<float>(bx), fy = static_cast<float>(by), fz = static_cast<float>(bz);
+    const double dx = fx, dy = fy, dz = fz;
+    cand[i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, static_cast<float>(dx * dx + dy * dy + dz * dz));
+    bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
+  }
+  upload(c->obj64, obj.data(), obj.size(), st);
+  upload(c->obj_cand, cand.data(), cand.size(), st);
+  upload(c->scene64, p.scene_cloud, 3 * p.n_scene, st);
+
+  // Preshapes.
+  std::vector<double> surf;
+  std::vector<int> pre_off(n_pre + 1, 0), pre_sdf(n_pre);
+  std::vector<double> tcp(3 * n_pre);
+  c->max_ns = 0;
+  for (int i = 0; i < n_pre; ++i) {
+    const asicp_preshape& s = p.preshapes[i];
+    pre_off[i] = static_cast<int>(surf.size() / 3);
+    surf.insert(surf.end(), s.inner_surface, s.inner_surface + 3 * s.n_surface);
+    pre_sdf[i] = static_cast<int>(s.sdf_index);
+    for (int a = 0; a < 3; ++a) tcp[3 * i + a] = s.tcp[a];
+    c->max_ns = std::max(c->max_ns, static_cast<int>(s.n_surface));
+  }
+  pre_off[n_pre] = static_cast<int>(surf.size() / 3);
+  upload(c->surf64, surf.data(), surf.size(), st);
+  upload(c->pre_surf_off, pre_off.data(), pre_off.size(), st);
+  upload(c->pre_tcp, tcp.data(), tcp.size(), st);
+  upload(c->pre_sdf, pre_sdf.data(), pre_sdf.size(), st);
+
+  // SDF grids.
+  std::vector<Grid> grids(p.n_sdf_grids);
+  std::vector<float> values;
+  for (int64_t g = 0; g < p.n_sdf_grids; ++g) {
+    const asicp_sdf_grid& s = p.sdf_grids[g];
+    Grid& d = grids[g];
+    for (int a = 0; a < 3; ++a) {
+      d.dims[a] = s.dims[a];
+      d.origin[a] = s.origin[a];
+      d.offset[a] = s.offset[a];
+    }
+    d.voxel = s.voxel;
+    d.boundary_max_abs = s.boundary_max_abs;
+    d.values_offset = static_cast<int64_t>(values.size());
+    const size_t total = static_cast<size_t>(s.dims[0]) * s.dims[1] * s.dims[2];
+    values.insert(values.end(), s.values, s.values + total);
+  }
+  upload(c->grids, grids.data(), grids.size(), st);
+  upload(c->sdf_values, values.data(), values.size(), st);
+
+  // Particles (preshape-major flattening, grasp.cpp:135-145).
+  std::vector<int> part_pre, part_pop, pop_off(n_pre + 1, 0);
+  std::vector<int64_t> part_surf_off;
+  std::vector<double> logk1(n_pre);
+  int64_t so = 0;
+  for (int i = 0; i < n_pre; ++i) {
+    pop_off[i] = static_cast<int>(part_pre.size());
+    for (int64_t k = 0; k < p.init_counts[i]; ++k) {
+      part_pre.push_back(i);
+      part_pop.push_back(i);
+      part_surf_off.push_back(so);
+      so += p.preshapes[i].n_surface;
+    }
+    logk1[i] = std::log(static_cast<double>(p.init_counts[i]) + 1.0);  // optim.cpp:143
+  }
+  pop_off[n_pre] = static_cast<int>(part_pre.size());
+  part_surf_off.push_back(so);
+  const int J = static_cast<int>(part_pre.size());
+  c->J = J;
+  c->total_surf = so;
+  c->part_pre = part_pre;
+  upload(c->part_pre_d, part_pre.data(), part_pre.size(), st);
+  upload(c->part_pop, part_pop.data(), part_pop.size(), st);
+  upload(c->pop_off, pop_off.data(), pop_off.size(), st);
+  upload(c->pop_logk1, logk1.data(), logk1.size(), st);
+  upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
+  c->init_theta.assign(p.init_poses, p.init_poses + 7 * J);
+  upload(c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
+
+  // Schedules (host-exact: llround / fmod / pow of the reference).
+  c->ms.resize(c->k_max);
+  c->gammas.resize(c->k_max);
+  for (int k = 0; k < c->k_max; ++k) {
+    c->ms[k] = minibatch_schedule(k, p.k_max, p.n_object);
+    c->gammas[k] = k < c->k_stein ? annealing(k, p.anneal_period_total, p.anneal_cycles, p.anneal_exponent) : 0.0;
+  }
+
+  // Split-K factor for the forward match: enough work items to fill the
+  // persistent grid several times over.
+  int base_items = 0;
+  for (int i = 0; i < n_pre; ++i)
+    base_items += static_cast<int>(p.init_counts[i] * ((p.preshapes[i].n_surface + kNnQB - 1) / kNnQB));
+  c->nchunks_max = std::clamp((4 * c->nn_grid + base_items - 1) / std::max(base_items, 1), 1, 16);
+
+  // State buffers.
+  const size_t Jz = static_cast<size_t>(J);
+  c->theta.ensure(Jz * 7 * 8);
+  c->theta_next.ensure(Jz * 7 * 8);
+  c->loss.ensure(Jz * 8);
+  c->prev_loss.ensure(Jz * 8);
+  c->in_col.ensure(Jz * 4);
+  c->converged.ensure(Jz * 4);
+  c->active.ensure(Jz * 4);
+  c->n_col.ensure(Jz * 4);
+  c->grad.ensure(Jz * 7 * 8);
+  c->prior.ensure(Jz * 7 * 8);
+  c->drift.ensure(Jz * 7 * 8);
+  c->h.ensure(static_cast<size_t>(n_pre) * 8);
+  c->S64.ensure(static_cast<size_t>(so) * 24);
+  c->Sq32.ensure(static_cast<size_t>(so) * 16);
+  c->Sc32.ensure(static_cast<size_t>(so) * 16);
+  c->Bs.ensure(Jz * 8);
+  const size_t jscene = Jz * static_cast<size_t>(c->n_scene);
+  c->col_idx.ensure(jscene * 4);
+  c->col_q.ensure(jscene * 16);
+  c->res_rev.ensure(jscene * 4);
+  c->res_fwd.ensure(static_cast<size_t>(so) * 4);
+  c->rng_state.ensure(Jz * mt::kN * 8);
+  c->rng_mti.ensure(Jz * 4);
+  const size_t jobj = Jz * static_cast<size_t>(c->n_obj);
+  c->pool_idx.ensure(jobj * 4);
+  c->pool32.ensure(jobj * 16);
+  if (static_cast<size_t>(c->n_obj) * 4 > static_cast<size_t>(minibatch_smem_cap())) c->fy_scratch.ensure(jobj * 4);
+  // Work items: forward <= base_items * nchunks, reverse <= J * ceil(n_scene / QB).
+  const size_t max_items = std::max<size_t>(static_cast<size_t>(base_items) * c->nchunks_max,
+                                            Jz * ((c->n_scene + kNnQB - 1) / kNnQB)) +
+                           Jz;
+  c->items.ensure(max_items * sizeof(NnItem));
+  c->item_count.ensure((Jz + 1) * 4);
+  c->item_off.ensure((Jz + 1) * 4);
+  c->item_counter.ensure(4);
+  c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
+  c->partials.ensure(static_cast<size_t>(so) * c->nchunks_max * sizeof(NnPartial));
+  const size_t refine_cap = std::min<size_t>(static_cast<size_t>(so) + jscene, 64ull << 20);
+  c->refine_list.ensure(refine_cap * sizeof(int4));
+  c->refine_count.ensure(4);
+  c->stats.ensure(8 * sizeof(unsigned long long));
+  if (c->record_trace) {
+    const size_t rows = static_cast<size_t>(c->k_max) * Jz;
+    c->trace_theta.ensure(std::max<size_t>(rows, 1) * 7 * 8);
+    c->trace_loss.ensure(std::max<size_t>(rows, 1) * 8);
+    c->trace_col.ensure(std::max<size_t>(rows, 1) * 4);
+  }
+  c->final_loss.ensure(Jz * 8);
+  c->final_free.ensure(Jz * 4);
+
+  // Device views.
+  DevProblem& P = c->P;
+  P.J = J;
+  P.n_obj = c->n_obj;
+  P.n_scene = c->n_scene;
+  P.n_pop = n_pre;
+  P.obj64 = c->obj64.as<double>();
+  P.obj_cand = c->obj_cand.as<float4>();
+  P.scene64 = c->scene64.as<double>();
+  P.surf64 = c->surf64.as<double>();
+  P.pre_surf_off = c->pre_surf_off.as<int>();
+  P.pre_tcp = c->pre_tcp.as<double>();
+  P.pre_sdf = c->pre_sdf.as<int>();
+  P.grids = c->grids.as<Grid>();
+  P.sdf_values = c->sdf_values.as<float>();
+  P.part_pre = c->part_pre_d.as<int>();
+  P.part_surf_off = c->part_surf_off.as<int64_t>();
+  P.part_pop = c->part_pop.as<int>();
+  P.pop_off = c->pop_off.as<int>();
+  P.pop_logk1 = c->pop_logk1.as<double>();
+  for (int a = 0; a < 3; ++a) {
+    P.center[a] = center[a];
+    P.com[a] = p.com[a];
+    P.prior_t_mean[a] = p.prior_t_mean[a];
+    P.prior_t_sigma[a] = p.prior_t_sigma[a];
+  }
+  P.B_obj = bmax * (1.0 + 1e-6) + 1e-12;
+  P.contact_tolerance = p.contact_tolerance;
+  for (int a = 0; a < 4; ++a) {
+    P.prior_q_location[a] = p.prior_q_location[a];
+    P.prior_q_kappa[a] = p.prior_q_kappa[a];
+  }
+  P.bandwidth_mode = p.bandwidth_mode == ASICP_BANDWIDTH_FIXED ? 1 : 0;
+  P.fixed_bandwidth = p.fixed_bandwidth;
+  for (int i = 0; i < 49; ++i) P.A[i] = p.A[i];
+  P.lr = p.learning_rate;
+  P.conv_thr = p.convergence_threshold;
+
+  DevState& S = c->S;
+  S.theta = c->theta.as<double>();
+  S.theta_next = c->theta_next.as<double>();
+  S.loss = c->loss.as<double>();
+  S.prev_loss = c->prev_loss.as<double>();
+  S.in_col = c->in_col.as<int>();
+  S.converged = c->converged.as<int>();
+  S.active = c->active.as<int>();
+  S.n_col = c->n_col.as<int>();
+  S.grad = c->grad.as<double>();
+  S.prior = c->prior.as<double>();
+  S.drift = c->drift.as<double>();
+  S.h = c->h.as<double>();
+  S.S64 = c->S64.as<double>();
+  S.Sq32 = c->Sq32.as<float4>();
+  S.Sc32 = c->Sc32.as<float4>();
+  S.Bs = c->Bs.as<double>();
+  S.col_idx = c->col_idx.as<int>();
+  S.col_q = c->col_q.as<float4>();
+  S.res_fwd = c->res_fwd.as<int>();
+  S.res_rev = c->res_rev.as<int>();
+  S.rng_state = c->rng_state.as<uint64_t>();
+  S.rng_mti = c->rng_mti.as<int>();
+  S.pool_idx = c->pool_idx.as<int>();
+  S.pool32 = c->pool32.as<float4>();
+  S.fy_scratch = c->fy_scratch.as<int>();
+  S.pool_map = nullptr;
+  S.items = c->items.as<NnItem>();
+  S.item_count = c->item_count.as<int>();
+  S.item_off = c->item_off.as<int>();
+  S.item_counter = c->item_counter.as<int>();
+  S.scan_tmp = c->scan_tmp.p;
+  S.scan_tmp_bytes = c->scan_tmp.bytes;
+  S.partials = c->partials.as<NnPartial>();
+  S.refine_list = c->refine_list.as<int4>();
+  S.refine_count = c->refine_count.as<int>();
+  S.refine_cap = static_cast<int>(refine_cap);
+  S.stats = c->stats.as<unsigned long long>();
+  S.trace_theta = c->trace_theta.as<double>();
+  S.trace_loss = c->trace_loss.as<double>();
+  S.trace_col = c->trace_col.as<int>();
+  S.final_loss = c->final_loss.as<double>();
+  S.final_free = c->final_free.as<int>();
+  CUDA_OK(cudaStreamSynchronize(st));
+  c->prepared = true;
+}
+
+NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
+  NnPlan plan{};
+  plan.kind = kind;
+  plan.pooled = pooled ? 1 : 0;
+  plan.m = static_cast<int>(m);
+  plan.fp64_mode = c->nn_mode == 1 ? 1 : 0;
+  const int max_chunks = std::max(1, static_cast<int>((m + 2 * kNnTile - 1) / (2 * kNnTile)));
+  int nch = std::min(c->nchunks_max, max_chunks);
+  int chunk = static_cast<int>((m + nch - 1) / nch);
+  chunk = (chunk + kNnTile - 1) / kNnTile * kNnTile;
+  nch = static_cast<int>((m + chunk - 1) / chunk);
+  plan.nchunks = nch;
+  plan.chunk = chunk;
+  return plan;
+}
+
+// Enqueue one NN round (plan, optional minibatch, filter, merge, refine).
+void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
+  cudaStream_t st = c->stream;
+  launch_nn_plan(c->P, c->S, plan, st);
+  if (minibatch_m > 0) launch_minibatch(c->P, c->S, minibatch_m, st);
+  const bool timed = c->profile && !capture;
+  if (timed) {
+    std::pair<cudaEvent_t, cudaEvent_t> e;
+    CUDA_OK(cudaEventCreate(&e.first));
+    CUDA_OK(cudaEventCreate(&e.second));
+    CUDA_OK(cudaEventRecord(e.first, st));
+    launch_nn_filter(c->P, c->S, plan, c->nn_grid, st);
+    CUDA_OK(cudaEventRecord(e.second, st));
+    c->nn_events.push_back(e);
+  } else {
+    launch_nn_filter(c->P, c->S, plan, c->nn_grid, st);
+  }
+  if (plan.nchunks > 1) launch_nn_merge(c->P, c->S, plan, c->max_ns, st);
+  launch_nn_refine(c->P, c->S, plan, 2 * c->num_sms, st);
+  c->launches += 6 + (minibatch_m > 0) + (plan.nchunks > 1);
+}
+
+// The whole optimize_grasp as a kernel sequence on c->stream.
+void enqueue_solve(asicp_ctx* c, bool capture) {
+  cudaStream_t st = c->stream;
+  DevProblem& P = c->P;
+  DevState& S = c->S;
+  c->launches = 0;
+  CUDA_OK(cudaMemcpyAsync(S.theta, c->init_theta_d.p, static_cast<size_t>(c->J) * 7 * 8, cudaMemcpyDeviceToDevice,
+                          st));
+  CUDA_OK(cudaMemsetAsync(S.stats, 0, 8 * sizeof(unsigned long long), st));
+  launch_init_state(P, S, st);
+  launch_seed_rng(P, S, c->seed, st);
+  c->launches += 2;
+  for (int k = 0; k < c->k_max; ++k) {
+    const bool stein = k < c->k_stein;
+    const int64_t m = c->ms[k];
+    const bool pooled = m < c->n_obj;
+    launch_pose_prep(P, S, 0, st);
+    launch_collide(P, S, 0, 0, st);
+    S.pool_map = pooled ? S.pool_idx : nullptr;
+    const NnPlan plan = make_plan(c, 0, m, pooled);
+    enqueue_nn(c, plan, pooled ? static_cast<int>(m) : 0, capture);
+    launch_cost(P, S, 0, st);
+    c->launches += 3;
+    if (c->record_trace) {
+      launch_trace(P, S, k, st);
+      ++c->launches;
+    }
+    if (stein) {
+      launch_svgd(P, S, c->gammas[k], c->n_ref, c->eta_stein, st);
+      c->launches += 4;
+    } else {
+      launch_sgd(P, S, st);
+      ++c->launches;
+    }
+    launch_bookkeeping(P, S, stein ? 1 : 0, (k + 1) < c->k_stein ? 1 : 0, st);
+    ++c->launches;
+  }
+  // Final ranking on the full reference cloud (grasp.cpp:260-281).
+  S.pool_map = nullptr;
+  launch_pose_prep(P, S, 1, st);
+  launch_collide(P, S, 1, 1, st);
+  const NnPlan fin = make_plan(c, 2, c->n_obj, false);
+  enqueue_nn(c, fin, 0, capture);
+  launch_cost(P, S, 1, st);
+  c->launches += 3;
+  CUDA_OK(cudaGetLastError());
+}
+
+void run(asicp_ctx* c, asicp_solution* out) {
+  if (!c->prepared) throw InvalidArgument("asicp_run: no prepared problem");
+  CUDA_OK(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  for (auto& e : c->nn_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->nn_events.clear();
+  CUDA_OK(cudaEventRecord(c->ev0, st));
+  const bool graph = c->use_graph && !c->profile;
+  if (graph) {
+    if (!c->graph_valid) {
+      cudaGraph_t g;
+      CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_solve(c, true);
+      } catch (...) {
+        cudaStreamEndCapture(st, &g);
+        throw;
+      }
+      CUDA_OK(cudaStreamEndCapture(st, &g));
+      CUDA_OK(cudaGraphInstantiate(&c->graph_exec, g, 0));
+      cudaGraphDestroy(g);
+      c->graph_valid = true;
+    }
+    CUDA_OK(cudaGraphLaunch(c->graph_exec, st));
+  } else {
+    enqueue_solve(c, false);
+  }
+  CUDA_OK(cudaEventRecord(c->ev1, st));
+
+  const int J = c->J;
+  std::vector<double> theta(7 * static_cast<size_t>(J)), floss(J);
+  std::vector<int> ffree(J), conv(J);
+  unsigned long long stats[8];
+  CUDA_OK(cudaMemcpyAsync(theta.data(), c->S.theta, theta.size() * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(floss.data(), c->S.final_loss, floss.size() * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(ffree.data(), c->S.final_free, ffree.size() * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(conv.data(), c->S.converged, conv.size() * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(stats, c->S.stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
+  int refine_total = 0;
+  CUDA_OK(cudaMemcpyAsync(&refine_total, c->S.refine_count, 4, cudaMemcpyDeviceToHost, st));
+  const size_t rows = static_cast<size_t>(c->k_max) * J;
+  if (c->record_trace && rows) {
+    if (out->trace_theta)
+      CUDA_OK(cudaMemcpyAsync(out->trace_theta, c->S.trace_theta, rows * 7 * 8, cudaMemcpyDeviceToHost, st));
+    if (out->trace_loss)
+      CUDA_OK(cudaMemcpyAsync(out->trace_loss, c->S.trace_loss, rows * 8, cudaMemcpyDeviceToHost, st));
+    if (out->trace_in_collision)
+      CUDA_OK(cudaMemcpyAsync(out->trace_in_collision, c->S.trace_col, rows * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_OK(cudaStreamSynchronize(st));
+  if (refine_total > c->S.refine_cap) throw DeviceError("asicp: FP64 refine list overflow");
+
+  float ms = 0.0f;
+  CUDA_OK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  asicp_stats& s = c->last_stats;
+  s = asicp_stats{};
+  s.solve_ms = ms;
+  for (auto& e : c->nn_events) {
+    float t = 0.0f;
+    CUDA_OK(cudaEventElapsedTime(&t, e.first, e.second));
+    s.nn_ms += t;
+    ++s.nn_launches;
+  }
+  s.kernel_launches = c->launches;
+
+  // Final selection (grasp.cpp:283-306): strict < over collision-free
+  // particles, else the best attempt with kNoGraspFound.
+  out->n_particles = J;
+  int best = -1;
+  for (int j = 0; j < J; ++j) {
+    if (!ffree[j]) continue;
+    if (best < 0 || floss[j] < floss[best]) best = j;
+  }
+  if (best < 0) {
+    out->status = ASICP_STATUS_NO_GRASP_FOUND;
+    for (int j = 0; j < J; ++j)
+      if (best < 0 || floss[j] < floss[best]) best = j;
+  } else {
+    out->status = ASICP_STATUS_FOUND;
+  }
+  for (int a = 0; a < 7; ++a) out->theta[a] = theta[7 * best + a];
+  out->preshape_id = c->part_pre[best];
+  out->final_loss = floss[best];
+  out->converged = conv[best];
+  for (int j = 0; j < J; ++j) {
+    if (out->particle_theta)
+      for (int a = 0; a < 7; ++a) out->particle_theta[7 * j + a] = theta[7 * j + a];
+    if (out->particle_loss) out->particle_loss[j] = floss[j];
+    if (out->particle_collision_free) out->particle_collision_free[j] = ffree[j];
+    if (out->particle_converged) out->particle_converged[j] = conv[j];
+    if (out->particle_preshape) out->particle_preshape[j] = c->part_pre[j];
+  }
+  out->nn_uncertified = static_cast<int64_t>(stats[0]);
+  out->nn_full_refines = static_cast<int64_t>(stats[1]);
+  out->nn_queries = static_cast<int64_t>(stats[2]);
+  out->nn_pool_ties = static_cast<int64_t>(stats[3]);
+  out->nn_pairs = static_cast<double>(stats[4]);
+  s.nn_pairs = out->nn_pairs;
+}
+
+template <typename F>
+int guarded(char* err, size_t errlen, F&& f) {
+  try {
+    f();
+    return ASICP_OK;
+  } catch (const InvalidArgument& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_DEVICE_ERROR;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int asicp_abi_version(void) { return ASICP_ABI_VERSION; }
+
+asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen) {
+  asicp_ctx* c = new asicp_ctx();
+  const int rc = guarded(err, errlen, [&] {
+    c->device = device;
+    CUDA_OK(cudaSetDevice(device));
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    nn_set_attrs();
+    CUDA_OK(cudaEventCreate(&c->ev0));
+    CUDA_OK(cudaEventCreate(&c->ev1));
+    c->nn_grid = c->num_sms * std::max(1, nn_blocks_per_sm());
+  });
+  if (rc != ASICP_OK) {
+    delete c;
+    return nullptr;
+  }
+  return c;
+}
+
+void asicp_destroy(asicp_ctx* ctx) { delete ctx; }
+
+int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return ASICP_INVALID_ARGUMENT;
+  switch (option) {
+    case ASICP_OPT_NN_MODE:
+      ctx->nn_mode = static_cast<int>(value);
+      break;
+    case ASICP_OPT_USE_GRAPH:
+      ctx->use_graph = static_cast<int>(value);
+      break;
+    case ASICP_OPT_PROFILE:
+      ctx->profile = static_cast<int>(value);
+      break;
+    default:
+      return ASICP_INVALID_ARGUMENT;
+  }
+  ctx->graph_valid = false;
+  if (ctx->graph_exec) {
+    cudaGraphExecDestroy(ctx->graph_exec);
+    ctx->graph_exec = nullptr;
+  }
+  return ASICP_OK;
+}
+
+int asicp_prepare(asicp_ctx* ctx, const asicp_problem* problem, char* err, size_t errlen) {
+  if (!ctx || !problem) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] { prepare(ctx, *problem); });
+}
+
+int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen) {
+  if (!ctx || !solution) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] { run(ctx, solution); });
+}
+
+int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution, char* err,
+                         size_t errlen) {
+  const int rc = asicp_prepare(ctx, problem, err, errlen);
+  if (rc != ASICP_OK) return rc;
+  return asicp_run(ctx, solution, err, errlen);
+}
+
+int asicp_get_stats(asicp_ctx* ctx, asicp_stats* stats) {
+  if (!ctx || !stats) return ASICP_INVALID_ARGUMENT;
+  *stats = ctx->last_stats;
+  return ASICP_OK;
+}
+
+int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
+  return minibatch_schedule(k, k_max, n_ref);
+}
+
+double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annealing(t, T, C, p); }
+
+}  // extern "C"
