@@ -5,6 +5,7 @@
 #include "dmath.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
+#include "gexp.cuh"
 
 #include <cub/block/block_scan.cuh>
 #include <cub/device/device_scan.cuh>
@@ -823,7 +824,7 @@ __global__ void svgd_kernel(DevProblem P, DevState S, double eta) {
     const double* thi = th_of(S.theta, i);
     const V3 ti = pose_t(thi);
     const V3 diff = sub(ti, tj);
-    const double value = exp(-sqnorm(diff) / h);  // rbf_kernel (optim.cpp:120-125)
+    const double value = glibc_exp(-sqnorm(diff) / h);  // rbf_kernel (optim.cpp:120-125)
     for (int a = 0; a < 3; ++a) pt[a] = pt[a] + (-di[a]) * value;
     const double dt[3] = {tj.x - ti.x, tj.y - ti.y, tj.z - ti.z};
     for (int a = 0; a < 3; ++a) pt[a] = pt[a] + (two_h * dt[a]) * value;
@@ -904,9 +905,18 @@ __global__ void init_state_kernel(DevProblem P, DevState S) {
   S.n_col[j] = 0;
 }
 
+__global__ void dbg_exp_kernel(const double* x, double* y, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = glibc_exp(x[i]);
+}
+
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
+void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st) {
+  dbg_exp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, y, n);
+}
+double host_glibc_exp(double x) { return glibc_exp(x); }
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st) {
   seed_rng_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(S.rng_state, S.rng_mti, seed, P.J);
 }

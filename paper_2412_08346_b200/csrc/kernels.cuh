@@ -119,6 +119,8 @@ void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t 
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
 void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, cudaStream_t st);
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
+void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st);
+double host_glibc_exp(double x);
 void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
 
 }  // namespace asicp

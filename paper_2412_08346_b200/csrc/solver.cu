@@ -8,6 +8,7 @@
 // gamma(k), the phase — is a host-side function of k, and every data-
 // dependent branch is resolved on the device through work lists).
 #include "asicp.h"
+#include "asicp_debug.h"
 #include "kernels.cuh"
 #include "mt64.cuh"
 
@@ -763,5 +764,25 @@ int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
 }
 
 double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annealing(t, T, C, p); }
+
+void asicp_dbg_exp_host(const double* x, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = host_glibc_exp(x[i]);
+}
+
+int asicp_dbg_exp_device(const double* x, double* y, int64_t n) {
+  double *dx = nullptr, *dy = nullptr;
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  if (cudaMalloc(&dx, bytes) != cudaSuccess) return ASICP_DEVICE_ERROR;
+  if (cudaMalloc(&dy, bytes) != cudaSuccess) {
+    cudaFree(dx);
+    return ASICP_DEVICE_ERROR;
+  }
+  cudaMemcpy(dx, x, bytes, cudaMemcpyHostToDevice);
+  launch_dbg_exp(dx, dy, n, nullptr);
+  const cudaError_t e = cudaMemcpy(y, dy, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dy);
+  return e == cudaSuccess ? ASICP_OK : ASICP_DEVICE_ERROR;
+}
 
 }  // extern "C"

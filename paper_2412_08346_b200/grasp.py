@@ -389,7 +389,7 @@ class Solver:
             pass
 
     def prepare(self, problem: GraspProblem | CProblem) -> None:
-        cp = problem if isinstance(problem, CProblem) else CProblem(problem)
+        cp = problem if hasattr(problem, "ptr") else CProblem(problem)
         err = C.create_string_buffer(512)
         _check(self.lib.asicp_prepare(self.ctx, cp.ptr(), err, 512), err)
         self._cp = cp
