@@ -20,6 +20,12 @@ void asicp_dbg_exp_host(const double* x, double* y, int64_t n);
 /* Returns 0 on success, ASICP_DEVICE_ERROR on a CUDA failure. */
 int asicp_dbg_exp_device(const double* x, double* y, int64_t n);
 
+/* FP32 FFMA throughput microbenchmark on the current device (the roofline
+ * denominator of the NN filter): every SM runs independent FFMA chains for
+ * `iters` iterations; returns achieved TFLOP/s (2 FLOP per FFMA), timed with
+ * CUDA events, or a negative value on failure. */
+double asicp_dbg_ffma_tflops(int iters);
+
 #ifdef __cplusplus
 }
 #endif

@@ -153,3 +153,31 @@ def build_sdf(cloud, voxel, padding=-1.0, band=0.003):
     lib.ref_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta,
                       vals.ctypes.data_as(L.c_float_p))
     return tuple(dims), np.array(meta[:3]), meta[3], meta[4], vals
+
+
+# ---------------------------------------------------------------------------
+# The plain-C restatement (oracle/port/asicp_port.c) — available wherever the
+# repo is built, even without /root/reference.
+# ---------------------------------------------------------------------------
+PORT_PATH = HERE / "_build" / "libasicp_port.so"
+_PORT = None
+
+
+def port_available() -> bool:
+    return PORT_PATH.exists()
+
+
+def port_optimize_grasp(problem) -> GraspSolution:
+    global _PORT
+    if _PORT is None:
+        _PORT = C.CDLL(str(PORT_PATH))
+        _PORT.port_optimize_grasp.argtypes = [C.POINTER(L.Problem), C.POINTER(L.Solution), C.c_char_p, C.c_size_t]
+    cp = problem if hasattr(problem, "ptr") else CProblem(problem)
+    bufs = SolutionBuffers(cp.J, cp.k_max, cp.record_trace)
+    err = C.create_string_buffer(512)
+    rc = _PORT.port_optimize_grasp(cp.ptr(), C.byref(bufs.struct), err, 512)
+    if rc == L.ASICP_INVALID_ARGUMENT:
+        raise InvalidArgument(err.value.decode())
+    if rc != L.ASICP_OK:
+        raise RuntimeError(err.value.decode())
+    return bufs.solution(cp.k_stein)

@@ -905,6 +905,47 @@ __global__ void init_state_kernel(DevProblem P, DevState S) {
   S.n_col[j] = 0;
 }
 
+// FFMA peak probe: 16 independent chains per thread, immediate-free 3-register
+// form like the NN filter's FMAs (register operands, one reused across chains).
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
+  float acc[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) acc[k] = threadIdx.x * 1e-3f + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc[k] = __fmaf_rn(acc[k], a, b);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += acc[k];
+  if (s == 1234.5f) out[0] = s;
+}
+
+double run_ffma_peak(int iters) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  float* out = nullptr;
+  if (cudaMalloc(&out, 4) != cudaSuccess) return -1.0;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8;
+  ffma_peak_kernel<<<blocks, 256>>>(out, iters / 4, 0.999f, 1e-4f);  // warm-up
+  cudaEventRecord(e0);
+  ffma_peak_kernel<<<blocks, 256>>>(out, iters, 0.999f, 1e-4f);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  if (cudaGetLastError() != cudaSuccess || ms <= 0.0f) return -1.0;
+  const double flops = 2.0 * 16.0 * static_cast<double>(iters) * blocks * 256.0;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
 __global__ void dbg_exp_kernel(const double* x, double* y, int64_t n) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) y[i] = glibc_exp(x[i]);

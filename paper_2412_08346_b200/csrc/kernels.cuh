@@ -121,6 +121,7 @@ void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, d
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st);
 double host_glibc_exp(double x);
+double run_ffma_peak(int iters);
 void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
 
 }  // namespace asicp

@@ -131,6 +131,7 @@ struct asicp_ctx {
 
   cudaGraphExec_t graph_exec = nullptr;
   bool graph_valid = false;
+  std::vector<char> graph_sig;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> nn_events;
   asicp_stats last_stats{};
@@ -223,11 +224,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   validate(p);
   CUDA_OK(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
-  if (c->graph_exec) {
-    cudaGraphExecDestroy(c->graph_exec);
-    c->graph_exec = nullptr;
-  }
-  c->graph_valid = false;
   const int n_pre = static_cast<int>(p.n_preshapes);
   c->n_pre = n_pre;
   c->n_obj = static_cast<int>(p.n_object);
@@ -475,6 +471,26 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.final_loss = c->final_loss.as<double>();
   S.final_free = c->final_free.as<int>();
   CUDA_OK(cudaStreamSynchronize(st));
+  // The captured graph bakes DevProblem/DevState and the k schedule into its
+  // kernel parameters: keep it only if all of them are unchanged.
+  std::vector<char> sig(sizeof(DevProblem) + sizeof(DevState));
+  std::memcpy(sig.data(), &P, sizeof(DevProblem));
+  std::memcpy(sig.data() + sizeof(DevProblem), &S, sizeof(DevState));
+  auto push = [&](const void* ptr, size_t n) {
+    const char* b = static_cast<const char*>(ptr);
+    sig.insert(sig.end(), b, b + n);
+  };
+  push(c->ms.data(), c->ms.size() * sizeof(int64_t));
+  push(c->gammas.data(), c->gammas.size() * sizeof(double));
+  const int64_t extra[5] = {c->k_max, c->k_stein, c->record_trace, c->nchunks_max, static_cast<int64_t>(c->seed)};
+  push(extra, sizeof(extra));
+  push(&c->eta_stein, sizeof(double));
+  if (sig != c->graph_sig) {
+    if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+    c->graph_exec = nullptr;
+    c->graph_valid = false;
+    c->graph_sig = std::move(sig);
+  }
   c->prepared = true;
 }
 
@@ -729,6 +745,7 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
       return ASICP_INVALID_ARGUMENT;
   }
   ctx->graph_valid = false;
+  ctx->graph_sig.clear();
   if (ctx->graph_exec) {
     cudaGraphExecDestroy(ctx->graph_exec);
     ctx->graph_exec = nullptr;
@@ -764,6 +781,8 @@ int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
 }
 
 double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annealing(t, T, C, p); }
+
+double asicp_dbg_ffma_tflops(int iters) { return run_ffma_peak(iters); }
 
 void asicp_dbg_exp_host(const double* x, double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = host_glibc_exp(x[i]);

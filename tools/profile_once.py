@@ -1,0 +1,15 @@
+"""Run one cfg2 solve (for ncu launch lists / captures).  Usage:
+   python tools/profile_once.py [cfg] [--graph] [--runs N]"""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2412_08346_b200 import Solver, fixtures
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 2
+runs = int(sys.argv[sys.argv.index("--runs") + 1]) if "--runs" in sys.argv else 1
+fx = fixtures.config(cfg, seed=0)
+s = Solver(use_graph="--graph" in sys.argv)
+s.prepare(fx)
+for _ in range(runs):
+    sol = s.run()
+print("status", sol.status, "loss", sol.final_loss, sol.diagnostics)
