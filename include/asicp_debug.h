@@ -26,6 +26,19 @@ int asicp_dbg_exp_device(const double* x, double* y, int64_t n);
  * CUDA events, or a negative value on failure. */
 double asicp_dbg_ffma_tflops(int iters);
 
+/* Raw NN counters of the last asicp_run: [0] windows decided in FP64, [1] full
+ * FP64 rescans, [2] queries, [3] canonical-order ties, [4] pairs, [5..7] rescans
+ * per match kind (forward, reverse, final), [8..11] rescan reasons (mode,
+ * top-3 overflow, window > list, merge overflow), [16 + k] full rescans in
+ * iteration k (k_max = final ranking).  `out` holds 256 entries. */
+struct asicp_ctx;
+int asicp_dbg_raw_stats(struct asicp_ctx* ctx, uint64_t* out);
+
+/* The device minibatch sampler (mt19937_64 + Lemire + partial Fisher-Yates,
+ * spatial_index.cpp:111-123) on one stream seeded with `seed`: `calls`
+ * consecutive draws of ms[c] indices from [0, n), written back to back. */
+int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

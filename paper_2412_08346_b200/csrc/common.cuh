@@ -1,0 +1,39 @@
+// Device helpers shared by kernels.cu and nn.cu.
+#pragma once
+
+#include "dmath.cuh"
+#include "kernels.cuh"
+
+#include <cstdint>
+
+namespace asicp {
+
+constexpr int kSub = 32;  // NN candidates per subtile (the unit of window tracking)
+
+__device__ __forceinline__ const double* th_of(const double* theta, int j) { return theta + 7 * j; }
+
+__device__ __forceinline__ V3 load3(const double* p, int64_t i) { return V3{p[3 * i], p[3 * i + 1], p[3 * i + 2]}; }
+
+__host__ __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ __forceinline__ int round_up(int a, int b) { return ceil_div(a, b) * b; }
+
+// Rigorous bound on the FP32 expansion-form distance error:
+// with a = query - centre, b = candidate - centre, A = |a|, B >= max |b|,
+//   |d32 - (|b|^2 - 2 a.b)| <= E = 1.01 u (6 B^2 + 10 A B) + 2^-50 (A + B)^2,
+// u = 2^-24 (the 2^-50 term covers the reference's own FP64 rounding).  Two
+// candidates whose FP32 values differ by more than 2E are ordered correctly,
+// so the window [b1, b1 + 2E] contains the reference's answer.
+__device__ __forceinline__ float nn_margin(double A, double B) {
+  const double u = 5.9604644775390625e-08;
+  const double e32 = 1.01 * u * (6.0 * B * B + 10.0 * A * B);
+  const double e64 = 8.881784197001252e-16 * (A + B) * (A + B);
+  return __double2float_ru(2.0 * (e32 + e64));
+}
+
+// True contact-surface size of particle j (surface rows are padded to kSub).
+__device__ __forceinline__ int surf_count(const DevProblem& P, int j) {
+  const int pre = P.part_pre[j];
+  return P.pre_surf_off[pre + 1] - P.pre_surf_off[pre];
+}
+
+}  // namespace asicp

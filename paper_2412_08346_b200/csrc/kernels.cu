@@ -1,36 +1,16 @@
-// Device kernels of the B200 AS-ICP solver.  Reference correspondences are
-// cited per kernel; every FP64 expression follows dmath.cuh's reference order
-// (this file is compiled with -fmad=false; the FP32 NN filter uses explicit
-// __fmaf_rn).
-#include "dmath.cuh"
-#include "kernels.cuh"
-#include "mt64.cuh"
+// Device kernels of the B200 AS-ICP solver (everything but the NN search,
+// which lives in nn.cu).  Reference correspondences are cited per kernel;
+// every FP64 expression follows dmath.cuh's reference order (this file is
+// compiled with -fmad=false).
+#include "common.cuh"
 #include "gexp.cuh"
+#include "mt64.cuh"
 
-#include <cub/block/block_scan.cuh>
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
-#include <cfloat>
 #include <cstdint>
 
 namespace asicp {
-
-// ---------------------------------------------------------------------------
-// Small helpers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ const double* th_of(const double* theta, int j) { return theta + 7 * j; }
-
-__device__ __forceinline__ V3 load3(const double* p, int64_t i) { return V3{p[3 * i], p[3 * i + 1], p[3 * i + 2]}; }
-
-// Rigorous half-window of the FP32 expansion-form distance:
-// |d32 - (|b|^2 - 2 a.b)| <= E,  E = 1.01 u (6 B^2 + 10 A B) + 2^-50 (A + B)^2.
-__device__ __forceinline__ float nn_margin(double A, double B) {
-  const double u = 5.9604644775390625e-08;  // 2^-24
-  const double e32 = 1.01 * u * (6.0 * B * B + 10.0 * A * B);
-  const double e64 = 8.881784197001252e-16 * (A + B) * (A + B);
-  return __double2float_ru(2.0 * (e32 + e64));
-}
 
 // ---------------------------------------------------------------------------
 // K0: per-particle RNG seeding, std::mt19937_64(seed + j) (grasp.cpp:149-151).
@@ -43,10 +23,12 @@ __global__ void seed_rng_kernel(uint64_t* state, int* mti, uint64_t seed, int J)
 }
 
 // ---------------------------------------------------------------------------
-// K1a: pose preparation — R(q), S_world = R s + t for the contact surface
-// (apply_transform, geometry.cpp:68-74) in FP64, plus its FP32 re-centred
-// forms: queries (x, y, z, margin) for the forward match and candidates
-// (-2x, -2y, -2z, |b|^2) for the reverse (collision) match.
+// K1: pose preparation — R(q) and S_world = R s + t (apply_transform,
+// geometry.cpp:68-74) in FP64, plus two FP32 forms for the NN filter:
+// forward queries (x, y, z, margin) centred at the object centroid, and
+// reverse candidates (-2b, |b|^2) centred at the particle's TCP in world
+// (keeps |b| at gripper scale, so the certification window stays tight).
+// Candidate rows are padded to a multiple of 32 with +inf.
 // ---------------------------------------------------------------------------
 __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   const int j = blockIdx.x;
@@ -57,6 +39,8 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   const V3 t = pose_t(th);
   const int s0 = P.pre_surf_off[pre], ns = P.pre_surf_off[pre + 1] - s0;
   const int64_t o = P.part_surf_off[j];
+  const V3 tcp = V3{P.pre_tcp[3 * pre], P.pre_tcp[3 * pre + 1], P.pre_tcp[3 * pre + 2]};
+  const V3 c = transform(r, t, tcp);
   __shared__ double s_bmax[kNnThreads];
   double bmax = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -65,19 +49,26 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
     S.S64[3 * (o + i) + 1] = w.y;
     S.S64[3 * (o + i) + 2] = w.z;
     const double ax = w.x - P.center[0], ay = w.y - P.center[1], az = w.z - P.center[2];
-    const float fx = __double2float_rn(ax), fy = __double2float_rn(ay), fz = __double2float_rn(az);
     const double A = sqrt(ax * ax + ay * ay + az * az);
-    S.Sq32[o + i] = make_float4(fx, fy, fz, nn_margin(A, P.B_obj));
-    const double bx = fx, by = fy, bz = fz;
-    S.Sc32[o + i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(bx * bx + by * by + bz * bz));
-    bmax = fmax(bmax, A);
+    S.Sq32[o + i] = make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az),
+                                nn_margin(A, P.B_obj));
+    const double bx = w.x - c.x, by = w.y - c.y, bz = w.z - c.z;
+    const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
+    const double gx = fx, gy = fy, gz = fz;
+    S.Sc32[o + i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(gx * gx + gy * gy + gz * gz));
+    bmax = fmax(bmax, sqrt(bx * bx + by * by + bz * bz));
   }
+  for (int i = ns + threadIdx.x; i < round_up(ns, kSub); i += blockDim.x)
+    S.Sc32[o + i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
   s_bmax[threadIdx.x] = bmax;
   __syncthreads();
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int i = 0; i < blockDim.x; ++i) m = fmax(m, s_bmax[i]);
     S.Bs[j] = m * (1.0 + 1e-6) + 1e-12;
+    S.ctr[3 * j] = c.x;
+    S.ctr[3 * j + 1] = c.y;
+    S.ctr[3 * j + 2] = c.z;
   }
 }
 
@@ -98,28 +89,33 @@ __global__ void __launch_bounds__(256) collide_kernel(DevProblem P, DevState S, 
   inverse(pose_q(th), pose_t(th), &qi, &ti);
   const M3 r = rotation_matrix(qi);
   const double B = S.Bs[j];
-  using Scan = cub::BlockScan<int, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int s_total;
+  const V3 c = V3{S.ctr[3 * j], S.ctr[3 * j + 1], S.ctr[3 * j + 2]};
+  const V3 off = V3{g.offset[0], g.offset[1], g.offset[2]};
+  __shared__ int warp_tot[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int base = 0;
   const int64_t row = static_cast<int64_t>(j) * P.n_scene;
   for (int c0 = 0; c0 < P.n_scene; c0 += 256) {
-    const int c = c0 + threadIdx.x;
-    int hit = 0;
-    if (c < P.n_scene) {
-      const V3 p = load3(P.scene64, c);
-      V3 local = add(add(mul(r, p), ti), V3{g.offset[0], g.offset[1], g.offset[2]});
-      local = sub(local, V3{g.offset[0], g.offset[1], g.offset[2]});
-      const double v = sdf_query(g, P.sdf_values, local.x, local.y, local.z);
-      hit = v > P.contact_tolerance ? 1 : 0;
+    const int idx = c0 + threadIdx.x;
+    bool hit = false;
+    if (idx < P.n_scene) {
+      const V3 p = load3(P.scene64, idx);
+      const V3 local = sub(add(add(mul(r, p), ti), off), off);
+      hit = sdf_query(g, P.sdf_values, local.x, local.y, local.z) > P.contact_tolerance;
     }
-    int off, total;
-    Scan(tmp).ExclusiveSum(hit, off, total);
+    const unsigned mask = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) warp_tot[wid] = __popc(mask);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < 8; ++w) {
+      before += w < wid ? warp_tot[w] : 0;
+      total += warp_tot[w];
+    }
     if (hit && !count_only) {
-      const int slot = base + off;
-      S.col_idx[row + slot] = c;
-      const V3 p = load3(P.scene64, c);
-      const double ax = p.x - P.center[0], ay = p.y - P.center[1], az = p.z - P.center[2];
+      const int slot = base + before + __popc(mask & ((1u << lane) - 1u));
+      S.col_idx[row + slot] = idx;
+      const V3 p = load3(P.scene64, idx);
+      const double ax = p.x - c.x, ay = p.y - c.y, az = p.z - c.z;
       const double A = sqrt(ax * ax + ay * ay + az * az);
       S.col_q[row + slot] =
           make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az), nn_margin(A, B));
@@ -135,7 +131,7 @@ __global__ void __launch_bounds__(256) collide_kernel(DevProblem P, DevState S, 
 // (spatial_index.cpp:111-131) with Rng::uniform_index (rng.hpp:32-44) on the
 // particle's own mt19937_64 stream.  Only non-colliding active particles
 // draw (grasp.cpp:183-184).  Output: pool object indices in sample order and
-// the gathered FP32 candidates.
+// the gathered FP32 candidates (+inf padded to a multiple of 32).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t serial_next(uint64_t* st, int* mti) {
   if (*mti >= mt::kN) {
@@ -146,7 +142,7 @@ __device__ __forceinline__ uint64_t serial_next(uint64_t* st, int* mti) {
 }
 
 template <bool kSmemIdx>
-__global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S, int m, int idx_cap) {
+__global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S, int m) {
   const int j = blockIdx.x;
   if (!S.active[j] || S.n_col[j] > 0) return;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -156,7 +152,7 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
   __shared__ int s_mti, s_reject;
   const int n = P.n_obj;
   int* idx = kSmemIdx ? reinterpret_cast<int*>(dyn) : S.fy_scratch + static_cast<int64_t>(j) * n;
-  int* pool = S.pool_idx + static_cast<int64_t>(j) * n;
+  int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
   uint64_t* gst = S.rng_state + static_cast<int64_t>(j) * mt::kN;
   for (int i = threadIdx.x; i < mt::kN; i += blockDim.x) st[i] = gst[i];
   for (int i = threadIdx.x; i < n; i += blockDim.x) idx[i] = i;  // iota (spatial_index.cpp:115-116)
@@ -197,7 +193,7 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
           jbuf[done] = static_cast<uint32_t>(i0 + done + u);
           ++done;
         }
-        consumed = -1;  // signal: engine position is lm
+        consumed = -1;
         s_mti = lm;
       }
       // Partial Fisher-Yates swaps (spatial_index.cpp:117-120).  Position i
@@ -219,406 +215,11 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
   }
   for (int i = threadIdx.x; i < mt::kN; i += blockDim.x) gst[i] = st[i];
   if (threadIdx.x == 0) S.rng_mti[j] = s_mti;
-  __threadfence_block();
   __syncthreads();
-  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * n;
+  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
   for (int i = threadIdx.x; i < m; i += blockDim.x) pool32[i] = P.obj_cand[pool[i]];
-}
-
-// ---------------------------------------------------------------------------
-// NN work planning: per particle item counts -> exclusive scan -> items.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
-
-__global__ void nn_count_kernel(DevProblem P, DevState S, NnPlan plan) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j > P.J) return;
-  if (j == P.J) {
-    S.item_count[j] = 0;
-    return;
-  }
-  int cnt = 0;
-  if (plan.kind == 2 || S.active[j]) {
-    const int ns = P.part_surf_off[j + 1] - P.part_surf_off[j];
-    if (plan.kind != 2 && S.n_col[j] > 0) {
-      cnt = ceil_div(S.n_col[j], kNnQB);
-    } else {
-      cnt = ceil_div(ns, kNnQB) * plan.nchunks;
-    }
-  }
-  S.item_count[j] = cnt;
-}
-
-__global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.J) return;
-  const int cnt = S.item_count[j];
-  if (cnt == 0) return;
-  int w = S.item_off[j];
-  const int64_t so = P.part_surf_off[j];
-  const int ns = P.part_surf_off[j + 1] - P.part_surf_off[j];
-  if (plan.kind != 2 && S.n_col[j] > 0) {
-    const int nq = S.n_col[j];
-    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
-    for (int b = 0; b < cnt; ++b) {
-      NnItem it;
-      it.q = S.col_q + row + b * kNnQB;
-      it.nq = min(kNnQB, nq - b * kNnQB);
-      it.c = S.Sc32 + so;
-      it.nc = ns;
-      it.c_base = 0;
-      it.kind = 1;
-      it.owner = j;
-      it.q_first = static_cast<int>(b * kNnQB);
-      it.chunk = 0;
-      it.nchunks = 1;
-      S.items[w++] = it;
-    }
-    return;
-  }
-  const float4* cands = plan.pooled ? S.pool32 + static_cast<int64_t>(j) * P.n_obj : P.obj_cand;
-  for (int b = 0; b < ceil_div(ns, kNnQB); ++b)
-    for (int s = 0; s < plan.nchunks; ++s) {
-      NnItem it;
-      it.q = S.Sq32 + so + b * kNnQB;
-      it.nq = min(kNnQB, ns - b * kNnQB);
-      const int c0 = s * plan.chunk;
-      it.c = cands + c0;
-      it.nc = min(plan.chunk, plan.m - c0);
-      it.c_base = c0;
-      it.kind = plan.kind;
-      it.owner = j;
-      it.q_first = static_cast<int>(b * kNnQB);
-      it.chunk = s;
-      it.nchunks = plan.nchunks;
-      S.items[w++] = it;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// FP64 reference distance for a window candidate (spatial_index.cpp:69:
-// (points[idx] - query).squaredNorm()).
-// ---------------------------------------------------------------------------
-struct NnGeom {
-  const double* qpt;     // query point (FP64)
-  const double* cbase;   // candidate FP64 base (xyz rows)
-  const int* cmap;       // candidate position -> row (pool), or null
-};
-
-__device__ __forceinline__ NnGeom nn_geom(const DevProblem& P, const DevState& S, const NnPlan& plan, int kind,
-                                          int j, int qlocal) {
-  NnGeom g;
-  const int64_t so = P.part_surf_off[j];
-  if (kind == 1) {
-    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
-    g.qpt = P.scene64 + 3 * static_cast<int64_t>(S.col_idx[row + qlocal]);
-    g.cbase = S.S64 + 3 * so;
-    g.cmap = nullptr;
-  } else {
-    g.qpt = S.S64 + 3 * (so + qlocal);
-    g.cbase = P.obj64;
-    g.cmap = (kind == 0 && plan.pooled) ? S.pool_idx + static_cast<int64_t>(j) * P.n_obj : nullptr;
-  }
-  return g;
-}
-
-__device__ __forceinline__ double nn_d64(const NnGeom& g, int pos) {
-  const int64_t r = g.cmap ? g.cmap[pos] : pos;
-  const V3 p = load3(g.cbase, r);
-  const V3 q = V3{g.qpt[0], g.qpt[1], g.qpt[2]};
-  return sqnorm(sub(p, q));
-}
-
-__device__ __forceinline__ int* nn_result_slot(const DevProblem& P, const DevState& S, int kind, int j, int qlocal) {
-  if (kind == 1) return S.res_rev + static_cast<int64_t>(j) * P.n_scene + qlocal;
-  return S.res_fwd + P.part_surf_off[j] + qlocal;
-}
-
-// Resolve a (merged) window: FP64 decision with the reference tie rule
-// (strictly closer wins, equal distance -> lowest position).  Exact ties
-// between distinct rows of a canonical-order candidate set are counted: the
-// reference breaks those by its sampled pool order.
-__device__ __forceinline__ int nn_decide(const NnGeom& g, const int* pos, int n, bool tie_sensitive,
-                                         unsigned long long* stats) {
-  if (n == 1) return pos[0];
-  atomicAdd(stats + 0, 1ull);
-  double best = 0.0;
-  int bi = -1;
-  bool tie = false;
-  for (int e = 0; e < n; ++e) {
-    const double d = nn_d64(g, pos[e]);
-    if (bi >= 0 && d == best) tie = true;
-    if (bi < 0 || d < best || (d == best && pos[e] < bi)) {
-      if (bi < 0 || d < best) tie = false;
-      best = d;
-      bi = pos[e];
-    }
-  }
-  if (tie && tie_sensitive) atomicAdd(stats + 3, 1ull);
-  return bi;
-}
-
-__device__ __forceinline__ void push_refine(DevState& S, int kind, int j, int qlocal) {
-  const int slot = atomicAdd(S.refine_count, 1);
-  if (slot < S.refine_cap) S.refine_list[slot] = make_int4(kind, j, qlocal, 0);
-  atomicAdd(S.stats + 1, 1ull);
-}
-
-// ---------------------------------------------------------------------------
-// K1/K3/K8: the FP32-filter NN kernel (persistent over work items).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-  } while (!done);
-}
-
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-constexpr int kNnSmemBytes = kNnStages * kNnTile * 16 + kNnQ * kNnL * kNnThreads * 8;
-
-__global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, DevState S, NnPlan plan) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  float4* tiles = reinterpret_cast<float4*>(smem_raw);
-  int* lpos = reinterpret_cast<int*>(smem_raw + kNnStages * kNnTile * 16);
-  float* ldist = reinterpret_cast<float*>(lpos + kNnQ * kNnL * kNnThreads);
-  __shared__ __align__(8) uint64_t full_bar[kNnStages];
-  __shared__ int s_item;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    for (int s = 0; s < kNnStages; ++s) mbar_init(&full_bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int n_items = S.item_off[P.J];
-  uint32_t gtile = 0;
-  for (;;) {
-    if (tid == 0) s_item = atomicAdd(S.item_counter, 1);
-    __syncthreads();
-    const int it = s_item;
-    __syncthreads();
-    if (it >= n_items) break;
-    const NnItem w = S.items[it];
-    const int ntiles = (w.nc + kNnTile - 1) / kNnTile;
-    if (tid == 0) {
-      atomicAdd(S.stats + 2, static_cast<unsigned long long>(w.chunk == 0 ? w.nq : 0));
-      atomicAdd(S.stats + 4, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
-      for (int t = 0; t < ntiles && t < kNnStages; ++t) {
-        const uint32_t s = (gtile + t) % kNnStages;
-        const int n_in = min(kNnTile, w.nc - t * kNnTile);
-        tma_load_1d(tiles + s * kNnTile, w.c + t * kNnTile, n_in * 16, &full_bar[s]);
-      }
-    }
-    float qx[kNnQ], qy[kNnQ], qz[kNnQ], mg[kNnQ], thr[kNnQ], b1[kNnQ], ovf[kNnQ];
-    int cnt[kNnQ];
-#pragma unroll
-    for (int k = 0; k < kNnQ; ++k) {
-      const int qi = tid + k * kNnThreads;
-      if (qi < w.nq) {
-        const float4 q = w.q[qi];
-        qx[k] = q.x;
-        qy[k] = q.y;
-        qz[k] = q.z;
-        mg[k] = q.w;
-        thr[k] = INFINITY;
-      } else {
-        qx[k] = qy[k] = qz[k] = 0.0f;
-        mg[k] = 0.0f;
-        thr[k] = -INFINITY;  // never enters the window
-      }
-      b1[k] = INFINITY;
-      ovf[k] = INFINITY;
-      cnt[k] = 0;
-    }
-    for (int t = 0; t < ntiles; ++t) {
-      const uint32_t G = gtile + t;
-      const uint32_t s = G % kNnStages;
-      mbar_wait(&full_bar[s], (G / kNnStages) & 1u);
-      const float4* tile = tiles + s * kNnTile;
-      const int n_in = min(kNnTile, w.nc - t * kNnTile);
-      const int pbase = t * kNnTile;
-#pragma unroll 2
-      for (int c = 0; c < n_in; ++c) {
-        const float4 v = tile[c];
-        float d[kNnQ];
-        bool hit = false;
-#pragma unroll
-        for (int k = 0; k < kNnQ; ++k) {
-          d[k] = __fmaf_rn(qx[k], v.x, __fmaf_rn(qy[k], v.y, __fmaf_rn(qz[k], v.z, v.w)));
-          hit |= d[k] <= thr[k];
-        }
-        if (hit) {
-#pragma unroll
-          for (int k = 0; k < kNnQ; ++k) {
-            if (d[k] <= thr[k]) {
-              if (d[k] < b1[k]) {
-                b1[k] = d[k];
-                thr[k] = __fadd_ru(d[k], mg[k]);
-                int out = 0;
-                const int n = min(cnt[k], kNnL);
-                for (int e = 0; e < n; ++e) {
-                  const int src = (k * kNnL + e) * kNnThreads + tid;
-                  const float de = ldist[src];
-                  if (de <= thr[k]) {
-                    const int dst = (k * kNnL + out) * kNnThreads + tid;
-                    ldist[dst] = de;
-                    lpos[dst] = lpos[src];
-                    ++out;
-                  }
-                }
-                cnt[k] = out;
-              }
-              if (cnt[k] < kNnL) {
-                const int dst = (k * kNnL + cnt[k]) * kNnThreads + tid;
-                ldist[dst] = d[k];
-                lpos[dst] = pbase + c;
-                ++cnt[k];
-              } else {
-                ovf[k] = fminf(ovf[k], d[k]);
-              }
-            }
-          }
-        }
-      }
-      __syncthreads();
-      if (tid == 0 && t + kNnStages < ntiles) {
-        const int tn = t + kNnStages;
-        const int n2 = min(kNnTile, w.nc - tn * kNnTile);
-        tma_load_1d(tiles + s * kNnTile, w.c + tn * kNnTile, n2 * 16, &full_bar[s]);
-      }
-    }
-    gtile += ntiles;
-    // Emit: final prune, then either resolve in place (single chunk) or
-    // write the partial window for the merge kernel.
-#pragma unroll
-    for (int k = 0; k < kNnQ; ++k) {
-      const int qi = tid + k * kNnThreads;
-      if (qi >= w.nq) continue;
-      int n = 0;
-      int pos[kNnL];
-      float dd[kNnL];
-      for (int e = 0; e < cnt[k]; ++e) {
-        const int src = (k * kNnL + e) * kNnThreads + tid;
-        if (ldist[src] <= thr[k]) {
-          pos[n] = lpos[src] + w.c_base;
-          dd[n] = ldist[src];
-          ++n;
-        }
-      }
-      const bool overflow = ovf[k] <= thr[k];
-      const int qlocal = w.q_first + qi;
-      if (w.nchunks == 1) {
-        if (plan.fp64_mode || overflow) {
-          push_refine(S, w.kind, w.owner, qlocal);
-        } else {
-          const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
-          *nn_result_slot(P, S, w.kind, w.owner, qlocal) =
-              nn_decide(g, pos, n, w.kind == 0 && !plan.pooled, S.stats);
-        }
-      } else {
-        NnPartial pr;
-        pr.b1 = b1[k];
-        pr.count = overflow ? -1 : n;
-        for (int e = 0; e < kNnL; ++e) {
-          pr.pos[e] = e < n ? pos[e] : 0;
-          pr.d[e] = e < n ? dd[e] : INFINITY;
-        }
-        S.partials[(P.part_surf_off[w.owner] + qlocal) * static_cast<int64_t>(w.nchunks) + w.chunk] = pr;
-      }
-    }
-  }
-}
-
-// Merge per-chunk windows of forward/final queries (nchunks > 1).
-__global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
-  const int j = blockIdx.y;
-  if (plan.kind != 2 && (!S.active[j] || S.n_col[j] > 0)) return;
-  const int64_t so = P.part_surf_off[j];
-  const int ns = P.part_surf_off[j + 1] - so;
-  const int qlocal = blockIdx.x * blockDim.x + threadIdx.x;
-  if (qlocal >= ns) return;
-  const NnPartial* pr = S.partials + (so + qlocal) * static_cast<int64_t>(plan.nchunks);
-  float b1 = INFINITY;
-  for (int s = 0; s < plan.nchunks; ++s) b1 = fminf(b1, pr[s].b1);
-  const float thr = __fadd_ru(b1, S.Sq32[so + qlocal].w);
-  constexpr int kMax = 64;
-  int pos[kMax];
-  int n = 0;
-  bool overflow = false;
-  for (int s = 0; s < plan.nchunks; ++s) {
-    const NnPartial p = pr[s];
-    if (p.b1 > thr) continue;
-    if (p.count < 0) {
-      overflow = true;
-      continue;
-    }
-    for (int e = 0; e < p.count; ++e)
-      if (p.d[e] <= thr) {
-        if (n < kMax)
-          pos[n++] = p.pos[e];
-        else
-          overflow = true;
-      }
-  }
-  if (plan.fp64_mode || overflow || n == 0) {
-    push_refine(S, plan.kind, j, qlocal);
-    return;
-  }
-  const NnGeom g = nn_geom(P, S, plan, plan.kind, j, qlocal);
-  S.res_fwd[so + qlocal] = nn_decide(g, pos, n, plan.kind == 0 && !plan.pooled, S.stats);
-}
-
-// Full FP64 rescan for overflowing windows (and the FP64 validation mode):
-// one warp per query, lexicographic (distance, position) minimum.
-__global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int total = min(*S.refine_count, S.refine_cap);
-  for (int e = warp; e < total; e += nwarps) {
-    const int4 r = S.refine_list[e];
-    const int kind = r.x, j = r.y, qlocal = r.z;
-    const NnGeom g = nn_geom(P, S, plan, kind, j, qlocal);
-    const int nc = kind == 1 ? P.part_surf_off[j + 1] - P.part_surf_off[j] : plan.m;
-    double best = INFINITY;
-    int bi = 0x7fffffff;
-    for (int c = lane; c < nc; c += 32) {
-      const double d = nn_d64(g, c);
-      if (d < best || (d == best && c < bi)) {
-        best = d;
-        bi = c;
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob < best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
-      }
-    }
-    if (lane == 0) *nn_result_slot(P, S, kind, j, qlocal) = bi;
-  }
+  for (int i = m + threadIdx.x; i < round_up(m, kSub); i += blockDim.x)
+    pool32[i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
 }
 
 // ---------------------------------------------------------------------------
@@ -653,13 +254,15 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   if (threadIdx.x < 8) {
     double init = 0.0;
     if (!reverse) {
-      if (threadIdx.x < 3) init = threadIdx.x == 0 ? com_residual.x : (threadIdx.x == 1 ? com_residual.y : com_residual.z);
-      else if (threadIdx.x < 7) init = dot(com_residual, mul(dR[threadIdx.x - 3], tcp));
+      if (threadIdx.x < 3)
+        init = threadIdx.x == 0 ? com_residual.x : (threadIdx.x == 1 ? com_residual.y : com_residual.z);
+      else if (threadIdx.x < 7)
+        init = dot(com_residual, mul(dR[threadIdx.x - 3], tcp));
     }
     acc[threadIdx.x] = init;  // slot 7: contact-loss sum starts at 0.0
   }
   const int64_t row = static_cast<int64_t>(j) * P.n_scene;
-  const int* pmap = S.pool_map;  // forward pool mapping (null when canonical)
+  const int* pmap = final_pass ? nullptr : S.pool_map;
   for (int c0 = 0; c0 < npairs; c0 += kCostThreads) {
     const int i = c0 + threadIdx.x;
     if (i < npairs) {
@@ -673,7 +276,7 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
         src = load3(P.surf64, s0 + i);
         tr = load3(S.S64, so + i);
         const int pos = S.res_fwd[so + i];
-        const int64_t oi = (!final_pass && pmap) ? pmap[static_cast<int64_t>(j) * P.n_obj + pos] : pos;
+        const int64_t oi = pmap ? pmap[static_cast<int64_t>(j) * P.n_obj_pad + pos] : pos;
         ref = load3(P.obj64, oi);
       }
       const V3 res = sub(tr, ref);
@@ -695,12 +298,7 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   if (threadIdx.x == 0) {
     const double m = static_cast<double>(npairs);
     const double contact = acc[7] / m;
-    double loss;
-    if (reverse) {
-      loss = contact;
-    } else {
-      loss = contact + sqnorm(com_residual);  // total_loss(contact, com_loss)
-    }
+    const double loss = reverse ? contact : contact + sqnorm(com_residual);  // total_loss(contact, com_loss)
     if (final_pass) {
       S.final_loss[j] = loss;
       S.final_free[j] = S.n_col[j] == 0 ? 1 : 0;
@@ -744,7 +342,19 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
   for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
 }
 
-// One CTA per population: 8 radix passes of 8 bits over the K(K-1)/2 keys.
+// Pair p of a population -> (i, j), i < j, row-major over the upper triangle.
+__device__ __forceinline__ void pair_of(long long p, int K, int* pi, int* pj) {
+  const double a = 2.0 * K - 1.0;
+  long long i = static_cast<long long>((a - sqrt(a * a - 8.0 * static_cast<double>(p))) * 0.5);
+  auto start = [K](long long r) { return r * (2LL * K - r - 1) / 2; };
+  while (i > 0 && start(i) > p) --i;
+  while (i + 1 < K && start(i + 1) <= p) ++i;
+  *pi = static_cast<int>(i);
+  *pj = static_cast<int>(i + 1 + (p - start(i)));
+}
+
+// One CTA per population: 8 radix passes of 8 bits over the K(K-1)/2 keys
+// (nth_element at M/2, optim.cpp:141-142: an exact order statistic).
 __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) {
   const int pop = blockIdx.x;
   const int b = P.pop_off[pop], K = P.pop_off[pop + 1] - b;
@@ -771,14 +381,12 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const unsigned long long prefix = s_prefix, mask = s_mask;
-    for (int i = 0; i < K; ++i) {
-      const V3 ti = pose_t(th_of(S.theta, b + i));
-      for (int jj = i + 1 + threadIdx.x; jj < K; jj += blockDim.x) {
-        const V3 tj = pose_t(th_of(S.theta, b + jj));
-        const double d2 = sqnorm(sub(ti, tj));
-        const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-      }
+    for (long long p = threadIdx.x; p < M; p += blockDim.x) {
+      int i, jj;
+      pair_of(p, K, &i, &jj);
+      const double d2 = sqnorm(sub(pose_t(th_of(S.theta, b + i)), pose_t(th_of(S.theta, b + jj))));
+      const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -801,47 +409,77 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
   }
 }
 
-__global__ void svgd_kernel(DevProblem P, DevState S, double eta) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.J) return;
-  const int pop = P.part_pop[j];
+// Stein direction + update.  CTA = (population, block of 32 particles j).
+// For each 32-wide tile of partners i the CTA evaluates the 32x32 kernel
+// values once (glibc-exact exp) into shared memory; then 7 threads per j (one
+// per pose component) accumulate their component over i in order — the
+// reference's per-component left-to-right sums.
+constexpr int kSvgdJ = 32;
+__global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState S, double eta) {
+  const int pop = blockIdx.y;
   const int b = P.pop_off[pop], K = P.pop_off[pop + 1] - b;
+  const int j0 = blockIdx.x * kSvgdJ;
+  if (j0 >= K) return;
+  __shared__ double kv[kSvgdJ][kSvgdJ + 1];   // rbf value [i][j]
+  __shared__ double kq[kSvgdJ][kSvgdJ + 1];   // |q_i . q_j|
+  __shared__ double ti[kSvgdJ][7];            // partner poses
+  __shared__ double di[kSvgdJ][7];            // partner drifts
+  __shared__ double tj[kSvgdJ][7];            // own poses
+  __shared__ double dir[kSvgdJ][7];
+  const int tid = threadIdx.x;
+  const int jl = tid / 7, comp = tid % 7;
+  const int nj = min(kSvgdJ, K - j0);
+  for (int e = tid; e < nj * 7; e += blockDim.x) tj[e / 7][e % 7] = S.theta[7 * (b + j0 + e / 7) + e % 7];
   const double h = S.h[pop];
-  const double* thj = th_of(S.theta, j);
-  const V3 tj = pose_t(thj);
-  const Q4 qj = pose_q(thj);
-  double pt[3] = {0.0, 0.0, 0.0};
-  double pq[4] = {0.0, 0.0, 0.0, 0.0};
   const double two_h = 2.0 / h;
-  for (int ii = 0; ii < K; ++ii) {
-    const int i = b + ii;
-    const double* di = S.drift + 7 * i;
-    if (i == j) {
-      for (int a = 0; a < 3; ++a) pt[a] = pt[a] - di[a];
-      for (int a = 0; a < 4; ++a) pq[a] = pq[a] - di[3 + a];
-      continue;
+  double acc = 0.0;
+  for (int i0 = 0; i0 < K; i0 += kSvgdJ) {
+    const int ni = min(kSvgdJ, K - i0);
+    __syncthreads();
+    for (int e = tid; e < ni * 7; e += blockDim.x) {
+      ti[e / 7][e % 7] = S.theta[7 * (b + i0 + e / 7) + e % 7];
+      di[e / 7][e % 7] = S.drift[7 * (b + i0 + e / 7) + e % 7];
     }
-    const double* thi = th_of(S.theta, i);
-    const V3 ti = pose_t(thi);
-    const V3 diff = sub(ti, tj);
-    const double value = glibc_exp(-sqnorm(diff) / h);  // rbf_kernel (optim.cpp:120-125)
-    for (int a = 0; a < 3; ++a) pt[a] = pt[a] + (-di[a]) * value;
-    const double dt[3] = {tj.x - ti.x, tj.y - ti.y, tj.z - ti.z};
-    for (int a = 0; a < 3; ++a) pt[a] = pt[a] + (two_h * dt[a]) * value;
-    const Q4 qi = pose_q(thi);
-    const double dq = ((qi.w * qj.w + qi.x * qj.x) + qi.y * qj.y) + qi.z * qj.z;  // rotation_kernel
-    const double kq = fabs(dq);
-    for (int a = 0; a < 4; ++a) pq[a] = pq[a] + (-di[3 + a]) * kq;
+    __syncthreads();
+    for (int e = tid; e < ni * nj; e += blockDim.x) {
+      const int ii = e / nj, jj = e % nj;
+      const V3 a = V3{ti[ii][0], ti[ii][1], ti[ii][2]};
+      const V3 c = V3{tj[jj][0], tj[jj][1], tj[jj][2]};
+      kv[ii][jj] = glibc_exp(-sqnorm(sub(a, c)) / h);  // rbf_kernel (optim.cpp:120-125)
+      const double dq = ((ti[ii][3] * tj[jj][3] + ti[ii][4] * tj[jj][4]) + ti[ii][5] * tj[jj][5]) +
+                        ti[ii][6] * tj[jj][6];
+      kq[ii][jj] = fabs(dq);  // rotation_kernel (optim.cpp:127-131)
+    }
+    __syncthreads();
+    if (jl < nj) {
+      const int jg = j0 + jl;
+      for (int ii = 0; ii < ni; ++ii) {
+        const double d = di[ii][comp];
+        if (i0 + ii == jg) {
+          acc = acc - d;  // analytic self-term (optim.cpp:206-212)
+        } else if (comp < 3) {
+          const double v = kv[ii][jl];
+          acc = acc + (-d) * v;
+          acc = acc + (two_h * (tj[jl][comp] - ti[ii][comp])) * v;
+        } else {
+          acc = acc + (-d) * kq[ii][jl];
+        }
+      }
+    }
   }
-  double* out = S.theta_next + 7 * j;
-  out[0] = tj.x + eta * pt[0];
-  out[1] = tj.y + eta * pt[1];
-  out[2] = tj.z + eta * pt[2];
-  const Q4 qn = normalized(Q4{qj.w + eta * pq[0], qj.x + eta * pq[1], qj.y + eta * pq[2], qj.z + eta * pq[3]});
-  out[3] = qn.w;
-  out[4] = qn.x;
-  out[5] = qn.y;
-  out[6] = qn.z;
+  if (jl < nj) dir[jl][comp] = acc;
+  __syncthreads();
+  if (tid < nj) {
+    const int jg = b + j0 + tid;
+    double* out = S.theta_next + 7 * jg;
+    for (int a = 0; a < 3; ++a) out[a] = tj[tid][a] + eta * dir[tid][a];
+    const Q4 qn = normalized(Q4{tj[tid][3] + eta * dir[tid][3], tj[tid][4] + eta * dir[tid][4],
+                                tj[tid][5] + eta * dir[tid][5], tj[tid][6] + eta * dir[tid][6]});
+    out[3] = qn.w;
+    out[4] = qn.x;
+    out[5] = qn.y;
+    out[6] = qn.z;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -881,8 +519,7 @@ __global__ void bookkeeping_kernel(DevProblem P, DevState S, int stein_phase, in
       S.converged[j] = 0;
     } else {
       const double prev = S.prev_loss[j];
-      if (isfinite(prev) && prev > 0.0)
-        S.converged[j] = (fabs(S.loss[j] - prev) / prev <= P.conv_thr) ? 1 : 0;
+      if (isfinite(prev) && prev > 0.0) S.converged[j] = (fabs(S.loss[j] - prev) / prev <= P.conv_thr) ? 1 : 0;
     }
     S.prev_loss[j] = S.loss[j];
   }
@@ -905,8 +542,7 @@ __global__ void init_state_kernel(DevProblem P, DevState S) {
   S.n_col[j] = 0;
 }
 
-// FFMA peak probe: 16 independent chains per thread, immediate-free 3-register
-// form like the NN filter's FMAs (register operands, one reused across chains).
+// FFMA peak probe: 16 independent FFMA chains per thread.
 __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float a, float b) {
   float acc[16];
 #pragma unroll
@@ -958,6 +594,7 @@ void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st) {
   dbg_exp_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(x, y, n);
 }
 double host_glibc_exp(double x) { return glibc_exp(x); }
+
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st) {
   seed_rng_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(S.rng_state, S.rng_mti, seed, P.J);
 }
@@ -979,42 +616,10 @@ void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) 
       cudaFuncSetAttribute(minibatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, minibatch_smem_cap());
       attr_done = true;
     }
-    minibatch_kernel<true><<<P.J, 128, need, st>>>(P, S, m, P.n_obj);
+    minibatch_kernel<true><<<P.J, 128, need, st>>>(P, S, m);
   } else {
-    minibatch_kernel<false><<<P.J, 128, 0, st>>>(P, S, m, P.n_obj);
+    minibatch_kernel<false><<<P.J, 128, 0, st>>>(P, S, m);
   }
-}
-void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
-  nn_count_kernel<<<(P.J + 1 + 127) / 128, 128, 0, st>>>(P, S, plan);
-  size_t bytes = S.scan_tmp_bytes;
-  cub::DeviceScan::ExclusiveSum(S.scan_tmp, bytes, S.item_count, S.item_off, P.J + 1, st);
-  nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
-  cudaMemsetAsync(S.item_counter, 0, sizeof(int), st);
-  cudaMemsetAsync(S.refine_count, 0, sizeof(int), st);
-}
-size_t scan_temp_bytes(int n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr), n);
-  return bytes;
-}
-int nn_smem_bytes() { return kNnSmemBytes; }
-void nn_set_attrs() {
-  cudaFuncSetAttribute(nn_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmemBytes);
-}
-int nn_blocks_per_sm() {
-  int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, nn_filter_kernel, kNnThreads, kNnSmemBytes);
-  return n;
-}
-void launch_nn_filter(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st) {
-  nn_filter_kernel<<<grid, kNnThreads, kNnSmemBytes, st>>>(P, S, plan);
-}
-void launch_nn_merge(const DevProblem& P, DevState& S, const NnPlan& plan, int max_ns, cudaStream_t st) {
-  dim3 grid((max_ns + 127) / 128, P.J);
-  nn_merge_kernel<<<grid, 128, 0, st>>>(P, S, plan);
-}
-void launch_nn_refine(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st) {
-  nn_refine_kernel<<<grid, 256, 0, st>>>(P, S, plan);
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
   cost_kernel<<<P.J, kCostThreads, 0, st>>>(P, S, final_pass);
@@ -1022,10 +627,12 @@ void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t 
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {
   trace_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, k);
 }
-void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, cudaStream_t st) {
+void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, int max_pop,
+                 cudaStream_t st) {
   drift_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, gamma, n_ref);
   median_kernel<<<P.n_pop, 1024, 0, st>>>(P, S);
-  svgd_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, eta);
+  dim3 grid((max_pop + kSvgdJ - 1) / kSvgdJ, P.n_pop);
+  svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
   copy_theta_kernel<<<(7 * P.J + 255) / 256, 256, 0, st>>>(S.theta, S.theta_next, 7 * P.J);
 }
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st) {

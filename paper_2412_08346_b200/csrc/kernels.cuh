@@ -1,5 +1,6 @@
 // Device-side problem / state layout of the B200 AS-ICP solver and the host
-// launchers of its kernels (kernels.cu).  See DESIGN.md §3 for the HBM layout.
+// launchers of its kernels (kernels.cu, nn.cu).  See DESIGN.md §3 for the HBM
+// layout.
 #pragma once
 
 #include "dmath.cuh"
@@ -15,6 +16,7 @@ namespace asicp {
 struct DevProblem {
   int J;            // particles (all preshapes, preshape-major)
   int n_obj;        // |R|
+  int n_obj_pad;    // |R| rounded up to the NN subtile (padding rows are +inf)
   int n_scene;      // |C|
   int n_pop;        // Stein populations (= preshapes)
   const double* obj64;      // R, n_obj x 3
@@ -27,11 +29,11 @@ struct DevProblem {
   const Grid* grids;
   const float* sdf_values;
   const int* part_pre;      // particle -> preshape
-  const int64_t* part_surf_off;  // particle -> offset of its surface rows (J + 1)
+  const int64_t* part_surf_off;  // particle -> first surface row (rows padded to 32) (J + 1)
   const int* part_pop;      // particle -> population
   const int* pop_off;       // population -> first particle (n_pop + 1)
   const double* pop_logk1;  // log(K + 1) per population (host std::log)
-  double center[3];         // FP32 re-centring origin (object centroid)
+  double center[3];         // FP32 re-centring origin of the forward match (object centroid)
   double B_obj;             // max |r - center| over R (with slack)
   double com[3];
   double contact_tolerance;
@@ -60,31 +62,32 @@ struct DevState {
   double* prior;       // J x 7 prior log-gradient
   double* drift;       // J x 7
   double* h;           // per population bandwidth
-  double* S64;         // transformed contact surface, sum_j N_s(j) x 3
-  float4* Sq32;        // its FP32 queries (x, y, z, margin)
-  float4* Sc32;        // its FP32 candidates (-2x, -2y, -2z, |b|^2)
-  double* Bs;          // per particle max |s - center|
+  double* S64;         // transformed contact surface, padded rows x 3
+  float4* Sq32;        // its FP32 forward queries (x, y, z, margin), object-centred
+  float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred
+  double* ctr;         // J x 3 per-particle reverse-match centre (TCP in world)
+  double* Bs;          // per particle max |s - ctr|
   int* col_idx;        // J x n_scene colliding scene indices (scene order)
-  float4* col_q;       // J x n_scene FP32 reverse queries
+  float4* col_q;       // J x n_scene FP32 reverse queries (particle-centred)
   int* res_fwd;        // per surface row: NN position in the candidate set
   int* res_rev;        // J x n_scene: nearest surface index per colliding point
   uint64_t* rng_state; // J x 312
   int* rng_mti;        // J
-  int* pool_idx;       // J x n_obj minibatch object indices (sample order)
-  float4* pool32;      // J x n_obj gathered FP32 candidates
+  int* pool_idx;       // J x n_obj_pad minibatch object indices (sample order)
+  float4* pool32;      // J x n_obj_pad gathered FP32 candidates (+inf padded)
   int* fy_scratch;     // J x n_obj Fisher-Yates scratch (large clouds only)
   const int* pool_map; // = pool_idx when this iteration's forward match is pooled
-  NnItem* items;
-  int* item_count;     // J + 1
-  int* item_off;       // J + 1
-  int* item_counter;
+  NnItem* items[2];    // work lists: [0] forward / final, [1] reverse
+  int* item_count[2];  // J + 1 each
+  int* item_off[2];    // J + 1 each
+  int* item_counter;   // 2 ints
   void* scan_tmp;
   size_t scan_tmp_bytes;
-  NnPartial* partials; // sum_j N_s(j) x max chunks
+  NnPartial* partials; // padded surface rows x max chunks
   int4* refine_list;
   int* refine_count;
   int refine_cap;
-  unsigned long long* stats;  // [0] windows > 1, [1] full refines, [2] queries, [3] canonical-order ties
+  unsigned long long* stats;  // [0] windows > 1, [1] full refines, [2] queries, [3] canonical-order ties, [4] pairs
   double* trace_theta;
   double* trace_loss;
   int* trace_col;
@@ -99,6 +102,8 @@ struct NnPlan {
   int nchunks;   // forward candidate chunks (split-K)
   int chunk;     // candidates per chunk (multiple of kNnTile)
   int fp64_mode; // resolve every query by FP64 brute force (validation mode)
+  int max_ns;    // largest contact surface (merge grid)
+  int iter;      // iteration index (diagnostic counters)
 };
 
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st);
@@ -107,21 +112,25 @@ void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
 int minibatch_smem_cap();
+void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
+void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
+void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, int max_pop,
+                 cudaStream_t st);
+void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
+void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
+void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st);
+double host_glibc_exp(double x);
+double run_ffma_peak(int iters);
+
+// nn.cu
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st);
 size_t scan_temp_bytes(int n);
 int nn_smem_bytes();
 void nn_set_attrs();
 int nn_blocks_per_sm();
-void launch_nn_filter(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st);
-void launch_nn_merge(const DevProblem& P, DevState& S, const NnPlan& plan, int max_ns, cudaStream_t st);
-void launch_nn_refine(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, cudaStream_t st);
-void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
-void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
-void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, cudaStream_t st);
-void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
-void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st);
-double host_glibc_exp(double x);
-double run_ffma_peak(int iters);
-void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
+// Launches the forward/final list (and the reverse list when kind == 0),
+// the merge (nchunks > 1) and the FP64 refine.  Returns the launch count.
+int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, int refine_grid, cudaStream_t st,
+              cudaEvent_t ev_begin, cudaEvent_t ev_end);
 
 }  // namespace asicp

@@ -1,0 +1,487 @@
+// Certified brute-force nearest neighbour (NN) on B200 — the hot loop of
+// optimize_grasp: the forward match of match_surface_to_pool
+// (grasp.cpp:92-106), the reverse match of collision_loss_and_gradients
+// (grasp.cpp:68-84) and the final full-cloud ranking (grasp.cpp:263-281),
+// replacing the per-call kd-trees of spatial_index.cpp:14-105.
+//
+// FP32 filter, FP64 decision:
+//   * candidates (-2b, |b|^2) stream through shared memory in 4 KB tiles
+//     by TMA bulk copies (cp.async.bulk + mbarrier, 4-stage ring);
+//   * each thread holds Q queries in registers; one (query, candidate) pair
+//     is 3 FFMA + 1 FMNMX (the expansion form |b|^2 - 2 a.b), branch-free;
+//   * every 32 candidates (a subtile) each query folds its subtile minimum
+//     into a running top-3 of subtile minima (b1 <= b2 <= b3, subtiles s1, s2);
+//   * at the end the reference's answer — min FP64 (p - q).squaredNorm(),
+//     ties to the lowest position (spatial_index.cpp:69-83) — is provably in
+//     the window {d32 <= b1 + 2E} (2E = the query's margin).  If b3 > b1 + 2E
+//     the window lies in subtiles s1/s2, which are rescanned; a window of one
+//     is certified, larger windows are decided in FP64 with the reference
+//     formula, and the rare b3 <= b1 + 2E case goes to a full FP64 rescan.
+#include "common.cuh"
+
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace asicp {
+
+constexpr int kFwdQ = 8;                     // forward / final: 8 queries per thread
+constexpr int kRevQ = 2;                     // reverse (few colliding points): 2
+constexpr int kFwdQB = kNnThreads * kFwdQ;   // queries per forward item
+constexpr int kRevQB = kNnThreads * kRevQ;   // queries per reverse item
+constexpr int kNnSmem = kNnStages * kNnTile * 16;
+
+// ---------------------------------------------------------------------------
+// Work planning: per particle item counts -> exclusive scans -> item lists.
+// ---------------------------------------------------------------------------
+__global__ void nn_count_kernel(DevProblem P, DevState S, NnPlan plan) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > P.J) return;
+  int fwd = 0, rev = 0;
+  if (j < P.J && (plan.kind == 2 || S.active[j])) {
+    if (plan.kind != 2 && S.n_col[j] > 0)
+      rev = ceil_div(S.n_col[j], kRevQB);
+    else
+      fwd = ceil_div(surf_count(P, j), kFwdQB) * plan.nchunks;
+  }
+  S.item_count[0][j] = fwd;
+  S.item_count[1][j] = rev;
+}
+
+__global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.J) return;
+  const int64_t so = P.part_surf_off[j];
+  const int ns = surf_count(P, j);
+  if (S.item_count[1][j] > 0) {
+    const int nq = S.n_col[j];
+    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
+    int w = S.item_off[1][j];
+    for (int b = 0; b < S.item_count[1][j]; ++b) {
+      NnItem it;
+      it.q = S.col_q + row + b * kRevQB;
+      it.nq = min(kRevQB, nq - b * kRevQB);
+      it.c = S.Sc32 + so;
+      it.nc = ns;
+      it.c_base = 0;
+      it.kind = 1;
+      it.owner = j;
+      it.q_first = b * kRevQB;
+      it.chunk = 0;
+      it.nchunks = 1;
+      S.items[1][w++] = it;
+    }
+  }
+  if (S.item_count[0][j] > 0) {
+    const float4* cands = plan.pooled ? S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad : P.obj_cand;
+    int w = S.item_off[0][j];
+    for (int b = 0; b < ceil_div(ns, kFwdQB); ++b)
+      for (int s = 0; s < plan.nchunks; ++s) {
+        NnItem it;
+        it.q = S.Sq32 + so + b * kFwdQB;
+        it.nq = min(kFwdQB, ns - b * kFwdQB);
+        const int c0 = s * plan.chunk;
+        it.c = cands + c0;
+        it.nc = min(plan.chunk, plan.m - c0);
+        it.c_base = c0;
+        it.kind = plan.kind;
+        it.owner = j;
+        it.q_first = b * kFwdQB;
+        it.chunk = s;
+        it.nchunks = plan.nchunks;
+        S.items[0][w++] = it;
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 decision with the reference formula.
+// ---------------------------------------------------------------------------
+struct NnGeom {
+  const double* qpt;     // query point (FP64)
+  const double* cbase;   // candidate FP64 rows
+  const int* cmap;       // candidate position -> row (minibatch pool), or null
+};
+
+__device__ __forceinline__ NnGeom nn_geom(const DevProblem& P, const DevState& S, const NnPlan& plan, int kind,
+                                          int j, int qlocal) {
+  NnGeom g;
+  const int64_t so = P.part_surf_off[j];
+  if (kind == 1) {
+    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
+    g.qpt = P.scene64 + 3 * static_cast<int64_t>(S.col_idx[row + qlocal]);
+    g.cbase = S.S64 + 3 * so;
+    g.cmap = nullptr;
+  } else {
+    g.qpt = S.S64 + 3 * (so + qlocal);
+    g.cbase = P.obj64;
+    g.cmap = (kind == 0 && plan.pooled) ? S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad : nullptr;
+  }
+  return g;
+}
+
+// spatial_index.cpp:69: (points[idx] - query).squaredNorm()
+__device__ __forceinline__ double nn_d64(const NnGeom& g, int pos) {
+  const int64_t r = g.cmap ? g.cmap[pos] : pos;
+  const V3 p = load3(g.cbase, r);
+  return sqnorm(sub(p, V3{g.qpt[0], g.qpt[1], g.qpt[2]}));
+}
+
+__device__ __forceinline__ int* nn_result_slot(const DevProblem& P, const DevState& S, int kind, int j, int qlocal) {
+  if (kind == 1) return S.res_rev + static_cast<int64_t>(j) * P.n_scene + qlocal;
+  return S.res_fwd + P.part_surf_off[j] + qlocal;
+}
+
+// Window decision: strictly closer wins, equal distance -> lowest position.
+// Exact ties between distinct rows of a canonical-order forward set are
+// counted (the reference would break them by its sampled pool order).
+__device__ __forceinline__ int nn_decide(const NnGeom& g, const int* pos, int n, bool tie_sensitive,
+                                         unsigned long long* stats) {
+  if (n == 1) return pos[0];
+  atomicAdd(stats + 0, 1ull);
+  double best = 0.0;
+  int bi = -1;
+  bool tie = false;
+  for (int e = 0; e < n; ++e) {
+    const double d = nn_d64(g, pos[e]);
+    if (bi >= 0 && d == best) tie = true;
+    if (bi < 0 || d < best || (d == best && pos[e] < bi)) {
+      if (bi < 0 || d < best) tie = false;
+      best = d;
+      bi = pos[e];
+    }
+  }
+  if (tie && tie_sensitive) atomicAdd(stats + 3, 1ull);
+  return bi;
+}
+
+// stats[5 + kind]: refines per match kind; stats[8 + reason]: 0 mode, 1 top-3
+// overflow, 2 window > kNnL, 3 merge overflow.
+__device__ __forceinline__ void push_refine(DevState& S, int kind, int j, int qlocal, int reason, int iter) {
+  const int slot = atomicAdd(S.refine_count, 1);
+  if (slot < S.refine_cap) S.refine_list[slot] = make_int4(kind, j, qlocal, 0);
+  atomicAdd(S.stats + 1, 1ull);
+  atomicAdd(S.stats + 5 + kind, 1ull);
+  atomicAdd(S.stats + 8 + reason, 1ull);
+  atomicAdd(S.stats + 16 + min(iter, 239), 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// TMA / mbarrier primitives
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ float d32(float qx, float qy, float qz, float4 v) {
+  return __fmaf_rn(qx, v.x, __fmaf_rn(qy, v.y, __fmaf_rn(qz, v.z, v.w)));
+}
+
+// ---------------------------------------------------------------------------
+// The filter kernel (persistent over one work list).
+// ---------------------------------------------------------------------------
+template <int Q>
+__global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, DevState S, NnPlan plan, int list) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float4* tiles = reinterpret_cast<float4*>(smem_raw);
+  __shared__ __align__(8) uint64_t full_bar[kNnStages];
+  __shared__ int s_item;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kNnStages; ++s) mbar_init(&full_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int n_items = S.item_off[list][P.J];
+  const NnItem* items = S.items[list];
+  uint32_t gtile = 0;
+  for (;;) {
+    if (tid == 0) s_item = atomicAdd(S.item_counter + list, 1);
+    __syncthreads();
+    const int it = s_item;
+    __syncthreads();
+    if (it >= n_items) break;
+    const NnItem w = items[it];
+    const int nc_pad = round_up(w.nc, kSub);  // candidate arrays are padded with +inf rows
+    const int ntiles = ceil_div(nc_pad, kNnTile);
+    if (tid == 0) {
+      atomicAdd(S.stats + 2, static_cast<unsigned long long>(w.chunk == 0 ? w.nq : 0));
+      atomicAdd(S.stats + 4, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
+      for (int t = 0; t < ntiles && t < kNnStages; ++t) {
+        const uint32_t s = (gtile + t) % kNnStages;
+        const int n_in = min(kNnTile, nc_pad - t * kNnTile);
+        tma_load_1d(tiles + s * kNnTile, w.c + t * kNnTile, n_in * 16, &full_bar[s]);
+      }
+    }
+    float qx[Q], qy[Q], qz[Q], b1[Q], b2[Q], b3[Q];
+    int s12[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      const int qi = tid + k * kNnThreads;
+      const float4 q = qi < w.nq ? w.q[qi] : make_float4(0.f, 0.f, 0.f, 0.f);
+      qx[k] = q.x;
+      qy[k] = q.y;
+      qz[k] = q.z;
+      b1[k] = b2[k] = b3[k] = INFINITY;
+      s12[k] = 0;
+    }
+    for (int t = 0; t < ntiles; ++t) {
+      const uint32_t G = gtile + t;
+      const uint32_t stage = G % kNnStages;
+      mbar_wait(&full_bar[stage], (G / kNnStages) & 1u);
+      const float4* tile = tiles + stage * kNnTile;
+      const int nsub = min(kNnTile, nc_pad - t * kNnTile) / kSub;
+      for (int sub = 0; sub < nsub; ++sub) {
+        const float4* sp = tile + sub * kSub;
+        float tm[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) tm[k] = INFINITY;
+#pragma unroll 8
+        for (int c = 0; c < kSub; ++c) {
+          const float4 v = sp[c];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) tm[k] = fminf(tm[k], d32(qx[k], qy[k], qz[k], v));
+        }
+        const int sid = t * (kNnTile / kSub) + sub;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          // Running top-3 of subtile minima (strict < keeps the earliest).
+          const bool lt1 = tm[k] < b1[k];
+          const bool lt2 = tm[k] < b2[k];
+          b3[k] = lt2 ? b2[k] : fminf(b3[k], tm[k]);
+          const int s1 = s12[k] & 0xffff;
+          const int s2 = lt1 ? s1 : (lt2 ? sid : (s12[k] >> 16));
+          b2[k] = lt1 ? b1[k] : (lt2 ? tm[k] : b2[k]);
+          b1[k] = lt1 ? tm[k] : b1[k];
+          s12[k] = (lt1 ? sid : s1) | (s2 << 16);
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && t + kNnStages < ntiles) {
+        const int tn = t + kNnStages;
+        const int n2 = min(kNnTile, nc_pad - tn * kNnTile);
+        tma_load_1d(tiles + stage * kNnTile, w.c + tn * kNnTile, n2 * 16, &full_bar[stage]);
+      }
+    }
+    gtile += ntiles;
+    // Emit: rescan the subtiles that can hold window members (fully unrolled
+    // so the per-query state stays in registers).
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      const int qi = tid + k * kNnThreads;
+      if (qi >= w.nq) continue;
+      const float mg = w.q[qi].w;
+      const float thr = __fadd_ru(b1[k], mg);
+      bool overflow = b3[k] <= thr;
+      int reason = overflow ? 1 : 0;
+      int pos[kNnL];
+      float dd[kNnL];
+      int n = 0;
+      if (!overflow) {
+        const int nscan = b2[k] <= thr ? 2 : 1;
+        for (int r = 0; r < nscan; ++r) {
+          const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
+          for (int c = 0; c < kSub; ++c) {
+            const int p = sid * kSub + c;
+            if (p >= w.nc) break;
+            const float d = d32(qx[k], qy[k], qz[k], w.c[p]);
+            if (d <= thr) {
+              if (n < kNnL) {
+                pos[n] = p + w.c_base;
+                dd[n] = d;
+                ++n;
+              } else {
+                overflow = true;
+                reason = 2;
+              }
+            }
+          }
+        }
+      }
+      const int qlocal = w.q_first + qi;
+      if (reason == 1 && atomicCAS(reinterpret_cast<unsigned long long*>(S.stats + 200), 0ull, 1ull) == 0ull) {
+        unsigned long long* dbg = S.stats + 201;
+        dbg[0] = plan.iter;
+        dbg[1] = w.owner;
+        dbg[2] = qlocal;
+        dbg[3] = __float_as_uint(b1[k]);
+        dbg[4] = __float_as_uint(b2[k]);
+        dbg[5] = __float_as_uint(b3[k]);
+        dbg[6] = __float_as_uint(thr);
+        dbg[7] = w.nc;
+        dbg[8] = s12[k];
+        dbg[9] = __float_as_uint(qx[k]);
+        dbg[10] = __float_as_uint(qy[k]);
+        dbg[11] = __float_as_uint(qz[k]);
+        dbg[12] = __float_as_uint(mg);
+        dbg[13] = w.c_base;
+      }
+      if (w.nchunks == 1) {
+        if (plan.fp64_mode || overflow || n == 0) {
+          push_refine(S, w.kind, w.owner, qlocal, overflow ? reason : 0, plan.iter);
+        } else {
+          const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
+          *nn_result_slot(P, S, w.kind, w.owner, qlocal) = nn_decide(g, pos, n, w.kind == 0 && !plan.pooled, S.stats);
+        }
+      } else {
+        NnPartial pr;
+        pr.b1 = b1[k];
+        pr.count = overflow ? -1 : n;
+        for (int e = 0; e < kNnL; ++e) {
+          pr.pos[e] = e < n ? pos[e] : 0;
+          pr.d[e] = e < n ? dd[e] : INFINITY;
+        }
+        S.partials[(P.part_surf_off[w.owner] + qlocal) * static_cast<int64_t>(w.nchunks) + w.chunk] = pr;
+      }
+    }
+  }
+}
+
+// Merge per-chunk windows of forward/final queries (nchunks > 1).
+__global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
+  const int j = blockIdx.y;
+  if (plan.kind != 2 && (!S.active[j] || S.n_col[j] > 0)) return;
+  const int64_t so = P.part_surf_off[j];
+  const int ns = surf_count(P, j);
+  const int qlocal = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qlocal >= ns) return;
+  const NnPartial* pr = S.partials + (so + qlocal) * static_cast<int64_t>(plan.nchunks);
+  float b1 = INFINITY;
+  for (int s = 0; s < plan.nchunks; ++s) b1 = fminf(b1, pr[s].b1);
+  const float thr = __fadd_ru(b1, S.Sq32[so + qlocal].w);
+  constexpr int kMax = 32;
+  int pos[kMax];
+  int n = 0;
+  bool overflow = false;
+  for (int s = 0; s < plan.nchunks; ++s) {
+    const NnPartial p = pr[s];
+    if (p.b1 > thr) continue;
+    if (p.count < 0) {
+      overflow = true;
+      continue;
+    }
+    for (int e = 0; e < p.count; ++e)
+      if (p.d[e] <= thr) {
+        if (n < kMax)
+          pos[n++] = p.pos[e];
+        else
+          overflow = true;
+      }
+  }
+  if (plan.fp64_mode || overflow || n == 0) {
+    push_refine(S, plan.kind, j, qlocal, overflow ? 3 : 0, plan.iter);
+    return;
+  }
+  const NnGeom g = nn_geom(P, S, plan, plan.kind, j, qlocal);
+  S.res_fwd[so + qlocal] = nn_decide(g, pos, n, plan.kind == 0 && !plan.pooled, S.stats);
+}
+
+// Full FP64 rescan (overflowing windows, and the FP64 validation mode):
+// one warp per query, lexicographic (distance, position) minimum.
+__global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int total = min(*S.refine_count, S.refine_cap);
+  for (int e = warp; e < total; e += nwarps) {
+    const int4 r = S.refine_list[e];
+    const int kind = r.x, j = r.y, qlocal = r.z;
+    const NnGeom g = nn_geom(P, S, plan, kind, j, qlocal);
+    const int nc = kind == 1 ? surf_count(P, j) : plan.m;
+    double best = INFINITY;
+    int bi = 0x7fffffff;
+    for (int c = lane; c < nc; c += 32) {
+      const double d = nn_d64(g, c);
+      if (d < best || (d == best && c < bi)) {
+        best = d;
+        bi = c;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob < best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) *nn_result_slot(P, S, kind, j, qlocal) = bi;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
+  nn_count_kernel<<<(P.J + 1 + 127) / 128, 128, 0, st>>>(P, S, plan);
+  for (int l = 0; l < 2; ++l) {
+    size_t bytes = S.scan_tmp_bytes;
+    cub::DeviceScan::ExclusiveSum(S.scan_tmp, bytes, S.item_count[l], S.item_off[l], P.J + 1, st);
+  }
+  nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
+  cudaMemsetAsync(S.item_counter, 0, 2 * sizeof(int), st);
+  cudaMemsetAsync(S.refine_count, 0, sizeof(int), st);
+}
+
+size_t scan_temp_bytes(int n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr), n);
+  return bytes;
+}
+
+int nn_smem_bytes() { return kNnSmem; }
+
+void nn_set_attrs() {
+  cudaFuncSetAttribute(nn_filter_kernel<kFwdQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
+  cudaFuncSetAttribute(nn_filter_kernel<kRevQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
+}
+
+int nn_blocks_per_sm() {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, nn_filter_kernel<kFwdQ>, kNnThreads, kNnSmem);
+  return n;
+}
+
+int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, int refine_grid, cudaStream_t st,
+              cudaEvent_t ev_begin, cudaEvent_t ev_end) {
+  int n = 0;
+  if (ev_begin) cudaEventRecord(ev_begin, st);
+  nn_filter_kernel<kFwdQ><<<grid, kNnThreads, kNnSmem, st>>>(P, S, plan, 0);
+  ++n;
+  if (ev_end) cudaEventRecord(ev_end, st);
+  if (plan.kind == 0) {
+    nn_filter_kernel<kRevQ><<<grid, kNnThreads, kNnSmem, st>>>(P, S, plan, 1);
+    ++n;
+  }
+  if (plan.nchunks > 1) {
+    dim3 mg((plan.max_ns + 127) / 128, P.J);
+    nn_merge_kernel<<<mg, 128, 0, st>>>(P, S, plan);
+    ++n;
+  }
+  nn_refine_kernel<<<refine_grid, 256, 0, st>>>(P, S, plan);
+  return n + 1;
+}
+
+}  // namespace asicp

@@ -9,6 +9,7 @@
 // dependent branch is resolved on the device through work lists).
 #include "asicp.h"
 #include "asicp_debug.h"
+#include "common.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
 
@@ -26,6 +27,9 @@
 namespace {
 
 using namespace asicp;
+
+constexpr int kSubRows = kSub;
+constexpr int kStats = 256;  // [0..15] NN counters, [16..255] full rescans per iteration
 
 struct InvalidArgument : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -103,10 +107,11 @@ struct asicp_ctx {
   int profile = 0;
   int num_sms = 148;
   int nn_grid = 296;
+  int max_chunks = 16;
 
   // Prepared problem (host side).
   bool prepared = false;
-  int J = 0, n_obj = 0, n_scene = 0, n_pre = 0, k_max = 0, k_stein = 0;
+  int J = 0, n_obj = 0, n_obj_pad = 0, n_scene = 0, n_pre = 0, k_max = 0, k_stein = 0, max_pop = 0;
   int max_ns = 0;
   int64_t total_surf = 0;
   int record_trace = 0;
@@ -125,8 +130,9 @@ struct asicp_ctx {
   Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
-      Bs, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items, item_count,
-      item_off, item_counter, scan_tmp, partials, refine_list, refine_count, stats, trace_theta, trace_loss, trace_col,
+      Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items0, items1,
+      item_count, item_off, item_counter, scan_tmp, partials, refine_list, refine_count, stats, trace_theta,
+      trace_loss, trace_col,
       final_loss, final_free;
 
   cudaGraphExec_t graph_exec = nullptr;
@@ -137,6 +143,7 @@ struct asicp_ctx {
   asicp_stats last_stats{};
   double nn_pairs_planned = 0.0;
   int64_t launches = 0;
+  unsigned long long raw_stats[kStats] = {};
 
   ~asicp_ctx() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
@@ -149,8 +156,8 @@ struct asicp_ctx {
     Buf* all[] = {&obj64, &obj_cand, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
-                  &S64, &Sq32, &Sc32, &Bs, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
-                  &pool_idx, &pool32, &fy_scratch, &items, &item_count, &item_off, &item_counter, &scan_tmp,
+                  &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
+                  &pool_idx, &pool32, &fy_scratch, &items0, &items1, &item_count, &item_off, &item_counter, &scan_tmp,
                   &partials, &refine_list, &refine_count, &stats, &trace_theta, &trace_loss, &trace_col,
                   &final_loss, &final_free};
     for (Buf* b : all) b->release();
@@ -241,7 +248,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   for (int64_t i = 0; i < p.n_object; ++i)
     for (int a = 0; a < 3; ++a) center[a] += obj[3 * i + a];
   for (int a = 0; a < 3; ++a) center[a] /= static_cast<double>(p.n_object);
-  std::vector<float4> cand(p.n_object);
+  // Candidate rows are padded to the NN subtile with +inf (never selected).
+  c->n_obj_pad = static_cast<int>((p.n_object + kSubRows - 1) / kSubRows * kSubRows);
+  std::vector<float4> cand(c->n_obj_pad, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
   double bmax = 0.0;
   for (int64_t i = 0; i < p.n_object; ++i) {
     const double bx = obj[3 * i] - center[0], by = obj[3 * i + 1] - center[1], bz = obj[3 * i + 2] - center[2];
@@ -259,6 +268,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   std::vector<int> pre_off(n_pre + 1, 0), pre_sdf(n_pre);
   std::vector<double> tcp(3 * n_pre);
   c->max_ns = 0;
+  c->max_pop = 0;
   for (int i = 0; i < n_pre; ++i) {
     const asicp_preshape& s = p.preshapes[i];
     pre_off[i] = static_cast<int>(surf.size() / 3);
@@ -304,9 +314,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
       part_pre.push_back(i);
       part_pop.push_back(i);
       part_surf_off.push_back(so);
-      so += p.preshapes[i].n_surface;
+      so += (p.preshapes[i].n_surface + kSubRows - 1) / kSubRows * kSubRows;  // rows padded to the subtile
     }
     logk1[i] = std::log(static_cast<double>(p.init_counts[i]) + 1.0);  // optim.cpp:143
+    c->max_pop = std::max(c->max_pop, static_cast<int>(p.init_counts[i]));
   }
   pop_off[n_pre] = static_cast<int>(part_pre.size());
   part_surf_off.push_back(so);
@@ -335,7 +346,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   int base_items = 0;
   for (int i = 0; i < n_pre; ++i)
     base_items += static_cast<int>(p.init_counts[i] * ((p.preshapes[i].n_surface + kNnQB - 1) / kNnQB));
-  c->nchunks_max = std::clamp((4 * c->nn_grid + base_items - 1) / std::max(base_items, 1), 1, 16);
+  c->nchunks_max = std::clamp((4 * c->nn_grid + base_items - 1) / std::max(base_items, 1), 1, c->max_chunks);
 
   // State buffers.
   const size_t Jz = static_cast<size_t>(J);
@@ -355,6 +366,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->Sq32.ensure(static_cast<size_t>(so) * 16);
   c->Sc32.ensure(static_cast<size_t>(so) * 16);
   c->Bs.ensure(Jz * 8);
+  c->ctr.ensure(Jz * 3 * 8);
   const size_t jscene = Jz * static_cast<size_t>(c->n_scene);
   c->col_idx.ensure(jscene * 4);
   c->col_q.ensure(jscene * 16);
@@ -362,24 +374,23 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->res_fwd.ensure(static_cast<size_t>(so) * 4);
   c->rng_state.ensure(Jz * mt::kN * 8);
   c->rng_mti.ensure(Jz * 4);
-  const size_t jobj = Jz * static_cast<size_t>(c->n_obj);
+  const size_t jobj = Jz * static_cast<size_t>(c->n_obj_pad);
   c->pool_idx.ensure(jobj * 4);
   c->pool32.ensure(jobj * 16);
-  if (static_cast<size_t>(c->n_obj) * 4 > static_cast<size_t>(minibatch_smem_cap())) c->fy_scratch.ensure(jobj * 4);
-  // Work items: forward <= base_items * nchunks, reverse <= J * ceil(n_scene / QB).
-  const size_t max_items = std::max<size_t>(static_cast<size_t>(base_items) * c->nchunks_max,
-                                            Jz * ((c->n_scene + kNnQB - 1) / kNnQB)) +
-                           Jz;
-  c->items.ensure(max_items * sizeof(NnItem));
-  c->item_count.ensure((Jz + 1) * 4);
-  c->item_off.ensure((Jz + 1) * 4);
-  c->item_counter.ensure(4);
+  if (static_cast<size_t>(c->n_obj) * 4 > static_cast<size_t>(minibatch_smem_cap()))
+    c->fy_scratch.ensure(Jz * static_cast<size_t>(c->n_obj) * 4);
+  // Work items: forward <= base_items * nchunks; reverse <= J * ceil(n_scene / 256).
+  c->items0.ensure((static_cast<size_t>(base_items) * c->nchunks_max + Jz) * sizeof(NnItem));
+  c->items1.ensure((Jz * ((c->n_scene + 255) / 256) + Jz) * sizeof(NnItem));
+  c->item_count.ensure(2 * (Jz + 1) * 4);
+  c->item_off.ensure(2 * (Jz + 1) * 4);
+  c->item_counter.ensure(2 * 4);
   c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
   c->partials.ensure(static_cast<size_t>(so) * c->nchunks_max * sizeof(NnPartial));
   const size_t refine_cap = std::min<size_t>(static_cast<size_t>(so) + jscene, 64ull << 20);
   c->refine_list.ensure(refine_cap * sizeof(int4));
   c->refine_count.ensure(4);
-  c->stats.ensure(8 * sizeof(unsigned long long));
+  c->stats.ensure(kStats * sizeof(unsigned long long));
   if (c->record_trace) {
     const size_t rows = static_cast<size_t>(c->k_max) * Jz;
     c->trace_theta.ensure(std::max<size_t>(rows, 1) * 7 * 8);
@@ -393,6 +404,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   DevProblem& P = c->P;
   P.J = J;
   P.n_obj = c->n_obj;
+  P.n_obj_pad = c->n_obj_pad;
   P.n_scene = c->n_scene;
   P.n_pop = n_pre;
   P.obj64 = c->obj64.as<double>();
@@ -444,6 +456,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.Sq32 = c->Sq32.as<float4>();
   S.Sc32 = c->Sc32.as<float4>();
   S.Bs = c->Bs.as<double>();
+  S.ctr = c->ctr.as<double>();
   S.col_idx = c->col_idx.as<int>();
   S.col_q = c->col_q.as<float4>();
   S.res_fwd = c->res_fwd.as<int>();
@@ -454,9 +467,12 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.pool32 = c->pool32.as<float4>();
   S.fy_scratch = c->fy_scratch.as<int>();
   S.pool_map = nullptr;
-  S.items = c->items.as<NnItem>();
-  S.item_count = c->item_count.as<int>();
-  S.item_off = c->item_off.as<int>();
+  S.items[0] = c->items0.as<NnItem>();
+  S.items[1] = c->items1.as<NnItem>();
+  S.item_count[0] = c->item_count.as<int>();
+  S.item_count[1] = c->item_count.as<int>() + (Jz + 1);
+  S.item_off[0] = c->item_off.as<int>();
+  S.item_off[1] = c->item_off.as<int>() + (Jz + 1);
   S.item_counter = c->item_counter.as<int>();
   S.scan_tmp = c->scan_tmp.p;
   S.scan_tmp_bytes = c->scan_tmp.bytes;
@@ -507,29 +523,25 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   nch = static_cast<int>((m + chunk - 1) / chunk);
   plan.nchunks = nch;
   plan.chunk = chunk;
+  plan.max_ns = c->max_ns;
   return plan;
 }
 
-// Enqueue one NN round (plan, optional minibatch, filter, merge, refine).
+// Enqueue one NN round (plan, optional minibatch, filter(s), merge, refine).
+// In profile mode the forward/final filter launch is bracketed by events
+// (the roofline kernel of bench.py).
 void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
   cudaStream_t st = c->stream;
   launch_nn_plan(c->P, c->S, plan, st);
   if (minibatch_m > 0) launch_minibatch(c->P, c->S, minibatch_m, st);
-  const bool timed = c->profile && !capture;
-  if (timed) {
-    std::pair<cudaEvent_t, cudaEvent_t> e;
+  std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
+  if (c->profile && !capture) {
     CUDA_OK(cudaEventCreate(&e.first));
     CUDA_OK(cudaEventCreate(&e.second));
-    CUDA_OK(cudaEventRecord(e.first, st));
-    launch_nn_filter(c->P, c->S, plan, c->nn_grid, st);
-    CUDA_OK(cudaEventRecord(e.second, st));
     c->nn_events.push_back(e);
-  } else {
-    launch_nn_filter(c->P, c->S, plan, c->nn_grid, st);
   }
-  if (plan.nchunks > 1) launch_nn_merge(c->P, c->S, plan, c->max_ns, st);
-  launch_nn_refine(c->P, c->S, plan, 2 * c->num_sms, st);
-  c->launches += 6 + (minibatch_m > 0) + (plan.nchunks > 1);
+  const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.first, e.second);
+  c->launches += 4 + n + (minibatch_m > 0);
 }
 
 // The whole optimize_grasp as a kernel sequence on c->stream.
@@ -540,7 +552,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
   c->launches = 0;
   CUDA_OK(cudaMemcpyAsync(S.theta, c->init_theta_d.p, static_cast<size_t>(c->J) * 7 * 8, cudaMemcpyDeviceToDevice,
                           st));
-  CUDA_OK(cudaMemsetAsync(S.stats, 0, 8 * sizeof(unsigned long long), st));
+  CUDA_OK(cudaMemsetAsync(S.stats, 0, kStats * sizeof(unsigned long long), st));
   launch_init_state(P, S, st);
   launch_seed_rng(P, S, c->seed, st);
   c->launches += 2;
@@ -551,7 +563,8 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
     launch_pose_prep(P, S, 0, st);
     launch_collide(P, S, 0, 0, st);
     S.pool_map = pooled ? S.pool_idx : nullptr;
-    const NnPlan plan = make_plan(c, 0, m, pooled);
+    NnPlan plan = make_plan(c, 0, m, pooled);
+    plan.iter = k;
     enqueue_nn(c, plan, pooled ? static_cast<int>(m) : 0, capture);
     launch_cost(P, S, 0, st);
     c->launches += 3;
@@ -560,7 +573,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
       ++c->launches;
     }
     if (stein) {
-      launch_svgd(P, S, c->gammas[k], c->n_ref, c->eta_stein, st);
+      launch_svgd(P, S, c->gammas[k], c->n_ref, c->eta_stein, c->max_pop, st);
       c->launches += 4;
     } else {
       launch_sgd(P, S, st);
@@ -573,7 +586,8 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
   S.pool_map = nullptr;
   launch_pose_prep(P, S, 1, st);
   launch_collide(P, S, 1, 1, st);
-  const NnPlan fin = make_plan(c, 2, c->n_obj, false);
+  NnPlan fin = make_plan(c, 2, c->n_obj, false);
+  fin.iter = c->k_max;
   enqueue_nn(c, fin, 0, capture);
   launch_cost(P, S, 1, st);
   c->launches += 3;
@@ -615,7 +629,7 @@ void run(asicp_ctx* c, asicp_solution* out) {
   const int J = c->J;
   std::vector<double> theta(7 * static_cast<size_t>(J)), floss(J);
   std::vector<int> ffree(J), conv(J);
-  unsigned long long stats[8];
+  unsigned long long stats[kStats];
   CUDA_OK(cudaMemcpyAsync(theta.data(), c->S.theta, theta.size() * 8, cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaMemcpyAsync(floss.data(), c->S.final_loss, floss.size() * 8, cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaMemcpyAsync(ffree.data(), c->S.final_free, ffree.size() * 4, cudaMemcpyDeviceToHost, st));
@@ -679,6 +693,7 @@ void run(asicp_ctx* c, asicp_solution* out) {
   out->nn_full_refines = static_cast<int64_t>(stats[1]);
   out->nn_queries = static_cast<int64_t>(stats[2]);
   out->nn_pool_ties = static_cast<int64_t>(stats[3]);
+  std::memcpy(c->raw_stats, stats, sizeof(stats));
   out->nn_pairs = static_cast<double>(stats[4]);
   s.nn_pairs = out->nn_pairs;
 }
@@ -738,6 +753,9 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
     case ASICP_OPT_USE_GRAPH:
       ctx->use_graph = static_cast<int>(value);
       break;
+    case ASICP_OPT_MAX_CHUNKS:
+      ctx->max_chunks = std::max<int>(1, static_cast<int>(value));
+      break;
     case ASICP_OPT_PROFILE:
       ctx->profile = static_cast<int>(value);
       break;
@@ -783,6 +801,58 @@ int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
 double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annealing(t, T, C, p); }
 
 double asicp_dbg_ffma_tflops(int iters) { return run_ffma_peak(iters); }
+
+int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t* out) {
+  // One particle stream (seed), `calls` consecutive minibatch draws of sizes
+  // ms[c]; pool indices written back to back into out.
+  try {
+    DevProblem P{};
+    DevState S{};
+    P.J = 1;
+    P.n_obj = static_cast<int>(n);
+    P.n_obj_pad = static_cast<int>((n + kSubRows - 1) / kSubRows * kSubRows);
+    Buf cand, active, ncol, st, mti, pidx, p32, fy;
+    cand.ensure(static_cast<size_t>(P.n_obj_pad) * 16);
+    CUDA_OK(cudaMemset(cand.p, 0, static_cast<size_t>(P.n_obj_pad) * 16));
+    active.ensure(4);
+    ncol.ensure(4);
+    const int one = 1, zero = 0;
+    CUDA_OK(cudaMemcpy(active.p, &one, 4, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(ncol.p, &zero, 4, cudaMemcpyHostToDevice));
+    st.ensure(mt::kN * 8);
+    mti.ensure(4);
+    pidx.ensure(static_cast<size_t>(P.n_obj_pad) * 4);
+    p32.ensure(static_cast<size_t>(P.n_obj_pad) * 16);
+    fy.ensure(static_cast<size_t>(n) * 4);
+    P.obj_cand = cand.as<float4>();
+    S.active = active.as<int>();
+    S.n_col = ncol.as<int>();
+    S.rng_state = st.as<uint64_t>();
+    S.rng_mti = mti.as<int>();
+    S.pool_idx = pidx.as<int>();
+    S.pool32 = p32.as<float4>();
+    S.fy_scratch = fy.as<int>();
+    launch_seed_rng(P, S, seed, nullptr);
+    int64_t o = 0;
+    for (int64_t c = 0; c < calls; ++c) {
+      launch_minibatch(P, S, static_cast<int>(ms[c]), nullptr);
+      CUDA_OK(cudaGetLastError());
+      CUDA_OK(cudaMemcpy(out + o, S.pool_idx, static_cast<size_t>(ms[c]) * 4, cudaMemcpyDeviceToHost));
+      o += ms[c];
+    }
+    const Buf* bufs[] = {&cand, &active, &ncol, &st, &mti, &pidx, &p32, &fy};
+    for (const Buf* b : bufs) const_cast<Buf*>(b)->release();
+    return ASICP_OK;
+  } catch (const std::exception&) {
+    return ASICP_DEVICE_ERROR;
+  }
+}
+
+int asicp_dbg_raw_stats(asicp_ctx* ctx, uint64_t* out16) {
+  if (!ctx || !out16) return ASICP_INVALID_ARGUMENT;
+  for (int i = 0; i < kStats; ++i) out16[i] = ctx->raw_stats[i];
+  return ASICP_OK;
+}
 
 void asicp_dbg_exp_host(const double* x, double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) y[i] = host_glibc_exp(x[i]);
