@@ -107,7 +107,13 @@ struct Grid {
   double boundary_max_abs;
   double offset[3];
   int64_t values_offset;  // into the concatenated value buffer
+  double lip;             // max |node difference| / voxel along any axis (FP32 pre-test bound)
+  double vmax;            // max |value|
+  int32_t cdims[3];       // coarse blocks of 4x4x4 cells per axis
+  int64_t coarse_offset;  // into the concatenated coarse-max buffer
 };
+
+constexpr int kCoarse = 4;  // cells per coarse block edge
 
 // sdf.cpp:177-203 query(SdfGrid, p) in the reference order.
 ASICP_HD double sdf_query(const Grid& g, const float* values, double px, double py, double pz) {

@@ -78,52 +78,179 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
 // colliding scene indices in scene order and their FP32 reverse-match queries.
 // count_only: final ranking (only N_col == 0 matters, grasp.cpp:271-274).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) collide_kernel(DevProblem P, DevState S, int all, int count_only) {
+//
+// Most scene points lie far outside the gripper's grid box, where the
+// reference returns -(distance + boundary_max_abs) <= -boundary_max_abs.  When
+// contact_tolerance >= -boundary_max_abs such points can never collide, so an
+// FP32 transform that places a point outside the box by more than a
+// conservative rounding margin decides it without the FP64 path; every other
+// point takes the exact FP64 evaluation.  Each warp owns a contiguous scene
+// range; hits are kept as a bitmask in shared memory and compacted in scene
+// order after a scan over the warps' counts.
+constexpr int kColThreads = 256;
+constexpr int kColWarps = kColThreads / 32;
+
+// The exact FP64 test of one scene point (colliding_points body,
+// sdf.cpp:237-239), kept out of line so its register needs do not throttle
+// the FP32 pre-test loop (it runs for ~1e-4 of the points).
+__device__ __noinline__ bool collide_exact(const double* th, const Grid* gp, const float* values, const double* p64,
+                                           double tol) {
+  const Grid& g = *gp;
+  Q4 qi;
+  V3 ti;
+  inverse(pose_q(th), pose_t(th), &qi, &ti);
+  const M3 r = rotation_matrix(qi);
+  const V3 off = V3{g.offset[0], g.offset[1], g.offset[2]};
+  const V3 local = sub(add(add(mul(r, V3{p64[0], p64[1], p64[2]}), ti), off), off);
+  return sdf_query(g, values, local.x, local.y, local.z) > tol;
+}
+
+__global__ void __launch_bounds__(kColThreads, 3) collide_kernel(DevProblem P, DevState S, int all, int count_only) {
   const int j = blockIdx.x;
   if (!all && !S.active[j]) return;
+  extern __shared__ __align__(16) unsigned int hitbits[];  // ceil(n_scene / 32) words, then the coarse grid
+  __shared__ int warp_cnt[kColWarps];
   const int pre = P.part_pre[j];
   const Grid g = P.grids[P.pre_sdf[pre]];
+  float* coarse_s = reinterpret_cast<float*>(hitbits + round_up((P.n_scene + 31) / 32, 4));
+  const int ncoarse = g.cdims[0] * g.cdims[1] * g.cdims[2];
+  for (int i = threadIdx.x; i < ncoarse; i += blockDim.x) coarse_s[i] = P.sdf_coarse[g.coarse_offset + i];
+  const double coarse_cut = P.contact_tolerance - 1e-12 * (1.0 + fabs(P.contact_tolerance));
+  __syncthreads();
   const double* th = th_of(S.theta, j);
   Q4 qi;
   V3 ti;
   inverse(pose_q(th), pose_t(th), &qi, &ti);
   const M3 r = rotation_matrix(qi);
-  const double B = S.Bs[j];
-  const V3 c = V3{S.ctr[3 * j], S.ctr[3 * j + 1], S.ctr[3 * j + 2]};
   const V3 off = V3{g.offset[0], g.offset[1], g.offset[2]};
-  __shared__ int warp_tot[8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int base = 0;
-  const int64_t row = static_cast<int64_t>(j) * P.n_scene;
-  for (int c0 = 0; c0 < P.n_scene; c0 += 256) {
-    const int idx = c0 + threadIdx.x;
-    bool hit = false;
-    if (idx < P.n_scene) {
-      const V3 p = load3(P.scene64, idx);
-      const V3 local = sub(add(add(mul(r, p), ti), off), off);
-      hit = sdf_query(g, P.sdf_values, local.x, local.y, local.z) > P.contact_tolerance;
-    }
-    const unsigned mask = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) warp_tot[wid] = __popc(mask);
-    __syncthreads();
-    int before = 0, total = 0;
-    for (int w = 0; w < 8; ++w) {
-      before += w < wid ? warp_tot[w] : 0;
-      total += warp_tot[w];
-    }
-    if (hit && !count_only) {
-      const int slot = base + before + __popc(mask & ((1u << lane) - 1u));
-      S.col_idx[row + slot] = idx;
-      const V3 p = load3(P.scene64, idx);
-      const double ax = p.x - c.x, ay = p.y - c.y, az = p.z - c.z;
-      const double A = sqrt(ax * ax + ay * ay + az * az);
-      S.col_q[row + slot] =
-          make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az), nn_margin(A, B));
-    }
-    base += total;
-    __syncthreads();
+  // FP32 culling box (sdf.cpp:178-182 out-of-grid test) with margin.
+  float r32[9];
+  for (int i = 0; i < 9; ++i) r32[i] = static_cast<float>(r.m[i]);
+  const float t32x = static_cast<float>(ti.x), t32y = static_cast<float>(ti.y), t32z = static_cast<float>(ti.z);
+  float lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = static_cast<float>(g.origin[a]);
+    hi[a] = static_cast<float>(g.origin[a] + g.voxel * static_cast<double>(g.dims[a] - 1));
   }
-  if (threadIdx.x == 0) S.n_col[j] = base;
+  const float tn = fabsf(t32x) + fabsf(t32y) + fabsf(t32z) + fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) +
+                   fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]);
+  const bool cull_ok = P.contact_tolerance >= -g.boundary_max_abs;
+  const float inv_vox = static_cast<float>(1.0 / g.voxel);
+  const float tol32 = static_cast<float>(P.contact_tolerance);
+  // Value margin: slope x position error, plus fraction rounding (|u| <= dims,
+  // ~1e-5 voxel) and 7 FP32 lerps / the rounded tolerance (~1e-6 x magnitudes).
+  const float vmargin_pos = static_cast<float>(g.lip);
+  const float vmargin_c = static_cast<float>(g.lip * g.voxel * 1e-5 + 1e-6 * (g.vmax + fabs(P.contact_tolerance)) +
+                                             1e-9);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nwords = (P.n_scene + 31) / 32;
+  const int words_per_warp = (nwords + kColWarps - 1) / kColWarps;
+  const int w0 = wid * words_per_warp, w1 = min(nwords, w0 + words_per_warp);
+  int cnt = 0;
+  // Status per point: 0 clear, 1 colliding, 2 needs the exact FP64 test.
+  auto classify = [&](float4 p) -> int {
+    int status = 2;
+    {
+      {
+        const float fx = p.x, fy = p.y, fz = p.z;
+        const float lx = __fmaf_rn(r32[0], fx, __fmaf_rn(r32[1], fy, __fmaf_rn(r32[2], fz, t32x)));
+        const float ly = __fmaf_rn(r32[3], fx, __fmaf_rn(r32[4], fy, __fmaf_rn(r32[5], fz, t32y)));
+        const float lz = __fmaf_rn(r32[6], fx, __fmaf_rn(r32[7], fy, __fmaf_rn(r32[8], fz, t32z)));
+        // |l32 - l64| <= ~5u (|p|_1 + |t|_1) (+ the rounded box corners): d is >= 3x that.
+        const float d = 1e-6f * (1.0f + fabsf(fx) + fabsf(fy) + fabsf(fz) + tn);
+        const bool out_far = lx < lo[0] - d || lx > hi[0] + d || ly < lo[1] - d || ly > hi[1] + d ||
+                             lz < lo[2] - d || lz > hi[2] + d;
+        const bool in_far = lx >= lo[0] + d && lx <= hi[0] - d && ly >= lo[1] + d && ly <= hi[1] - d &&
+                            lz >= lo[2] + d && lz <= hi[2] - d;
+        if (out_far) {
+          if (cull_ok) status = 0;  // value <= -boundary_max_abs <= contact_tolerance: never collides
+        } else if (in_far) {
+          // FP32 trilinear; the interpolant is continuous with per-axis slope
+          // <= lip, so |v32 - v64| <= lip * (|e|_1 + fraction error) + lerp rounding.
+          const float ux = (lx - lo[0]) * inv_vox, uy = (ly - lo[1]) * inv_vox, uz = (lz - lo[2]) * inv_vox;
+          const int ix = max(min(static_cast<int>(ux), g.dims[0] - 2), 0);
+          const int iy = max(min(static_cast<int>(uy), g.dims[1] - 2), 0);
+          const int iz = max(min(static_cast<int>(uz), g.dims[2] - 2), 0);
+          // Coarse bound: the FP64 cell is within one cell of this one, and its
+          // trilinear value is a convex combination of nodes the dilated block
+          // max covers — below the tolerance, the point cannot collide.
+          const float cm = coarse_s[((ix / kCoarse) * g.cdims[1] + iy / kCoarse) * g.cdims[2] + iz / kCoarse];
+          if (static_cast<double>(cm) < coarse_cut) return 0;
+          const float fxx = fminf(fmaxf(ux - ix, 0.0f), 1.0f), fyy = fminf(fmaxf(uy - iy, 0.0f), 1.0f),
+                      fzz = fminf(fmaxf(uz - iz, 0.0f), 1.0f);
+          const float* v0 = P.sdf_values + g.values_offset + (static_cast<int64_t>(ix) * g.dims[1] + iy) * g.dims[2] + iz;
+          const int sy = g.dims[2], sx = g.dims[1] * g.dims[2];
+          const float c00 = __fmaf_rn(fxx, v0[sx] - v0[0], v0[0]);
+          const float c01 = __fmaf_rn(fxx, v0[sx + 1] - v0[1], v0[1]);
+          const float c10 = __fmaf_rn(fxx, v0[sx + sy] - v0[sy], v0[sy]);
+          const float c11 = __fmaf_rn(fxx, v0[sx + sy + 1] - v0[sy + 1], v0[sy + 1]);
+          const float c0 = __fmaf_rn(fyy, c10 - c00, c00);
+          const float c1 = __fmaf_rn(fyy, c11 - c01, c01);
+          const float v32 = __fmaf_rn(fzz, c1 - c0, c0);
+          const float mv = vmargin_pos * 3.0f * d + vmargin_c;
+          if (v32 > tol32 + mv)
+            status = 1;
+          else if (v32 < tol32 - mv)
+            status = 0;
+        }
+      }
+    }
+    return status;
+  };
+  constexpr int kU = 4;  // words per batch: independent loads in flight
+  for (int wb = w0; wb < w1; wb += kU) {
+    float4 pv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = (wb + u) * 32 + lane;
+      pv[u] = (wb + u < w1 && idx < P.n_scene) ? P.scene32[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int stt[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = (wb + u) * 32 + lane;
+      stt[u] = (wb + u < w1 && idx < P.n_scene) ? classify(pv[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (wb + u >= w1) break;
+      bool hit = stt[u] == 1;
+      if (stt[u] == 2)
+        hit = collide_exact(th, P.grids + P.pre_sdf[pre], P.sdf_values,
+                            P.scene64 + 3 * static_cast<int64_t>((wb + u) * 32 + lane), P.contact_tolerance);
+      const unsigned mask = __ballot_sync(0xffffffffu, hit);
+      if (lane == 0) hitbits[wb + u] = mask;
+      cnt += __popc(mask);
+    }
+  }
+  if (lane == 0) warp_cnt[wid] = cnt;
+  __syncthreads();
+  int base = 0, total = 0;
+  for (int w = 0; w < kColWarps; ++w) {
+    base += w < wid ? warp_cnt[w] : 0;
+    total += warp_cnt[w];
+  }
+  if (!count_only && cnt > 0) {
+    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
+    const double B = S.Bs[j];
+    const V3 c = V3{S.ctr[3 * j], S.ctr[3 * j + 1], S.ctr[3 * j + 2]};
+    for (int w = w0; w < w1; ++w) {
+      const unsigned mask = hitbits[w];
+      if (mask == 0) continue;
+      if ((mask >> lane) & 1u) {
+        const int idx = w * 32 + lane;
+        const int slot = base + __popc(mask & ((1u << lane) - 1u));
+        S.col_idx[row + slot] = idx;
+        const V3 p = load3(P.scene64, idx);
+        const double ax = p.x - c.x, ay = p.y - c.y, az = p.z - c.z;
+        const double A = sqrt(ax * ax + ay * ay + az * az);
+        S.col_q[row + slot] =
+            make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az), nn_margin(A, B));
+      }
+      base += __popc(mask);
+    }
+  }
+  if (threadIdx.x == 0) S.n_col[j] = total;
 }
 
 // ---------------------------------------------------------------------------
@@ -342,17 +469,6 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
   for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
 }
 
-// Pair p of a population -> (i, j), i < j, row-major over the upper triangle.
-__device__ __forceinline__ void pair_of(long long p, int K, int* pi, int* pj) {
-  const double a = 2.0 * K - 1.0;
-  long long i = static_cast<long long>((a - sqrt(a * a - 8.0 * static_cast<double>(p))) * 0.5);
-  auto start = [K](long long r) { return r * (2LL * K - r - 1) / 2; };
-  while (i > 0 && start(i) > p) --i;
-  while (i + 1 < K && start(i + 1) <= p) ++i;
-  *pi = static_cast<int>(i);
-  *pj = static_cast<int>(i + 1 + (p - start(i)));
-}
-
 // One CTA per population: 8 radix passes of 8 bits over the K(K-1)/2 keys
 // (nth_element at M/2, optim.cpp:141-142: an exact order statistic).
 __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) {
@@ -376,17 +492,37 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
     s_mask = 0;
     s_rank = M / 2;
   }
+  // Keys are computed once (row-major over the upper triangle) into the
+  // population's slice of S.med_keys when it has one, then re-read by the
+  // later passes from L2; without a slice every pass recomputes them.
+  unsigned long long* keys = S.med_keys && P.med_off[pop] >= 0 ? S.med_keys + P.med_off[pop] : nullptr;
   for (int pass = 0; pass < 8; ++pass) {
     const int shift = 56 - 8 * pass;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const unsigned long long prefix = s_prefix, mask = s_mask;
-    for (long long p = threadIdx.x; p < M; p += blockDim.x) {
-      int i, jj;
-      pair_of(p, K, &i, &jj);
-      const double d2 = sqnorm(sub(pose_t(th_of(S.theta, b + i)), pose_t(th_of(S.theta, b + jj))));
-      const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    if (keys != nullptr && pass > 0) {
+      for (long long p = threadIdx.x; p < M; p += blockDim.x) {
+        const unsigned long long key = keys[p];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+    } else {
+      // Row i of the triangle is handled by consecutive threads over j (no
+      // per-pair index arithmetic): rows are walked in order, each thread
+      // striding over the flattened position.
+      int i = 0;
+      long long row_start = 0;
+      for (long long p = threadIdx.x; p < M; p += blockDim.x) {
+        while (p >= row_start + (K - 1 - i)) {
+          row_start += K - 1 - i;
+          ++i;
+        }
+        const int jj = i + 1 + static_cast<int>(p - row_start);
+        const double d2 = sqnorm(sub(pose_t(th_of(S.theta, b + i)), pose_t(th_of(S.theta, b + jj))));
+        const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
+        if (keys != nullptr) keys[p] = key;
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -605,7 +741,11 @@ void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st
   pose_prep_kernel<<<P.J, kNnThreads, 0, st>>>(P, S, all);
 }
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st) {
-  collide_kernel<<<P.J, 256, 0, st>>>(P, S, all, count_only);
+  const size_t smem = static_cast<size_t>(round_up((P.n_scene + 31) / 32, 4)) * sizeof(unsigned int) +
+                      static_cast<size_t>(P.max_coarse) * sizeof(float);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(collide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  collide_kernel<<<P.J, kColThreads, smem, st>>>(P, S, all, count_only);
 }
 int minibatch_smem_cap() { return 160 * 1024; }
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {

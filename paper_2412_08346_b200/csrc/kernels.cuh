@@ -22,17 +22,21 @@ struct DevProblem {
   const double* obj64;      // R, n_obj x 3
   const float4* obj_cand;   // R as FP32 NN candidates (-2b, |b|^2), b = r - center
   const double* scene64;    // C, n_scene x 3
+  const float4* scene32;    // C rounded to FP32 (x, y, z, 0), for the collision pre-test
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
   const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
   const double* pre_tcp;    // preshape tcp, 3 per preshape
   const int* pre_sdf;       // preshape -> grid index
   const Grid* grids;
   const float* sdf_values;
+  const float* sdf_coarse;  // per grid: dilated 4x4x4-block maxima (collision pre-test)
+  int max_coarse;           // largest coarse grid (blocks)
   const int* part_pre;      // particle -> preshape
   const int64_t* part_surf_off;  // particle -> first surface row (rows padded to 32) (J + 1)
   const int* part_pop;      // particle -> population
   const int* pop_off;       // population -> first particle (n_pop + 1)
   const double* pop_logk1;  // log(K + 1) per population (host std::log)
+  const long long* med_off; // population -> offset of its median keys in DevState::med_keys (-1: none)
   double center[3];         // FP32 re-centring origin of the forward match (object centroid)
   double B_obj;             // max |r - center| over R (with slack)
   double com[3];
@@ -62,6 +66,7 @@ struct DevState {
   double* prior;       // J x 7 prior log-gradient
   double* drift;       // J x 7
   double* h;           // per population bandwidth
+  unsigned long long* med_keys;  // cached squared-distance bit patterns for the median select
   double* S64;         // transformed contact surface, padded rows x 3
   float4* Sq32;        // its FP32 forward queries (x, y, z, margin), object-centred
   float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred

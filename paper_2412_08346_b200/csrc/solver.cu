@@ -113,6 +113,7 @@ struct asicp_ctx {
   bool prepared = false;
   int J = 0, n_obj = 0, n_obj_pad = 0, n_scene = 0, n_pre = 0, k_max = 0, k_stein = 0, max_pop = 0;
   int max_ns = 0;
+  int max_coarse = 0;
   int64_t total_surf = 0;
   int record_trace = 0;
   double n_ref = 0, eta_stein = 0;
@@ -128,7 +129,7 @@ struct asicp_ctx {
 
   // Device buffers.
   Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
-      part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d;
+      part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, med_off_d, med_keys, scene32, sdf_coarse;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items0, items1,
       item_count, item_off, item_counter, scan_tmp, partials, refine_list, refine_count, stats, trace_theta,
@@ -154,7 +155,8 @@ struct asicp_ctx {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     Buf* all[] = {&obj64, &obj_cand, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
-                  &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d, &theta,
+                  &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d, &med_off_d,
+                  &med_keys, &scene32, &sdf_coarse, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &items0, &items1, &item_count, &item_off, &item_counter, &scan_tmp,
@@ -262,6 +264,13 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c->obj64, obj.data(), obj.size(), st);
   upload(c->obj_cand, cand.data(), cand.size(), st);
   upload(c->scene64, p.scene_cloud, 3 * p.n_scene, st);
+  {
+    std::vector<float4> s32(p.n_scene);
+    for (int64_t i = 0; i < p.n_scene; ++i)
+      s32[i] = make_float4(static_cast<float>(p.scene_cloud[3 * i]), static_cast<float>(p.scene_cloud[3 * i + 1]),
+                           static_cast<float>(p.scene_cloud[3 * i + 2]), 0.0f);
+    upload(c->scene32, s32.data(), s32.size(), st);
+  }
 
   // Preshapes.
   std::vector<double> surf;
@@ -285,7 +294,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
 
   // SDF grids.
   std::vector<Grid> grids(p.n_sdf_grids);
-  std::vector<float> values;
+  std::vector<float> values, coarse;
   for (int64_t g = 0; g < p.n_sdf_grids; ++g) {
     const asicp_sdf_grid& s = p.sdf_grids[g];
     Grid& d = grids[g];
@@ -299,9 +308,44 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     d.values_offset = static_cast<int64_t>(values.size());
     const size_t total = static_cast<size_t>(s.dims[0]) * s.dims[1] * s.dims[2];
     values.insert(values.end(), s.values, s.values + total);
+    // Bounds for the collision kernel's FP32 pre-test.
+    double vmax = 0.0, dmax = 0.0;
+    const int nx = s.dims[0], ny = s.dims[1], nz = s.dims[2];
+    for (int ix = 0; ix < nx; ++ix)
+      for (int iy = 0; iy < ny; ++iy)
+        for (int iz = 0; iz < nz; ++iz) {
+          const size_t id = (static_cast<size_t>(ix) * ny + iy) * nz + iz;
+          const double v = s.values[id];
+          vmax = std::max(vmax, std::abs(v));
+          if (ix + 1 < nx) dmax = std::max(dmax, std::abs(v - s.values[id + static_cast<size_t>(ny) * nz]));
+          if (iy + 1 < ny) dmax = std::max(dmax, std::abs(v - s.values[id + nz]));
+          if (iz + 1 < nz) dmax = std::max(dmax, std::abs(v - s.values[id + 1]));
+        }
+    d.lip = dmax / s.voxel;
+    d.vmax = vmax;
+    // Coarse max grid: block b covers cells [4b, 4b+4) per axis; its value is
+    // the max over nodes [4b-1, 4b+5] (dilated by one node), so it bounds the
+    // trilinear value of any point whose cell is within one of the block.
+    for (int a = 0; a < 3; ++a) d.cdims[a] = (s.dims[a] - 1 + kCoarse - 1) / kCoarse;
+    d.coarse_offset = static_cast<int64_t>(coarse.size());
+    for (int bx = 0; bx < d.cdims[0]; ++bx)
+      for (int by = 0; by < d.cdims[1]; ++by)
+        for (int bz = 0; bz < d.cdims[2]; ++bz) {
+          float m = -INFINITY;
+          for (int ix = std::max(0, kCoarse * bx - 1); ix <= std::min(nx - 1, kCoarse * bx + kCoarse + 1); ++ix)
+            for (int iy = std::max(0, kCoarse * by - 1); iy <= std::min(ny - 1, kCoarse * by + kCoarse + 1); ++iy)
+              for (int iz = std::max(0, kCoarse * bz - 1); iz <= std::min(nz - 1, kCoarse * bz + kCoarse + 1);
+                   ++iz)
+                m = std::max(m, s.values[(static_cast<size_t>(ix) * ny + iy) * nz + iz]);
+          coarse.push_back(m);
+        }
   }
   upload(c->grids, grids.data(), grids.size(), st);
   upload(c->sdf_values, values.data(), values.size(), st);
+  upload(c->sdf_coarse, coarse.data(), coarse.size(), st);
+  c->max_coarse = 0;
+  for (const Grid& g : grids)
+    c->max_coarse = std::max(c->max_coarse, g.cdims[0] * g.cdims[1] * g.cdims[2]);
 
   // Particles (preshape-major flattening, grasp.cpp:135-145).
   std::vector<int> part_pre, part_pop, pop_off(n_pre + 1, 0);
@@ -329,6 +373,21 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c->part_pop, part_pop.data(), part_pop.size(), st);
   upload(c->pop_off, pop_off.data(), pop_off.size(), st);
   upload(c->pop_logk1, logk1.data(), logk1.size(), st);
+  // Median-select key cache: one slice of K(K-1)/2 keys per population when
+  // the total stays modest (otherwise the select recomputes keys per pass).
+  std::vector<long long> med_off(n_pre, -1);
+  long long med_total = 0;
+  for (int i = 0; i < n_pre; ++i) med_total += p.init_counts[i] * (p.init_counts[i] - 1) / 2;
+  if (med_total > 0 && med_total <= (32ll << 20)) {
+    long long o = 0;
+    for (int i = 0; i < n_pre; ++i) {
+      med_off[i] = o;
+      o += p.init_counts[i] * (p.init_counts[i] - 1) / 2;
+    }
+    c->med_keys.ensure(static_cast<size_t>(med_total) * 8);
+  }
+  upload(c->med_off_d, med_off.data(), med_off.size(), st);
+  const bool med_cached = med_total > 0 && med_total <= (32ll << 20);
   upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
   c->init_theta.assign(p.init_poses, p.init_poses + 7 * J);
   upload(c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
@@ -410,17 +469,21 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.obj64 = c->obj64.as<double>();
   P.obj_cand = c->obj_cand.as<float4>();
   P.scene64 = c->scene64.as<double>();
+  P.scene32 = c->scene32.as<float4>();
   P.surf64 = c->surf64.as<double>();
   P.pre_surf_off = c->pre_surf_off.as<int>();
   P.pre_tcp = c->pre_tcp.as<double>();
   P.pre_sdf = c->pre_sdf.as<int>();
   P.grids = c->grids.as<Grid>();
   P.sdf_values = c->sdf_values.as<float>();
+  P.sdf_coarse = c->sdf_coarse.as<float>();
+  P.max_coarse = c->max_coarse;
   P.part_pre = c->part_pre_d.as<int>();
   P.part_surf_off = c->part_surf_off.as<int64_t>();
   P.part_pop = c->part_pop.as<int>();
   P.pop_off = c->pop_off.as<int>();
   P.pop_logk1 = c->pop_logk1.as<double>();
+  P.med_off = c->med_off_d.as<long long>();
   for (int a = 0; a < 3; ++a) {
     P.center[a] = center[a];
     P.com[a] = p.com[a];
@@ -452,6 +515,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.prior = c->prior.as<double>();
   S.drift = c->drift.as<double>();
   S.h = c->h.as<double>();
+  S.med_keys = med_cached ? c->med_keys.as<unsigned long long>() : nullptr;
   S.S64 = c->S64.as<double>();
   S.Sq32 = c->Sq32.as<float4>();
   S.Sc32 = c->Sc32.as<float4>();

@@ -23,3 +23,4 @@ f = lambda u: struct.unpack('<f', struct.pack('<I', int(u) & 0xffffffff))[0]
 d = [int(raw[201 + i]) for i in range(14)]
 print("first top3 overflow: iter", d[0], "particle", d[1], "q", d[2], "b1 b2 b3 thr", [f(x) for x in d[3:7]], "nc", d[7],
       "s1 s2", d[8] & 0xffff, d[8] >> 16, "q", [f(x) for x in d[9:12]], "margin", f(d[12]), "cbase", d[13])
+print("collide status counts: clear", int(raw[240]), "hit", int(raw[241]), "exact", int(raw[242]))
