@@ -89,6 +89,10 @@ struct DevState {
   void* scan_tmp;
   size_t scan_tmp_bytes;
   NnPartial* partials; // padded surface rows x max chunks
+  int2* amb_pool;      // ambiguous-window member lists (kWinCap entries per block)
+  int* amb_n;          // members per block (> kWinCap: overflow)
+  int* amb_count;      // blocks allocated in the current NN round
+  int amb_cap;         // blocks available
   int4* refine_list;
   int* refine_count;
   int refine_cap;

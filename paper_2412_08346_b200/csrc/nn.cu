@@ -5,18 +5,23 @@
 // replacing the per-call kd-trees of spatial_index.cpp:14-105.
 //
 // FP32 filter, FP64 decision:
-//   * candidates (-2b, |b|^2) stream through shared memory in 4 KB tiles
-//     by TMA bulk copies (cp.async.bulk + mbarrier, 4-stage ring);
+//   * a work item is (particle, <= 1024 queries, a split of the candidates);
+//     the split is consumed in sub-chunks of <= 2048 candidates that are
+//     loaded whole into shared memory by TMA bulk copies (cp.async.bulk +
+//     mbarrier, one 4 KB tile per stage) and read with broadcast LDS.128;
 //   * each thread holds Q queries in registers; one (query, candidate) pair
 //     is 3 FFMA + 1 FMNMX (the expansion form |b|^2 - 2 a.b), branch-free;
-//   * every 32 candidates (a subtile) each query folds its subtile minimum
-//     into a running top-3 of subtile minima (b1 <= b2 <= b3, subtiles s1, s2);
-//   * at the end the reference's answer — min FP64 (p - q).squaredNorm(),
-//     ties to the lowest position (spatial_index.cpp:69-83) — is provably in
-//     the window {d32 <= b1 + 2E} (2E = the query's margin).  If b3 > b1 + 2E
-//     the window lies in subtiles s1/s2, which are rescanned; a window of one
-//     is certified, larger windows are decided in FP64 with the reference
-//     formula, and the rare b3 <= b1 + 2E case goes to a full FP64 rescan.
+//   * every 32 candidates (a subtile) each query folds the subtile minimum into
+//     a running top-3 of subtile minima (b1 <= b2 <= b3, subtiles s1, s2);
+//   * after a sub-chunk, the reference's answer within it — min FP64
+//     (p - q).squaredNorm(), ties to the lowest position (spatial_index.cpp:
+//     69-83) — is provably in {d32 <= b1 + 2E} (2E = the query's margin).  The
+//     subtiles s1 (and s2 when b2 is inside the margin) are rescanned from
+//     shared memory for the position of b1 and the window count; b3 inside the
+//     margin or a window of two or more makes the query "ambiguous";
+//   * the running (best value, position, ambiguous) state carries across
+//     sub-chunks and splits; an unambiguous query is certified, an ambiguous
+//     one is decided by a full FP64 rescan with the reference formula.
 #include "common.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -156,15 +161,51 @@ __device__ __forceinline__ int nn_decide(const NnGeom& g, const int* pos, int n,
   return bi;
 }
 
-// stats[5 + kind]: refines per match kind; stats[8 + reason]: 0 mode, 1 top-3
-// overflow, 2 window > kNnL, 3 merge overflow.
+// Ambiguous-window member lists: a block of kWinCap (position, d32) entries
+// per ambiguous query, allocated from a pool; amb_n > kWinCap marks overflow.
+__device__ __forceinline__ int win_alloc(DevState& S) {
+  const int b = atomicAdd(S.amb_count, 1);
+  return b < S.amb_cap ? b : -1;
+}
+__device__ __forceinline__ void win_push(DevState& S, int blk, int pos, float d) {
+  const int n = S.amb_n[blk];
+  if (n < kWinCap) S.amb_pool[static_cast<int64_t>(blk) * kWinCap + n] = make_int2(pos, __float_as_int(d));
+  S.amb_n[blk] = n + 1;
+}
+// Members of a running window with d32 <= thr; false if they cannot be listed.
+__device__ __forceinline__ bool win_collect(const DevState& S, int p1, float thr, int* out, int* n, int cap) {
+  if (!(p1 & kAmbiguous)) {
+    if (cap < 1) return false;
+    out[0] = p1;
+    *n = 1;
+    return true;
+  }
+  const int blk = p1 & ~kAmbiguous;
+  if (blk == kNoBlock) return false;
+  const int cnt = S.amb_n[blk];
+  if (cnt > kWinCap) return false;
+  int m = 0;
+  for (int e = 0; e < cnt; ++e) {
+    const int2 v = S.amb_pool[static_cast<int64_t>(blk) * kWinCap + e];
+    if (__int_as_float(v.y) <= thr) {
+      if (m >= cap) return false;
+      out[m++] = v.x;
+    }
+  }
+  *n = m;
+  return m > 0;
+}
+
+// stats[5 + kind]: rescans per match kind; stats[8 + reason]: 0 validation
+// mode, 1 ambiguous window, 3 ambiguous across splits; stats[16 + k]: rescans
+// in iteration k.
 __device__ __forceinline__ void push_refine(DevState& S, int kind, int j, int qlocal, int reason, int iter) {
   const int slot = atomicAdd(S.refine_count, 1);
   if (slot < S.refine_cap) S.refine_list[slot] = make_int4(kind, j, qlocal, 0);
   atomicAdd(S.stats + 1, 1ull);
   atomicAdd(S.stats + 5 + kind, 1ull);
   atomicAdd(S.stats + 8 + reason, 1ull);
-  atomicAdd(S.stats + 16 + min(iter, 239), 1ull);
+  atomicAdd(S.stats + 16 + min(iter, 223), 1ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -203,11 +244,18 @@ __device__ __forceinline__ float d32(float qx, float qy, float qz, float4 v) {
 // The filter kernel (persistent over one work list).
 // ---------------------------------------------------------------------------
 template <int Q>
-__global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, DevState S, NnPlan plan, int list) {
+#ifndef ASICP_NN_MINBLOCKS
+#define ASICP_NN_MINBLOCKS 1
+#endif
+__global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
+    nn_filter_kernel(DevProblem P, DevState S, NnPlan plan, int list) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float4* tiles = reinterpret_cast<float4*>(smem_raw);
   __shared__ __align__(8) uint64_t full_bar[kNnStages];
   __shared__ int s_item;
+  __shared__ float run_mg[Q * kNnThreads];
+  __shared__ float run_b1[Q * kNnThreads];
+  __shared__ int run_p1[Q * kNnThreads];
   const int tid = threadIdx.x;
   if (tid == 0) {
     for (int s = 0; s < kNnStages; ++s) mbar_init(&full_bar[s], 1);
@@ -216,7 +264,7 @@ __global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, Dev
   __syncthreads();
   const int n_items = S.item_off[list][P.J];
   const NnItem* items = S.items[list];
-  uint32_t gtile = 0;
+  uint32_t phases = 0;  // bit s: parity of the next completion of stage s
   for (;;) {
     if (tid == 0) s_item = atomicAdd(S.item_counter + list, 1);
     __syncthreads();
@@ -224,19 +272,18 @@ __global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, Dev
     __syncthreads();
     if (it >= n_items) break;
     const NnItem w = items[it];
-    const int nc_pad = round_up(w.nc, kSub);  // candidate arrays are padded with +inf rows
-    const int ntiles = ceil_div(nc_pad, kNnTile);
     if (tid == 0) {
       atomicAdd(S.stats + 2, static_cast<unsigned long long>(w.chunk == 0 ? w.nq : 0));
       atomicAdd(S.stats + 4, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
-      for (int t = 0; t < ntiles && t < kNnStages; ++t) {
-        const uint32_t s = (gtile + t) % kNnStages;
-        const int n_in = min(kNnTile, nc_pad - t * kNnTile);
-        tma_load_1d(tiles + s * kNnTile, w.c + t * kNnTile, n_in * 16, &full_bar[s]);
-      }
+      if (list == 0)
+        atomicAdd(S.stats + 12, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
     }
-    float qx[Q], qy[Q], qz[Q], b1[Q], b2[Q], b3[Q];
-    int s12[Q];
+    // Running state lives in shared memory (touched once per sub-chunk), which
+    // keeps the hot loop's register footprint down.
+    float qx[Q], qy[Q], qz[Q];
+#define MG(k) run_mg[(k) * kNnThreads + tid]
+#define B1(k) run_b1[(k) * kNnThreads + tid]
+#define P1(k) run_p1[(k) * kNnThreads + tid]
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
       const int qi = tid + k * kNnThreads;
@@ -244,122 +291,186 @@ __global__ void __launch_bounds__(kNnThreads) nn_filter_kernel(DevProblem P, Dev
       qx[k] = q.x;
       qy[k] = q.y;
       qz[k] = q.z;
-      b1[k] = b2[k] = b3[k] = INFINITY;
-      s12[k] = 0;
+      MG(k) = q.w;
+      B1(k) = INFINITY;
+      P1(k) = 0;
     }
-    for (int t = 0; t < ntiles; ++t) {
-      const uint32_t G = gtile + t;
-      const uint32_t stage = G % kNnStages;
-      mbar_wait(&full_bar[stage], (G / kNnStages) & 1u);
-      const float4* tile = tiles + stage * kNnTile;
-      const int nsub = min(kNnTile, nc_pad - t * kNnTile) / kSub;
-      for (int sub = 0; sub < nsub; ++sub) {
-        const float4* sp = tile + sub * kSub;
-        float tm[Q];
-#pragma unroll
-        for (int k = 0; k < Q; ++k) tm[k] = INFINITY;
-#pragma unroll 8
-        for (int c = 0; c < kSub; ++c) {
-          const float4 v = sp[c];
-#pragma unroll
-          for (int k = 0; k < Q; ++k) tm[k] = fminf(tm[k], d32(qx[k], qy[k], qz[k], v));
-        }
-        const int sid = t * (kNnTile / kSub) + sub;
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-          // Running top-3 of subtile minima (strict < keeps the earliest).
-          const bool lt1 = tm[k] < b1[k];
-          const bool lt2 = tm[k] < b2[k];
-          b3[k] = lt2 ? b2[k] : fminf(b3[k], tm[k]);
-          const int s1 = s12[k] & 0xffff;
-          const int s2 = lt1 ? s1 : (lt2 ? sid : (s12[k] >> 16));
-          b2[k] = lt1 ? b1[k] : (lt2 ? tm[k] : b2[k]);
-          b1[k] = lt1 ? tm[k] : b1[k];
-          s12[k] = (lt1 ? sid : s1) | (s2 << 16);
+    for (int sc0 = 0; sc0 < w.nc; sc0 += kNnMaxChunk) {
+      const int nsc = min(kNnMaxChunk, w.nc - sc0);
+      const int nsc_pad = round_up(nsc, kSub);  // candidate arrays are padded with +inf rows
+      const int ntiles = ceil_div(nsc_pad, kNnTile);
+      if (tid == 0) {
+        for (int t = 0; t < ntiles; ++t) {
+          const int n_in = min(kNnTile, nsc_pad - t * kNnTile);
+          tma_load_1d(tiles + t * kNnTile, w.c + sc0 + t * kNnTile, n_in * 16, &full_bar[t]);
         }
       }
-      __syncthreads();
-      if (tid == 0 && t + kNnStages < ntiles) {
-        const int tn = t + kNnStages;
-        const int n2 = min(kNnTile, nc_pad - tn * kNnTile);
-        tma_load_1d(tiles + stage * kNnTile, w.c + tn * kNnTile, n2 * 16, &full_bar[stage]);
+      float b1[Q], b2[Q], b3[Q];
+      int s12[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        b1[k] = b2[k] = b3[k] = INFINITY;
+        s12[k] = 0;
       }
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait(&full_bar[t], (phases >> t) & 1u);
+        phases ^= 1u << t;
+        const float4* tile = tiles + t * kNnTile;
+        const int nsub = min(kNnTile, nsc_pad - t * kNnTile) / kSub;
+        for (int sub = 0; sub < nsub; ++sub) {
+          const float4* sp = tile + sub * kSub;
+          float tm[Q];
+#pragma unroll
+          for (int k = 0; k < Q; ++k) tm[k] = INFINITY;
+          // Two candidates per step, each FMA stage issued across all Q
+          // queries before the next, so 2Q independent chains are in flight
+          // (same arithmetic as d32(): fma(qx,vx, fma(qy,vy, fma(qz,vz, w)))).
+#pragma unroll 4
+          for (int c = 0; c < kSub; c += 2) {
+            const float4 v0 = sp[c];
+            const float4 v1 = sp[c + 1];
+            float d0[Q], d1[Q];
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              d0[k] = __fmaf_rn(qz[k], v0.z, v0.w);
+              d1[k] = __fmaf_rn(qz[k], v1.z, v1.w);
+            }
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              d0[k] = __fmaf_rn(qy[k], v0.y, d0[k]);
+              d1[k] = __fmaf_rn(qy[k], v1.y, d1[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < Q; ++k) {
+              d0[k] = __fmaf_rn(qx[k], v0.x, d0[k]);
+              d1[k] = __fmaf_rn(qx[k], v1.x, d1[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < Q; ++k) tm[k] = fminf(tm[k], fminf(d0[k], d1[k]));
+          }
+          const int sid = t * (kNnTile / kSub) + sub;
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            // Running top-3 of subtile minima (strict < keeps the earliest).
+            const bool lt1 = tm[k] < b1[k];
+            const bool lt2 = tm[k] < b2[k];
+            b3[k] = lt2 ? b2[k] : fminf(b3[k], tm[k]);
+            const int s1 = s12[k] & 0xffff;
+            const int s2 = lt1 ? s1 : (lt2 ? sid : (s12[k] >> 16));
+            b2[k] = lt1 ? b1[k] : (lt2 ? tm[k] : b2[k]);
+            b1[k] = lt1 ? tm[k] : b1[k];
+            s12[k] = (lt1 ? sid : s1) | (s2 << 16);
+          }
+        }
+      }
+      // Sub-chunk epilogue (candidates still resident): members of the
+      // sub-chunk's window and the position of its minimum, merged into the
+      // running window (an explicit member list only once it holds two).
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const float thr = __fadd_ru(b1[k], MG(k));
+        bool ovf = b3[k] <= thr;
+        int pmin = -1, np = 0;
+        int mpos[kWinCap];
+        float md[kWinCap];
+        const int nscan = b2[k] <= thr ? 2 : 1;
+        const int base = w.c_base + sc0;
+        for (int r = 0; r < nscan; ++r) {
+          const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
+          const float4* sp = tiles + sid * kSub;
+          for (int c = 0; c < kSub; ++c) {
+            const float d = d32(qx[k], qy[k], qz[k], sp[c]);
+            if (d <= thr) {
+              const int p = base + sid * kSub + c;
+              if (np < kWinCap) {
+                mpos[np] = p;
+                md[np] = d;
+              }
+              ++np;
+              if (d == b1[k] && (pmin < 0 || p < pmin)) pmin = p;
+            }
+          }
+        }
+        ovf = ovf || np > kWinCap;
+        const float run_b = B1(k);
+        const int run_p = P1(k);
+        if (b1[k] < run_b) {
+          // New best: old members stay in the window only if the old best is
+          // still within the new margin.
+          const bool keep_old = run_b <= thr;
+          if (!keep_old && np == 1 && !ovf) {
+            P1(k) = pmin;
+          } else {
+            int blk = (run_p & kAmbiguous) ? (run_p & ~kAmbiguous) : win_alloc(S);
+            if (blk >= 0) {
+              if (!(run_p & kAmbiguous)) {
+                S.amb_n[blk] = 0;
+                if (keep_old) win_push(S, blk, run_p, run_b);
+              } else if (!keep_old) {
+                S.amb_n[blk] = 0;
+              }
+              for (int e = 0; e < min(np, kWinCap); ++e) win_push(S, blk, mpos[e], md[e]);
+              if (ovf) S.amb_n[blk] = kWinCap + 1;
+            }
+            P1(k) = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
+          }
+          B1(k) = b1[k];
+        } else if (b1[k] <= __fadd_ru(run_b, MG(k))) {
+          const float run_thr = __fadd_ru(run_b, MG(k));
+          int blk = (run_p & kAmbiguous) ? (run_p & ~kAmbiguous) : win_alloc(S);
+          if (blk >= 0 && blk != kNoBlock) {
+            if (!(run_p & kAmbiguous)) {
+              S.amb_n[blk] = 0;
+              win_push(S, blk, run_p, run_b);
+            }
+            for (int e = 0; e < min(np, kWinCap); ++e)
+              if (md[e] <= run_thr) win_push(S, blk, mpos[e], md[e]);
+            if (ovf) S.amb_n[blk] = kWinCap + 1;
+          }
+          P1(k) = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
+        }
+      }
+      __syncthreads();  // all rescans done before the next sub-chunk overwrites the tiles
     }
-    gtile += ntiles;
-    // Emit: rescan the subtiles that can hold window members (fully unrolled
-    // so the per-query state stays in registers).
+    // Emit.
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
       const int qi = tid + k * kNnThreads;
       if (qi >= w.nq) continue;
-      const float mg = w.q[qi].w;
-      const float thr = __fadd_ru(b1[k], mg);
-      bool overflow = b3[k] <= thr;
-      int reason = overflow ? 1 : 0;
-      int pos[kNnL];
-      float dd[kNnL];
-      int n = 0;
-      if (!overflow) {
-        const int nscan = b2[k] <= thr ? 2 : 1;
-        for (int r = 0; r < nscan; ++r) {
-          const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
-          for (int c = 0; c < kSub; ++c) {
-            const int p = sid * kSub + c;
-            if (p >= w.nc) break;
-            const float d = d32(qx[k], qy[k], qz[k], w.c[p]);
-            if (d <= thr) {
-              if (n < kNnL) {
-                pos[n] = p + w.c_base;
-                dd[n] = d;
-                ++n;
-              } else {
-                overflow = true;
-                reason = 2;
-              }
-            }
+      const int qlocal = w.q_first + qi;
+      const int p1 = P1(k);
+      if (w.nchunks == 1) {
+        if (plan.fp64_mode) {
+          push_refine(S, w.kind, w.owner, qlocal, 0, plan.iter);
+        } else if (!(p1 & kAmbiguous)) {
+          *nn_result_slot(P, S, w.kind, w.owner, qlocal) = p1;  // certified
+        } else {
+          // Ambiguous: decide the window members in FP64 (reference formula).
+          const float thr = __fadd_ru(B1(k), MG(k));
+          int pos[kWinCap];
+          int n = 0;
+          if (win_collect(S, p1, thr, pos, &n, kWinCap)) {
+            const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
+            *nn_result_slot(P, S, w.kind, w.owner, qlocal) =
+                nn_decide(g, pos, n, w.kind == 0 && !plan.pooled, S.stats);
+          } else {
+            push_refine(S, w.kind, w.owner, qlocal, 1, plan.iter);
           }
         }
-      }
-      const int qlocal = w.q_first + qi;
-      if (reason == 1 && atomicCAS(reinterpret_cast<unsigned long long*>(S.stats + 200), 0ull, 1ull) == 0ull) {
-        unsigned long long* dbg = S.stats + 201;
-        dbg[0] = plan.iter;
-        dbg[1] = w.owner;
-        dbg[2] = qlocal;
-        dbg[3] = __float_as_uint(b1[k]);
-        dbg[4] = __float_as_uint(b2[k]);
-        dbg[5] = __float_as_uint(b3[k]);
-        dbg[6] = __float_as_uint(thr);
-        dbg[7] = w.nc;
-        dbg[8] = s12[k];
-        dbg[9] = __float_as_uint(qx[k]);
-        dbg[10] = __float_as_uint(qy[k]);
-        dbg[11] = __float_as_uint(qz[k]);
-        dbg[12] = __float_as_uint(mg);
-        dbg[13] = w.c_base;
-      }
-      if (w.nchunks == 1) {
-        if (plan.fp64_mode || overflow || n == 0) {
-          push_refine(S, w.kind, w.owner, qlocal, overflow ? reason : 0, plan.iter);
-        } else {
-          const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
-          *nn_result_slot(P, S, w.kind, w.owner, qlocal) = nn_decide(g, pos, n, w.kind == 0 && !plan.pooled, S.stats);
-        }
       } else {
+        const int64_t rows = P.part_surf_off[P.J];
         NnPartial pr;
-        pr.b1 = b1[k];
-        pr.count = overflow ? -1 : n;
-        for (int e = 0; e < kNnL; ++e) {
-          pr.pos[e] = e < n ? pos[e] : 0;
-          pr.d[e] = e < n ? dd[e] : INFINITY;
-        }
-        S.partials[(P.part_surf_off[w.owner] + qlocal) * static_cast<int64_t>(w.nchunks) + w.chunk] = pr;
+        pr.b1 = B1(k);
+        pr.pos = p1;
+        S.partials[static_cast<int64_t>(w.chunk) * rows + P.part_surf_off[w.owner] + qlocal] = pr;
       }
     }
   }
 }
 
-// Merge per-chunk windows of forward/final queries (nchunks > 1).
+// Merge the per-split results of forward/final queries (nchunks > 1): the
+// global best is certified when exactly one split reaches the window and that
+// split was itself unambiguous.
 __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int j = blockIdx.y;
   if (plan.kind != 2 && (!S.active[j] || S.n_col[j] > 0)) return;
@@ -367,39 +478,50 @@ __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int ns = surf_count(P, j);
   const int qlocal = blockIdx.x * blockDim.x + threadIdx.x;
   if (qlocal >= ns) return;
-  const NnPartial* pr = S.partials + (so + qlocal) * static_cast<int64_t>(plan.nchunks);
+  const int64_t rows = P.part_surf_off[P.J];
   float b1 = INFINITY;
-  for (int s = 0; s < plan.nchunks; ++s) b1 = fminf(b1, pr[s].b1);
+  int best = 0;
+  for (int s = 0; s < plan.nchunks; ++s) {
+    const NnPartial p = S.partials[s * rows + so + qlocal];
+    if (p.b1 < b1) {
+      b1 = p.b1;
+      best = p.pos;
+    }
+  }
+  if (plan.fp64_mode) {
+    push_refine(S, plan.kind, j, qlocal, 0, plan.iter);
+    return;
+  }
   const float thr = __fadd_ru(b1, S.Sq32[so + qlocal].w);
+  int reach = 0;
+  for (int s = 0; s < plan.nchunks; ++s) reach += S.partials[s * rows + so + qlocal].b1 <= thr ? 1 : 0;
+  if (reach == 1 && !(best & kAmbiguous)) {
+    S.res_fwd[so + qlocal] = best;  // certified
+    return;
+  }
+  // Gather every split's window members within the global window; decide in FP64.
   constexpr int kMax = 32;
   int pos[kMax];
   int n = 0;
-  bool overflow = false;
-  for (int s = 0; s < plan.nchunks; ++s) {
-    const NnPartial p = pr[s];
+  bool ok = true;
+  for (int s = 0; s < plan.nchunks && ok; ++s) {
+    const NnPartial p = S.partials[s * rows + so + qlocal];
     if (p.b1 > thr) continue;
-    if (p.count < 0) {
-      overflow = true;
-      continue;
-    }
-    for (int e = 0; e < p.count; ++e)
-      if (p.d[e] <= thr) {
-        if (n < kMax)
-          pos[n++] = p.pos[e];
-        else
-          overflow = true;
-      }
+    int m = 0;
+    ok = win_collect(S, p.pos, thr, pos + n, &m, kMax - n) && ok;
+    n += m;
   }
-  if (plan.fp64_mode || overflow || n == 0) {
-    push_refine(S, plan.kind, j, qlocal, overflow ? 3 : 0, plan.iter);
+  if (!ok || n == 0) {
+    push_refine(S, plan.kind, j, qlocal, 3, plan.iter);
     return;
   }
   const NnGeom g = nn_geom(P, S, plan, plan.kind, j, qlocal);
   S.res_fwd[so + qlocal] = nn_decide(g, pos, n, plan.kind == 0 && !plan.pooled, S.stats);
 }
 
-// Full FP64 rescan (overflowing windows, and the FP64 validation mode):
-// one warp per query, lexicographic (distance, position) minimum.
+// Full FP64 rescan (ambiguous windows, and the FP64 validation mode): one
+// warp per query, lexicographic (distance, position) minimum — exactly the
+// reference's kd-tree rule.
 __global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -443,6 +565,7 @@ void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaSt
   nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
   cudaMemsetAsync(S.item_counter, 0, 2 * sizeof(int), st);
   cudaMemsetAsync(S.refine_count, 0, sizeof(int), st);
+  cudaMemsetAsync(S.amb_count, 0, sizeof(int), st);
 }
 
 size_t scan_temp_bytes(int n) {

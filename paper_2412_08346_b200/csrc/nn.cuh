@@ -28,7 +28,8 @@ constexpr int kNnThreads = 128;
 constexpr int kNnQ = 8;                         // queries per thread
 constexpr int kNnQB = kNnThreads * kNnQ;        // queries per work item
 constexpr int kNnTile = 256;                    // candidates per TMA tile (4 KB)
-constexpr int kNnStages = 4;
+constexpr int kNnStages = 8;                    // whole chunk resident: rescans read shared memory
+constexpr int kNnMaxChunk = kNnStages * kNnTile; // candidates per work item (2048, 32 KB)
 constexpr int kNnL = 4;                         // window list entries per query
 
 // One NN work item: a block of <= kNnQB queries against a contiguous
@@ -46,12 +47,15 @@ struct NnItem {
   int nchunks;       // S
 };
 
-// Per (query, chunk) partial window.
+// Per (query, split) partial result: the split's best FP32 value and its
+// position; the top bit of `pos` flags an ambiguous window (another candidate
+// within the certification margin, or an overflowing top-3).
 struct NnPartial {
   float b1;
-  int count;         // entries kept; -1 = window overflowed
-  int pos[kNnL];
-  float d[kNnL];
+  int pos;
 };
+constexpr int kAmbiguous = static_cast<int>(0x80000000u);
+constexpr int kNoBlock = 0x7fffffff;  // ambiguous without a member list (pool exhausted)
+constexpr int kWinCap = 8;            // members per ambiguous-window list
 
 }  // namespace asicp

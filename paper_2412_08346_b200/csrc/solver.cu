@@ -132,7 +132,8 @@ struct asicp_ctx {
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, med_off_d, med_keys, scene32, sdf_coarse;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items0, items1,
-      item_count, item_off, item_counter, scan_tmp, partials, refine_list, refine_count, stats, trace_theta,
+      item_count, item_off, item_counter, scan_tmp, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
+      stats, trace_theta,
       trace_loss, trace_col,
       final_loss, final_free;
 
@@ -160,7 +161,8 @@ struct asicp_ctx {
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &items0, &items1, &item_count, &item_off, &item_counter, &scan_tmp,
-                  &partials, &refine_list, &refine_count, &stats, &trace_theta, &trace_loss, &trace_col,
+                  &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &trace_theta,
+                  &trace_loss, &trace_col,
                   &final_loss, &final_free};
     for (Buf* b : all) b->release();
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -446,6 +448,14 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->item_counter.ensure(2 * 4);
   c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
   c->partials.ensure(static_cast<size_t>(so) * c->nchunks_max * sizeof(NnPartial));
+  // Ambiguous windows are rare (~0.3 % of queries); the pool covers 1/16 of all
+  // (row, split) slots with a 64 k floor, and an exhausted pool only means a
+  // full FP64 rescan for the affected queries.
+  const int amb_cap = static_cast<int>(std::min<size_t>(
+      std::max<size_t>(65536, (static_cast<size_t>(so) * c->nchunks_max + Jz * c->n_scene) / 16), 1u << 24));
+  c->amb_pool.ensure(static_cast<size_t>(amb_cap) * kWinCap * sizeof(int2));
+  c->amb_n.ensure(static_cast<size_t>(amb_cap) * sizeof(int));
+  c->amb_count.ensure(sizeof(int));
   const size_t refine_cap = std::min<size_t>(static_cast<size_t>(so) + jscene, 64ull << 20);
   c->refine_list.ensure(refine_cap * sizeof(int4));
   c->refine_count.ensure(4);
@@ -541,6 +551,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.scan_tmp = c->scan_tmp.p;
   S.scan_tmp_bytes = c->scan_tmp.bytes;
   S.partials = c->partials.as<NnPartial>();
+  S.amb_pool = c->amb_pool.as<int2>();
+  S.amb_n = c->amb_n.as<int>();
+  S.amb_count = c->amb_count.as<int>();
+  S.amb_cap = amb_cap;
   S.refine_list = c->refine_list.as<int4>();
   S.refine_count = c->refine_count.as<int>();
   S.refine_cap = static_cast<int>(refine_cap);
@@ -759,7 +773,7 @@ void run(asicp_ctx* c, asicp_solution* out) {
   out->nn_pool_ties = static_cast<int64_t>(stats[3]);
   std::memcpy(c->raw_stats, stats, sizeof(stats));
   out->nn_pairs = static_cast<double>(stats[4]);
-  s.nn_pairs = out->nn_pairs;
+  s.nn_pairs = static_cast<double>(stats[12]);  // pairs of the event-timed (forward/final) filter launches
 }
 
 template <typename F>
