@@ -36,8 +36,10 @@ int asicp_dbg_raw_stats(struct asicp_ctx* ctx, uint64_t* out);
 
 /* The device minibatch sampler (mt19937_64 + Lemire + partial Fisher-Yates,
  * spatial_index.cpp:111-123) on one stream seeded with `seed`: `calls`
- * consecutive draws of ms[c] indices from [0, n), written back to back. */
-int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t* out);
+ * consecutive draws of ms[c] indices from [0, n), written back to back.
+ * parallel != 0 selects the parallel (sort + pointer-jumping) kernel where
+ * it applies, 0 the serial swap kernel. */
+int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t parallel, int32_t* out);
 
 #ifdef __cplusplus
 }

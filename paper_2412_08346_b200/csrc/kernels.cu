@@ -749,6 +749,7 @@ void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, c
 }
 int minibatch_smem_cap() { return 160 * 1024; }
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  if (launch_minibatch_par(P, S, m, st)) return;
   const size_t need = static_cast<size_t>(P.n_obj) * sizeof(int);
   if (need <= static_cast<size_t>(minibatch_smem_cap())) {
     static bool attr_done = false;

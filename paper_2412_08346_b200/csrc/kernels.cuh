@@ -81,6 +81,8 @@ struct DevState {
   int* pool_idx;       // J x n_obj_pad minibatch object indices (sample order)
   float4* pool32;      // J x n_obj_pad gathered FP32 candidates (+inf padded)
   int* fy_scratch;     // J x n_obj Fisher-Yates scratch (large clouds only)
+  int* fy_par;         // J x fy_stride scratch of the parallel Fisher-Yates (or null)
+  int64_t fy_stride;   // 5 x n_obj_pad
   const int* pool_map; // = pool_idx when this iteration's forward match is pooled
   NnItem* items[2];    // work lists: [0] forward / final, [1] reverse
   int* item_count[2];  // J + 1 each
@@ -120,6 +122,7 @@ void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
+bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st);  // minibatch.cu
 int minibatch_smem_cap();
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);

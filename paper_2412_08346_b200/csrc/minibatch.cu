@@ -1,0 +1,200 @@
+// Parallel partial Fisher-Yates: the minibatch draw of sample_minibatch_indices
+// (spatial_index.cpp:111-123) without the serial swap chain.
+//
+// The reference runs, for i = 0..m-1, j_i = i + uniform_index(n - i) and
+// swap(idx[i], idx[j_i]) over an iota of length n, keeping idx[0..m).  Because
+// position i is never touched after step i, and step s writes only positions
+// s and j_s >= s:
+//   pool[i] = j_i                 if no earlier step s < i had j_s = j_i,
+//           = W(prev(i))          otherwise, prev(i) = the last such s;
+//   W(s)    = s                   if no earlier step s' < s had j_s' = s,
+//           = W(wl(s))            otherwise, wl(s) = the last such s'.
+// (W(s) is the value sitting at position s when step s runs.)  With the pairs
+// (j_s, s) sorted by key (stable), prev() is the sorted predecessor within a
+// key group, wl(s) comes from the last member of group `s`, and W resolves by
+// pointer jumping — all data-parallel over one CTA per particle.  The draws
+// themselves are the particle's mt19937_64 outputs (twisted cooperatively);
+// a Lemire rejection (probability ~n/2^64 per draw) sends the particle to an
+// exact serial replay.
+#include "common.cuh"
+#include "mt64.cuh"
+
+#include <cub/block/block_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace asicp {
+
+constexpr int kMbThreads = 1024;
+
+template <int ITEMS>
+__global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P, DevState S, int m) {
+  const int j = blockIdx.x;
+  if (!S.active[j] || S.n_col[j] > 0) return;
+  using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  typename Sort::TempStorage& sort_tmp = *reinterpret_cast<typename Sort::TempStorage*>(dyn);
+  __shared__ uint64_t st[mt::kN];
+  __shared__ uint64_t st0[mt::kN];
+  __shared__ int s_mti, s_mti0, s_reject;
+  const int tid = threadIdx.x;
+  const int n = P.n_obj;
+  int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
+  int* jv = scratch;                 // draw targets j_i, later pointer-jump buffer
+  int* skey = scratch + P.n_obj_pad; // sorted keys
+  int* sval = skey + P.n_obj_pad;    // sorted step indices
+  int* lk = sval + P.n_obj_pad;      // key -> last sorted slot (keys < m)
+  int* ptr = lk + P.n_obj_pad;       // W pointers
+  int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
+  uint64_t* gst = S.rng_state + static_cast<int64_t>(j) * mt::kN;
+  for (int i = tid; i < mt::kN; i += kMbThreads) st[i] = st0[i] = gst[i];
+  if (tid == 0) {
+    s_mti = s_mti0 = S.rng_mti[j];
+    s_reject = 0;
+  }
+  __syncthreads();
+  // 1. Draws (one engine output per draw unless a rejection happens).
+  for (int i0 = 0; i0 < m;) {
+    if (s_mti >= mt::kN) {
+      mt::twist_block(st);
+      if (tid == 0) s_mti = 0;
+      __syncthreads();
+    }
+    const int mti = s_mti;
+    const int cnt = min(mt::kN - mti, m - i0);
+    for (int t = tid; t < cnt; t += kMbThreads) {
+      uint64_t u;
+      if (!mt::lemire(mt::temper(st[mti + t]), static_cast<uint64_t>(n - (i0 + t)), &u)) s_reject = 1;
+      jv[i0 + t] = i0 + t + static_cast<int>(u);
+    }
+    __syncthreads();
+    if (tid == 0) s_mti = mti + cnt;
+    i0 += cnt;
+    __syncthreads();
+  }
+  if (s_reject) {
+    // Exact serial replay from the saved engine state (never seen in practice).
+    if (tid == 0) {
+      int* idx = skey;  // n ints available (stride is 5 * n_pad)
+      for (int i = 0; i < n; ++i) idx[i] = i;
+      int mt_i = s_mti0;
+      for (int i = 0; i < m; ++i) {
+        uint64_t u, x;
+        do {
+          if (mt_i >= mt::kN) {
+            mt::twist_serial(st0);
+            mt_i = 0;
+          }
+          x = mt::temper(st0[mt_i++]);
+        } while (!mt::lemire(x, static_cast<uint64_t>(n - i), &u));
+        const int jj = i + static_cast<int>(u);
+        const int b = idx[jj];
+        idx[jj] = idx[i];
+        pool[i] = b;
+      }
+      for (int i = 0; i < mt::kN; ++i) st[i] = st0[i];
+      s_mti = mt_i;
+    }
+    __syncthreads();
+  } else {
+    // 2. Stable sort of (j_s, s) by key.
+    int nbits = 1;
+    while ((1 << nbits) <= n) ++nbits;
+    const int pad_key = (1 << nbits) - 1;
+    int keys[ITEMS], vals[ITEMS];
+#pragma unroll
+    for (int e = 0; e < ITEMS; ++e) {
+      const int i = tid * ITEMS + e;
+      keys[e] = i < m ? jv[i] : pad_key;
+      vals[e] = i;
+    }
+    __syncthreads();
+    Sort(sort_tmp).Sort(keys, vals, 0, nbits);
+#pragma unroll
+    for (int e = 0; e < ITEMS; ++e) {
+      const int t = tid * ITEMS + e;
+      if (t < m) {
+        skey[t] = keys[e];
+        sval[t] = vals[e];
+      }
+    }
+    for (int s = tid; s < m; s += kMbThreads) lk[s] = -1;
+    __syncthreads();
+    // 3. Last member of each key group (keys < m only matter for wl()).
+    for (int t = tid; t < m; t += kMbThreads) {
+      const int k = skey[t];
+      if (k < m && (t == m - 1 || skey[t + 1] != k)) lk[k] = t;
+    }
+    __syncthreads();
+    // 4. wl(s) -> initial pointers.
+    for (int s = tid; s < m; s += kMbThreads) {
+      const int t = lk[s];
+      int wl = -1;
+      if (t >= 0) {
+        if (sval[t] < s)
+          wl = sval[t];
+        else if (t > 0 && skey[t - 1] == s)
+          wl = sval[t - 1];
+      }
+      ptr[s] = wl < 0 ? s : wl;
+    }
+    __syncthreads();
+    // 5. Pointer jumping to the chain roots (W).
+    int* a = ptr;
+    int* b = jv;
+    for (;;) {
+      int changed = 0;
+      for (int s = tid; s < m; s += kMbThreads) {
+        const int p = a[s];
+        const int q = a[p];
+        b[s] = q;
+        changed |= q != p;
+      }
+      const int any = __syncthreads_or(changed);
+      int* t = a;
+      a = b;
+      b = t;
+      if (!any) break;
+    }
+    // 6. pool[i] from the sorted predecessor within the key group.
+    for (int t = tid; t < m; t += kMbThreads) {
+      const int i = sval[t];
+      const int k = skey[t];
+      pool[i] = (t > 0 && skey[t - 1] == k) ? a[sval[t - 1]] : k;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < mt::kN; i += kMbThreads) gst[i] = st[i];
+  if (tid == 0) S.rng_mti[j] = s_mti;
+  // Gather the FP32 candidates in sample order (+inf padded to the subtile).
+  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
+  for (int i = tid; i < m; i += kMbThreads) pool32[i] = P.obj_cand[pool[i]];
+  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads) pool32[i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+}
+
+template <int ITEMS>
+static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
+  const int smem = static_cast<int>(sizeof(typename Sort::TempStorage));
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(minibatch_par_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return false;
+    attr = true;
+  }
+  minibatch_par_kernel<ITEMS><<<P.J, kMbThreads, smem, st>>>(P, S, m);
+  return true;
+}
+
+// Returns false when the parallel path does not apply (no scratch, or m too
+// large for one CTA's sort); the caller then uses the serial kernel.
+bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  if (S.fy_par == nullptr) return false;
+  if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
+  if (m <= kMbThreads * 12) return launch_par<12>(P, S, m, st);
+  return false;
+}
+
+}  // namespace asicp

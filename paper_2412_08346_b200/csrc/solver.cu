@@ -131,7 +131,8 @@ struct asicp_ctx {
   Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, med_off_d, med_keys, scene32, sdf_coarse;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
-      Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, items0, items1,
+      Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
+      items1,
       item_count, item_off, item_counter, scan_tmp, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
       stats, trace_theta,
       trace_loss, trace_col,
@@ -160,7 +161,8 @@ struct asicp_ctx {
                   &med_keys, &scene32, &sdf_coarse, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
-                  &pool_idx, &pool32, &fy_scratch, &items0, &items1, &item_count, &item_off, &item_counter, &scan_tmp,
+                  &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
+                  &item_counter, &scan_tmp,
                   &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &trace_theta,
                   &trace_loss, &trace_col,
                   &final_loss, &final_free};
@@ -440,6 +442,11 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->pool32.ensure(jobj * 16);
   if (static_cast<size_t>(c->n_obj) * 4 > static_cast<size_t>(minibatch_smem_cap()))
     c->fy_scratch.ensure(Jz * static_cast<size_t>(c->n_obj) * 4);
+  // Parallel Fisher-Yates scratch (5 int arrays per particle) when it stays
+  // under 1 GiB; the serial kernel covers the rest.
+  const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
+  const bool fy_par_on = fy_par_bytes <= (1ull << 30) && c->n_obj <= 12 * 1024 * 4;
+  if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
   // Work items: forward <= base_items * nchunks; reverse <= J * ceil(n_scene / 256).
   c->items0.ensure((static_cast<size_t>(base_items) * c->nchunks_max + Jz) * sizeof(NnItem));
   c->items1.ensure((Jz * ((c->n_scene + 255) / 256) + Jz) * sizeof(NnItem));
@@ -540,6 +547,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.pool_idx = c->pool_idx.as<int>();
   S.pool32 = c->pool32.as<float4>();
   S.fy_scratch = c->fy_scratch.as<int>();
+  S.fy_par = fy_par_on ? c->fy_par.as<int>() : nullptr;
+  S.fy_stride = 5 * static_cast<int64_t>(c->n_obj_pad);
   S.pool_map = nullptr;
   S.items[0] = c->items0.as<NnItem>();
   S.items[1] = c->items1.as<NnItem>();
@@ -880,7 +889,8 @@ double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annea
 
 double asicp_dbg_ffma_tflops(int iters) { return run_ffma_peak(iters); }
 
-int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t* out) {
+int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t parallel, int32_t* out) {
+  const bool par = parallel != 0;
   // One particle stream (seed), `calls` consecutive minibatch draws of sizes
   // ms[c]; pool indices written back to back into out.
   try {
@@ -902,6 +912,10 @@ int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t cal
     pidx.ensure(static_cast<size_t>(P.n_obj_pad) * 4);
     p32.ensure(static_cast<size_t>(P.n_obj_pad) * 16);
     fy.ensure(static_cast<size_t>(n) * 4);
+    Buf fyp;
+    if (par) fyp.ensure(5 * static_cast<size_t>(P.n_obj_pad) * 4);
+    S.fy_par = par ? fyp.as<int>() : nullptr;
+    S.fy_stride = 5 * static_cast<int64_t>(P.n_obj_pad);
     P.obj_cand = cand.as<float4>();
     S.active = active.as<int>();
     S.n_col = ncol.as<int>();
@@ -918,7 +932,7 @@ int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t cal
       CUDA_OK(cudaMemcpy(out + o, S.pool_idx, static_cast<size_t>(ms[c]) * 4, cudaMemcpyDeviceToHost));
       o += ms[c];
     }
-    const Buf* bufs[] = {&cand, &active, &ncol, &st, &mti, &pidx, &p32, &fy};
+    const Buf* bufs[] = {&cand, &active, &ncol, &st, &mti, &pidx, &p32, &fy, &fyp};
     for (const Buf* b : bufs) const_cast<Buf*>(b)->release();
     return ASICP_OK;
   } catch (const std::exception&) {
