@@ -1,0 +1,132 @@
+"""Object / preshape sharding across ranks.
+
+Stein populations are per preshape and particles never migrate
+(grasp.cpp:213-234); particle j's minibatch stream is seeded with seed + j over
+the preshape-major flattening (grasp.cpp:135-151); the only cross-preshape step
+is the final argmin (grasp.cpp:283-306).  So an (object, preshape) unit solved
+on its own — the object's problem restricted to that preshape, with the seed
+advanced by the unit's first global particle index and the preshape's stacked
+SDF offset kept — reproduces exactly the particles the full solve would, and
+the per-object answer is a tiny gather of particle summaries followed by the
+reference's selection rule.  No collective touches the data path.
+
+`solve_sharded` is solver-agnostic (the B200 Solver in production, the CPU
+restatement in the multi-process tests) and takes an `all_gather` callable
+(torch.distributed.all_gather_object over NCCL or gloo).
+"""
+from __future__ import annotations
+
+import copy
+from dataclasses import dataclass
+from typing import Callable, List, Sequence
+
+import numpy as np
+
+from .grasp import GraspProblem, GraspStatus, StackedSdf
+
+
+@dataclass
+class Unit:
+    obj: int          # object (problem) index
+    preshape: int     # preshape index within the object
+    first: int        # first global particle index of the preshape
+    count: int        # particles
+
+
+def units_of(problems: Sequence[GraspProblem]) -> List[Unit]:
+    out = []
+    for o, p in enumerate(problems):
+        first = 0
+        for s, init in enumerate(p.initializations):
+            k = len(np.asarray(init).reshape(-1, 7))
+            out.append(Unit(o, s, first, k))
+            first += k
+    return out
+
+
+def assign(units: Sequence[Unit], world: int) -> List[int]:
+    """Longest-processing-time assignment of units to ranks (deterministic)."""
+    load = [0] * world
+    owner = [0] * len(units)
+    for i in sorted(range(len(units)), key=lambda i: (-units[i].count, i)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        owner[i] = r
+        load[r] += units[i].count
+    return owner
+
+
+def subproblem(p: GraspProblem, u: Unit) -> GraspProblem:
+    """The object's problem restricted to one preshape (same SDF grid and
+    offset, seed advanced to the preshape's first global particle)."""
+    q = copy.copy(p)
+    pre = copy.copy(p.preshapes[u.preshape])
+    g = pre.sdf_index
+    q.sdf = StackedSdf([p.sdf.grids[g]], p.sdf.epsilon, [p.sdf.offsets[g]])
+    pre.sdf_index = 0
+    q.preshapes = [pre]
+    q.initializations = [p.initializations[u.preshape]]
+    q.seed = int(p.seed) + u.first
+    q.record_trace = False
+    return q
+
+
+def select(theta, loss, free, conv, preshape):
+    """grasp.cpp:283-306: strict < over collision-free particles in global
+    order, else the best attempt with kNoGraspFound."""
+    best = -1
+    for j in range(len(loss)):
+        if free[j] and (best < 0 or loss[j] < loss[best]):
+            best = j
+    status = GraspStatus.kFound
+    if best < 0:
+        status = GraspStatus.kNoGraspFound
+        for j in range(len(loss)):
+            if best < 0 or loss[j] < loss[best]:
+                best = j
+    return dict(status=status, theta=np.asarray(theta[best]), preshape_id=int(preshape[best]),
+                final_loss=float(loss[best]), converged=bool(conv[best]), particle_theta=np.asarray(theta),
+                particle_loss=np.asarray(loss), particle_collision_free=np.asarray(free),
+                particle_converged=np.asarray(conv), particle_preshape=np.asarray(preshape))
+
+
+def solve_local(problems: Sequence[GraspProblem], solve_fn: Callable[[GraspProblem], object], rank: int,
+                world: int) -> list:
+    """Solve the (object, preshape) units owned by `rank`; returns the
+    particle summaries to gather."""
+    units = units_of(problems)
+    owner = assign(units, world)
+    mine = []
+    for i, u in enumerate(units):
+        if owner[i] != rank:
+            continue
+        sol = solve_fn(subproblem(problems[u.obj], u))
+        mine.append((i, np.asarray(sol.particle_theta), np.asarray(sol.particle_loss),
+                     np.asarray(sol.particle_collision_free), np.asarray(sol.particle_converged)))
+    return mine
+
+
+def solve_sharded(problems: Sequence[GraspProblem], solve_fn: Callable[[GraspProblem], object], rank: int,
+                  world: int, all_gather: Callable[[object], list]) -> list:
+    """Solve every (object, preshape) unit owned by `rank`, gather the
+    summaries from all ranks and return the per-object selections (identical
+    on every rank)."""
+    return combine(problems, all_gather(solve_local(problems, solve_fn, rank, world)))
+
+
+def combine(problems: Sequence[GraspProblem], gathered: list) -> list:
+    """Per-object selection from the gathered unit summaries."""
+    units = units_of(problems)
+    by_unit = {}
+    for part in gathered:
+        for rec in part:
+            by_unit[rec[0]] = rec[1:]
+    results = []
+    for o, _ in enumerate(problems):
+        idx = [i for i, u in enumerate(units) if u.obj == o]
+        theta = np.concatenate([by_unit[i][0] for i in idx])
+        loss = np.concatenate([by_unit[i][1] for i in idx])
+        free = np.concatenate([by_unit[i][2] for i in idx])
+        conv = np.concatenate([by_unit[i][3] for i in idx])
+        pre = np.concatenate([np.full(units[i].count, units[i].preshape) for i in idx])
+        results.append(select(theta, loss, free, conv, pre))
+    return results

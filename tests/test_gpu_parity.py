@@ -133,6 +133,27 @@ def test_invalid_arguments_match_reference(solver, oracle):
     del base
 
 
+def test_preshape_sharding_on_gpu_is_bit_identical(solver):
+    """Object/preshape sharding (shard.py) with the B200 solver: three
+    simulated ranks solve their (object, preshape) units independently; the
+    combined answers equal the unsharded B200 solves bit for bit."""
+    from paper_2412_08346_b200 import shard
+
+    problems = []
+    for seed in (0, 1):
+        problems.append(fixtures.config(2, seed=seed, particles_per_preshape=6).set(
+            k_max=10, k_stein=4, anneal_period_total=10).problem())
+    world = 3
+    parts = [shard.solve_local(problems, solver.optimize, r, world) for r in range(world)]
+    got = shard.combine(problems, parts)
+    for res, p in zip(got, problems):
+        want = solver.optimize(p)
+        assert int(res["status"]) == int(want.status)
+        assert np.array_equal(res["theta"], want.theta)
+        assert res["final_loss"] == want.final_loss
+        assert np.array_equal(res["particle_theta"], want.particle_theta)
+
+
 def test_golden_vectors_without_oracle(solver):
     """The committed golden vectors (reference outputs) on the GPU path."""
     from pathlib import Path
