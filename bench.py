@@ -1,17 +1,26 @@
 #!/usr/bin/env python
 """B200 AS-ICP bench: particle-iterations/s and per-grasp solve latency.
 
-Workload (BASELINE.json configs[1]): 3 KG3 preshapes x 256
-particles (J = 768) against a 10k-point synthetic cylinder, 64^3 gripper SDFs,
-k_max = 100 (38 annealed Stein + 62 SGD iterations).  One step = one complete
-optimize_grasp solve: J * k_max = 76,800 particle-iterations.
+Default workload (BASELINE.json configs[1]): 3 KG3
+preshapes x 256 particles (J = 768) against a 10k-point synthetic cylinder,
+64^3 gripper SDFs, k_max = 100 (38 annealed Stein + 62 SGD iterations).  One
+step = one complete optimize_grasp solve: J * k_max = 76,800
+particle-iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload cfg2|cfg3|cfg4]
 
-N > 1 runs under torchrun, one rank per GPU; each rank solves its own object
-instance (object sharding, cfg4 semantics: no data-path collective), so the
-scaling is weak and `value` is the total particle-iterations of all ranks over
-the max-over-ranks device time.
+cfg2 / cfg3 at N > 1 run under torchrun, one rank per GPU; each rank solves its
+own object instance (object sharding: no data-path collective), so the scaling
+is weak and `value` is the total particle-iterations of all ranks over the
+max-over-ranks device time.
+
+cfg4 (BASELINE.json configs[3]) is the 11-object batch x 3 KG3 preshapes x
+1024 particles (40 iterations): its 33 (object, preshape) units are spread over
+the ranks by longest-processing-time (shard.py), each rank keeps its units
+device-resident and overlaps them on one GPU (batch.py), and the per-object
+answers are gathered and selected after the solves.  Total work is fixed, so
+the scaling is strong.
 """
 from __future__ import annotations
 
@@ -32,8 +41,15 @@ import numpy as np  # noqa: E402
 
 METRIC = "particle-iterations/sec"
 UNIT = "particle-iterations/s"
-CFG = 2
 PAPER_LATENCY_S = 0.926  # a different metric (latency), not vs_baseline
+WORKLOADS = {
+    "cfg2": (2, "cfg2: 3 KG3 preshapes x 256 particles vs 10k-pt cylinder, 64^3 SDF, 100 iters (38 Stein)"),
+    "cfg3": (3, "cfg3: noisy 40%-occluded single-view 20k-pt scan, 3 KG3 preshapes x 1024 particles, 40 iters "
+                "(15 Stein), SDF collision on"),
+    "cfg4": (4, "cfg4: 11-object batch (cylinders/boxes/spheres/blobs, 10k pts) x 3 KG3 preshapes x 1024 "
+                "particles, 40 iters (15 Stein), (object, preshape) units sharded over ranks"),
+}
+N_BATCH_OBJECTS = 11
 
 
 def parse():
@@ -42,6 +58,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -111,6 +128,10 @@ def problem_bytes(view) -> int:
     return int(b)
 
 
+def solution_bytes(J: int) -> int:
+    return J * (7 * 8 + 8 + 4 + 4) + 64
+
+
 def cpu_reference(fixture, threads: int):
     """Reference optimize_grasp (oracle/_ref) on the host cores, full workload."""
     from oracle import ref
@@ -123,18 +144,24 @@ def cpu_reference(fixture, threads: int):
     return dt, sol
 
 
+def sample_fixture(workload: str, seed: int = 0):
+    """The bounded CPU-reference sample: one full solve of one object."""
+    from paper_2412_08346_b200 import fixtures
+
+    return fixtures.config(WORKLOADS[workload][0], seed=seed)
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from oracle import ref
-    from paper_2412_08346_b200 import fixtures
 
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
         return 0
     threads = os.cpu_count() or 1
-    fx = fixtures.config(CFG, seed=0)
+    fx = sample_fixture(args.workload)
     pits = fx.J * fx.k_max
     for _ in range(args.warmup):
         cpu_reference(fx, threads)
@@ -144,28 +171,62 @@ def run_reference_arm(args):
         times.append(dt)
     ms = 1e3 * float(np.mean(times))
     value = pits / (ms * 1e-3)
+    sample = (f"full {args.workload} solve of object 0 ({pits} particle-iterations) per step, "
+              f"graspmatch::optimize_grasp workers={threads}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(fx, world),
+        "scaling": "strong" if args.workload == "cfg4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args.workload, fx, world),
         "solve_latency_ms": ms,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full cfg2 solve ({pits} particle-iterations) per step, "
-                                   f"graspmatch::optimize_grasp workers={threads}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(fx, world):
+def config_dict(workload, fx, world):
     v = fx.struct
-    return {"workload": "cfg2: 3 KG3 preshapes x 256 particles vs 10k-pt cylinder, 64^3 SDF, 100 iters (38 Stein)",
-            "particles": fx.J, "k_max": fx.k_max, "k_stein": fx.k_stein, "n_object": int(v.n_object),
-            "n_scene": int(v.n_scene), "n_surface": int(v.preshapes[0].n_surface),
-            "sdf_dims": list(v.sdf_grids[0].dims), "parallelism": f"object-shard x{world}" if world > 1 else "1 GPU",
-            "l2": "flushed (256 MiB write) before every timed step", "step": "one full optimize_grasp solve"}
+    d = {"workload": WORKLOADS[workload][1],
+         "particles": fx.J, "k_max": fx.k_max, "k_stein": fx.k_stein, "n_object": int(v.n_object),
+         "n_scene": int(v.n_scene), "n_surface": int(v.preshapes[0].n_surface),
+         "sdf_dims": list(v.sdf_grids[0].dims),
+         "l2": "flushed (256 MiB write) before every timed step"}
+    if workload == "cfg4":
+        d.update({"objects": N_BATCH_OBJECTS, "units": 3 * N_BATCH_OBJECTS,
+                  "parallelism": f"(object, preshape) units, LPT over {world} GPU(s), overlapped streams per GPU",
+                  "step": "all 11 objects solved (33 units) + per-object selection"})
+    else:
+        d.update({"parallelism": f"object-shard x{world}" if world > 1 else "1 GPU",
+                  "step": "one full optimize_grasp solve"})
+    return d
+
+
+class Timer:
+    """Device time of a region spanning several streams: a start event on the
+    main stream that every worker stream waits on, and an end event recorded
+    after the main stream has waited on every worker."""
+
+    def __init__(self, torch, main, workers):
+        self.torch, self.main, self.workers = torch, main, workers
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.b = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        self.a.record(self.main)
+        for s in self.workers:
+            s.wait_event(self.a)
+
+    def stop(self):
+        for s in self.workers:
+            e = self.torch.cuda.Event()
+            e.record(s)
+            self.main.wait_event(e)
+        self.b.record(self.main)
+
+    def ms(self):
+        return self.a.elapsed_time(self.b)
 
 
 def main():
@@ -181,15 +242,13 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2412_08346_b200 import Solver, fixtures
+    from paper_2412_08346_b200 import Solver, fixtures, shard
     from paper_2412_08346_b200 import _lib as L
+    from paper_2412_08346_b200.batch import BatchSolver
+    from paper_2412_08346_b200.grasp import CProblem
     import ctypes as C
 
-    stream = torch.cuda.current_stream()
-    fx = fixtures.config(CFG, seed=rank)  # object instance per rank (object sharding)
-    pits = fx.J * fx.k_max
-    solver = Solver(device=local, stream=stream.cuda_stream)
-    solver.prepare(fx)
+    main_stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -197,48 +256,111 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    def all_max(x: float) -> float:
+        t = torch.tensor([x], device="cuda")
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_gather(obj):
+        if dist is None:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    batch = args.workload == "cfg4"
+    if batch:
+        problems = [fixtures.config(4, seed=o).problem() for o in range(N_BATCH_OBJECTS)]
+        units = shard.units_of(problems)
+        owner = shard.assign(units, world)
+        mine = [i for i in range(len(units)) if owner[i] == rank]
+        subs = [CProblem(shard.subproblem(problems[units[i].obj], units[i])) for i in mine]
+        k_max = problems[0].k_max
+        pits_total = sum(u.count for u in units) * k_max
+        streams = [torch.cuda.Stream() for _ in subs]
+        runner = BatchSolver(subs, device=local, streams=[s.cuda_stream for s in streams])
+        fx = fixtures.config(4, seed=0)  # config description / CPU sample (object 0)
+
+        def solve_resident():
+            runner.launch()
+
+        def finish():
+            sols = runner.wait()
+            parts = all_gather([(i, np.asarray(s.particle_theta), np.asarray(s.particle_loss),
+                                 np.asarray(s.particle_collision_free), np.asarray(s.particle_converged))
+                                for i, s in zip(mine, sols)])
+            return shard.combine(problems, parts)
+
+        def solve_e2e():
+            for s, cp in zip(runner.solvers, subs):
+                s.prepare(cp)  # asicp_prepare: H2D of the unit's host buffers
+            runner.launch()
+            return finish()
+
+        worker_streams = streams
+        h2d = sum(problem_bytes(cp) for cp in subs)
+        d2h = sum(solution_bytes(cp.J) for cp in subs)
+        launches_of = runner.launches
+    else:
+        cfg = WORKLOADS[args.workload][0]
+        fx = fixtures.config(cfg, seed=rank)  # object instance per rank (object sharding)
+        pits_total = world * fx.J * fx.k_max
+        solver = Solver(device=local, stream=main_stream.cuda_stream)
+        solver.prepare(fx)
+        holder = {}
+
+        def solve_resident():
+            holder["sol"] = solver.run()
+
+        def finish():
+            return holder["sol"]
+
+        def solve_e2e():
+            return solver.optimize(fx)  # asicp_optimize_grasp: H2D + solve + D2H
+
+        worker_streams = []
+        h2d = problem_bytes(fx)
+        d2h = solution_bytes(fx.J)
+        launches_of = lambda: solver.stats().kernel_launches  # noqa: E731
+
     # ---- device-resident timing (value): inputs already in HBM ----
     for _ in range(args.warmup):
-        sol = solver.run()
+        solve_resident()
+        result = finish()
     barrier()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    timers = [Timer(torch, main_stream, worker_streams) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
-            ev[k][0].record(stream)
-            sol = solver.run()
-            ev[k][1].record(stream)
+            timers[k].start()
+            solve_resident()
+            timers[k].stop()
+            if batch:
+                result = finish()
         barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    ms = float(np.mean(step_ms))
-    ms_t = torch.tensor([ms], device="cuda")
-    if dist is not None:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * pits / (ms_max * 1e-3)
-    launches = solver.stats().kernel_launches
+    if not batch:
+        result = finish()
+    ms_max = all_max(float(np.mean([t.ms() for t in timers])))
+    value = pits_total / (ms_max * 1e-3)
+    launches = launches_of()
 
     # ---- end-to-end through the public API with host buffers ----
-    h2d = problem_bytes(fx)
-    d2h = fx.J * (7 * 8 + 8 + 4 + 4) + 64
     e2e_ms = []
     for k in range(max(1, args.steps)):
         barrier()
         flush.fill_(k & 0xFF)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        sol = solver.optimize(fx)  # asicp_optimize_grasp: H2D + solve + D2H
+        result = solve_e2e()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    e2e = float(np.mean(e2e_ms))
-    e_t = torch.tensor([e2e], device="cuda")
-    if dist is not None:
-        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * pits / (float(e_t.item()) * 1e-3)
+    e2e_max = all_max(float(np.mean(e2e_ms)))
+    e2e_value = pits_total / (e2e_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (NN filter), profiled run ----
-    prof = Solver(device=local, stream=stream.cuda_stream, profile=True)
-    prof.prepare(fx)
+    # ---- roofline of the dominant kernel (NN filter), profiled run on one problem ----
+    prof = Solver(device=local, stream=main_stream.cuda_stream, profile=True)
+    prof.prepare(subs[0] if batch else fx)
     prof.run()
     st = prof.stats()
     prof.close()
@@ -250,22 +372,26 @@ def main():
     peak = float(lib.asicp_dbg_ffma_tflops(20000))
     traffic = None
     tfile = ROOT / "profiles" / "nn_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and args.workload == "cfg2":
         try:
             traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
     if rank == 0:
+        best = result[0] if batch else result
+        status = int(best["status"]) if batch else int(best.status)
+        final_loss = best["final_loss"] if batch else best.final_loss
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong" if batch else "weak",
             "vs_baseline": None, "dtype": "f64 (FP32-certified NN filter)", "data": "synthetic",
-            "config": config_dict(fx, world),
+            "config": config_dict(args.workload, fx, world),
             "solve_latency_ms": ms_max,
             "paper_latency_ms": PAPER_LATENCY_S * 1e3,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "latency_ms": float(e_t.item())},
+                    "latency_ms": e2e_max},
             "gpu_launches": int(launches) * args.steps,
             "clocks": clk.summary(),
             "roofline": {"bound": "fp32", "kernel": "nn_filter_kernel",
@@ -275,28 +401,41 @@ def main():
                          "traffic": traffic, "nn_ms_per_launch": nn_ms_per_launch,
                          "nn_launches": int(st.nn_launches), "nn_share_of_step": st.nn_ms / st.solve_ms,
                          "algorithmic": "8 FLOP x (query, candidate) pairs; pairs counted by the kernel"},
-            "status": int(sol.status), "final_loss": sol.final_loss,
-            "nn": sol.diagnostics,
+            "status": status, "final_loss": final_loss,
         }
+        if batch:
+            line["objects_found"] = int(sum(int(r["status"]) == 0 for r in result))
+        else:
+            line["nn"] = result.diagnostics
         if world == 1 and not args.no_cpu_baseline:
             try:
                 from oracle import ref
 
                 if ref.available():
                     threads = os.cpu_count() or 1
-                    dt, rs = cpu_reference(fx, threads)
+                    sfx = sample_fixture(args.workload)
+                    spits = sfx.J * sfx.k_max
+                    dt, rs = cpu_reference(sfx, threads)
+                    if batch:
+                        same = bool(rs.final_loss == result[0]["final_loss"]
+                                    and np.array_equal(rs.theta, result[0]["theta"]))
+                    else:
+                        same = bool(np.array_equal(rs.particle_theta, result.particle_theta)
+                                    and rs.final_loss == result.final_loss)
                     line["cpu_baseline"] = {
-                        "value": pits / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                        "sample": f"one full cfg2 solve ({pits} particle-iterations), oracle/_ref "
-                                  f"graspmatch::optimize_grasp workers={threads}",
+                        "value": spits / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+                        "sample": f"one full {args.workload} solve of object 0 ({spits} particle-iterations), "
+                                  f"oracle/_ref graspmatch::optimize_grasp workers={threads}",
                         "latency_ms": dt * 1e3,
-                        "bit_identical": bool(np.array_equal(rs.particle_theta, sol.particle_theta)
-                                              and rs.final_loss == sol.final_loss),
+                        "bit_identical": same,
                     }
             except Exception as e:  # the baseline is reported, never required
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)
-    solver.close()
+    if batch:
+        runner.close()
+    else:
+        solver.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

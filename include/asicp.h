@@ -174,6 +174,13 @@ int asicp_prepare(asicp_ctx* ctx, const asicp_problem* problem, char* err, size_
  * solution (synchronous with respect to the host). */
 int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen);
 
+/* asicp_run split in two: enqueue the solve on the ctx stream and return
+ * (per-particle summaries land in pinned staging), then wait and fill the
+ * solution.  Contexts on different streams overlap on one GPU (batched
+ * objects / preshape units).  One solve in flight per ctx. */
+int asicp_run_async(asicp_ctx* ctx, char* err, size_t errlen);
+int asicp_wait(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen);
+
 /* prepare + run: the drop-in for graspmatch::optimize_grasp. */
 int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution,
                          char* err, size_t errlen);

@@ -112,6 +112,125 @@ Cloud box_surface_cloud(int n, const P3& half, uint64_t seed) {
   return cloud;
 }
 
+// synthetic.cpp:53-67
+Cloud sphere_cloud(int n, double radius, uint64_t seed) {
+  Rng rng(seed);
+  Cloud cloud;
+  for (int i = 0; i < n; ++i) {
+    const P3 v{rng.normal(), rng.normal(), rng.normal()};
+    const double norm = std::sqrt(sqn(v));
+    if (norm < 1e-12) {
+      --i;
+      continue;
+    }
+    cloud.push_back(P3{radius * v.x / norm, radius * v.y / norm, radius * v.z / norm});
+  }
+  return cloud;
+}
+
+// synthetic.cpp:69-83
+Cloud blob_cloud(int n, double radius, uint64_t seed) {
+  Rng rng(seed);
+  Cloud cloud;
+  for (int i = 0; i < n; ++i) {
+    const P3 v{rng.normal(), rng.normal(), rng.normal()};
+    const double norm = std::sqrt(sqn(v));
+    if (norm < 1e-12) {
+      --i;
+      continue;
+    }
+    const double s = rng.uniform(0.3, 1.0);
+    cloud.push_back(P3{v.x / norm * radius * s, v.y / norm * radius * s, v.z / norm * radius * s});
+  }
+  return cloud;
+}
+
+Cloud shifted(Cloud c, double dx, double dy, double dz) {
+  for (P3& p : c) p = P3{p.x + dx, p.y + dy, p.z + dz};
+  return c;
+}
+
+// cfg3: a noisy single-view partial scan of a cylinder +
+// box union.  Outward normals are known per sample; the view keeps the
+// camera-facing points, a seeded slab removes 40 % of them along a random
+// direction, every coordinate gets N(0, sigma) noise (Rng::normal), and the
+// result is trimmed to exactly n points.
+Cloud partial_view(int n, double sigma, uint64_t seed) {
+  Rng rng(seed * 7919 + 17);
+  const double R = 0.04, H = 0.15;
+  const P3 half{0.06, 0.045, 0.025}, box_c{0.07, 0.0, 0.025};
+  std::vector<P3> pts, nrm;
+  const int n_cyl = 2 * n, n_box = 2 * n;
+  for (int i = 0; i < n_cyl; ++i) {  // lateral surface + caps, area-weighted
+    const double a_side = 2.0 * M_PI * R * H, a_cap = M_PI * R * R;
+    const double u = rng.uniform01() * (a_side + 2.0 * a_cap);
+    const double th = rng.uniform(0.0, 2.0 * M_PI);
+    if (u < a_side) {
+      pts.push_back(P3{R * std::cos(th), R * std::sin(th), rng.uniform(0.0, H)});
+      nrm.push_back(P3{std::cos(th), std::sin(th), 0.0});
+    } else {
+      const double rr = R * std::sqrt(rng.uniform01());
+      const bool top = u < a_side + a_cap;
+      pts.push_back(P3{rr * std::cos(th), rr * std::sin(th), top ? H : 0.0});
+      nrm.push_back(P3{0.0, 0.0, top ? 1.0 : -1.0});
+    }
+  }
+  const double areas[3] = {half.y * half.z, half.x * half.z, half.x * half.y};
+  for (int i = 0; i < n_box; ++i) {
+    const double u = rng.uniform01() * (areas[0] + areas[1] + areas[2]);
+    const int axis = u < areas[0] ? 0 : (u < areas[0] + areas[1] ? 1 : 2);
+    const double sign = rng.uniform01() < 0.5 ? -1.0 : 1.0;
+    P3 p, q{0.0, 0.0, 0.0};
+    for (int a = 0; a < 3; ++a) p[a] = rng.uniform(-half[a], half[a]);
+    p[axis] = sign * half[axis];
+    q[axis] = sign;
+    pts.push_back(P3{p.x + box_c.x, p.y + box_c.y, p.z + box_c.z});
+    nrm.push_back(q);
+  }
+  // Camera-facing half.
+  const P3 cam{0.6, -0.45, 0.66};
+  std::vector<P3> front;
+  for (size_t i = 0; i < pts.size(); ++i)
+    if (nrm[i].x * cam.x + nrm[i].y * cam.y + nrm[i].z * cam.z > 0.0) front.push_back(pts[i]);
+  // Occlusion slab: drop the 40 % of points whose projection on a random
+  // direction falls in a random band of the sorted projections.
+  const P3 dir{rng.normal(), rng.normal(), rng.normal()};
+  std::vector<std::pair<double, size_t>> proj(front.size());
+  for (size_t i = 0; i < front.size(); ++i)
+    proj[i] = {front[i].x * dir.x + front[i].y * dir.y + front[i].z * dir.z, i};
+  std::sort(proj.begin(), proj.end());
+  const size_t drop = static_cast<size_t>(0.4 * static_cast<double>(front.size()));
+  const size_t start = static_cast<size_t>(rng.uniform01() * static_cast<double>(front.size() - drop));
+  std::vector<char> keep(front.size(), 1);
+  for (size_t r = start; r < start + drop; ++r) keep[proj[r].second] = 0;
+  Cloud out;
+  for (size_t i = 0; i < front.size() && static_cast<int>(out.size()) < n; ++i) {
+    if (!keep[i]) continue;
+    const P3& p = front[i];
+    out.push_back(P3{p.x + sigma * rng.normal(), p.y + sigma * rng.normal(), p.z + sigma * rng.normal()});
+  }
+  return out;
+}
+
+// cfg4: 11 objects from the reference's generators, each
+// standing on the table plane.
+Cloud batch_object(int which, int n) {
+  const uint64_t s = static_cast<uint64_t>(which) + 1;
+  switch (which % 11) {
+    case 0: return cylinder_cloud(0.03, 0.12, n, s);
+    case 1: return cylinder_cloud(0.04, 0.15, n, s);
+    case 2: return cylinder_cloud(0.025, 0.10, n, s);
+    case 3: return shifted(box_surface_cloud(n, P3{0.03, 0.03, 0.06}, s), 0.0, 0.0, 0.06);
+    case 4: return shifted(box_surface_cloud(n, P3{0.05, 0.02, 0.04}, s), 0.0, 0.0, 0.04);
+    case 5: return shifted(box_surface_cloud(n, P3{0.02, 0.02, 0.08}, s), 0.0, 0.0, 0.08);
+    case 6: return shifted(sphere_cloud(n, 0.04, s), 0.0, 0.0, 0.04);
+    case 7: return shifted(sphere_cloud(n, 0.05, s), 0.0, 0.0, 0.05);
+    case 8: return shifted(blob_cloud(n, 0.05, s), 0.0, 0.0, 0.05);
+    case 9: return shifted(blob_cloud(n, 0.06, s), 0.0, 0.0, 0.06);
+    default: return cylinder_cloud(0.035, 0.08, n, s);
+  }
+}
+
 // synthetic.cpp:85-91
 Cloud table_cloud(double half_extent = 0.12, double pitch = 0.01, double cutout_radius = 0.035) {
   Cloud cloud;
@@ -709,6 +828,25 @@ asicp_fixture* asicp_fx_config(int cfg, uint64_t seed, int64_t ppp, int64_t n_ob
     // populations to |t| ~ 1e22 m by k = 37 (bit-identically in the reference).
     // 0.25 keeps every population bounded (tools/stability.py).
     s.step_scale = 0.25;
+  } else if (cfg == 3 || cfg == 4) {
+    // cfg3: noisy 40 %-occluded single-view scan (20k points); cfg4: object
+    // `seed % 11` of the 11-object batch (10k points).  Both: 3 KG3 preshapes
+    // x 1024 particles (1018 Fibonacci + 6 top-down), 40 iterations (15 Stein),
+    // 5 mm gripper fields; the Stein step scales as 64 / K for stability.
+    const int n = static_cast<int>(n_object > 0 ? n_object : (cfg == 3 ? 20000 : 10000));
+    s.object = cfg == 3 ? partial_view(n, 0.0015, seed) : batch_object(static_cast<int>(seed % 11), n);
+    s.com = centroid(s.object);
+    s.scene = with_table(s.object);
+    const double gaps[3] = {0.09, 0.10, 0.11};
+    const size_t count = ppp > 0 ? static_cast<size_t>(ppp) : 1024;
+    for (double gap : gaps) {
+      s.grippers.push_back(kg3(gap));
+      s.voxels.push_back(0.005);
+      s.inits.push_back(fib_inits(count, 6, 0.25, s.com));
+    }
+    s.k_stein = 15;
+    s.k_max = 40;
+    s.step_scale = std::min(1.0, 64.0 / static_cast<double>(count));
   } else {
     return nullptr;
   }

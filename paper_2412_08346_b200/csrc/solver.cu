@@ -148,7 +148,42 @@ struct asicp_ctx {
   int64_t launches = 0;
   unsigned long long raw_stats[kStats] = {};
 
+  // Pinned host staging for the per-particle summaries, so a launched solve
+  // returns control to the host (asicp_run_async) and several contexts on
+  // different streams overlap on one GPU.
+  struct Staging {
+    double* theta = nullptr;
+    double* floss = nullptr;
+    int* ffree = nullptr;
+    int* conv = nullptr;
+    unsigned long long* stats = nullptr;
+    int* refine_total = nullptr;
+    int cap = 0;
+  } host;
+  bool in_flight = false;
+
+  void ensure_staging(int J) {
+    if (J <= host.cap) return;
+    free_staging();
+    const size_t j = static_cast<size_t>(J);
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.theta), 7 * j * 8));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.floss), j * 8));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.ffree), j * 4));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.conv), j * 4));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.stats), kStats * 8));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host.refine_total), 4));
+    host.cap = J;
+  }
+  void free_staging() {
+    void* all[] = {host.theta, host.floss, host.ffree, host.conv, host.stats, host.refine_total};
+    for (void* p : all)
+      if (p) cudaFreeHost(p);
+    host = Staging{};
+  }
+
   ~asicp_ctx() {
+    if (in_flight && stream) cudaStreamSynchronize(stream);
+    free_staging();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto& e : nn_events) {
       cudaEventDestroy(e.first);
@@ -681,8 +716,11 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
   CUDA_OK(cudaGetLastError());
 }
 
-void run(asicp_ctx* c, asicp_solution* out) {
+// Enqueue one solve (graph replay) plus the D2H of the particle summaries
+// into pinned staging; returns without waiting.
+void launch(asicp_ctx* c) {
   if (!c->prepared) throw InvalidArgument("asicp_run: no prepared problem");
+  if (c->in_flight) throw InvalidArgument("asicp_run_async: a solve is already in flight (call asicp_wait)");
   CUDA_OK(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   for (auto& e : c->nn_events) {
@@ -713,17 +751,29 @@ void run(asicp_ctx* c, asicp_solution* out) {
   }
   CUDA_OK(cudaEventRecord(c->ev1, st));
 
+  const size_t J = static_cast<size_t>(c->J);
+  c->ensure_staging(c->J);
+  CUDA_OK(cudaMemcpyAsync(c->host.theta, c->S.theta, 7 * J * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(c->host.floss, c->S.final_loss, J * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(c->host.ffree, c->S.final_free, J * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(c->host.conv, c->S.converged, J * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(c->host.stats, c->S.stats, kStats * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaMemcpyAsync(c->host.refine_total, c->S.refine_count, 4, cudaMemcpyDeviceToHost, st));
+  c->in_flight = true;
+}
+
+// Wait for the launched solve and fill `out` (traces are copied here).
+void finish(asicp_ctx* c, asicp_solution* out) {
+  if (!c->in_flight) throw InvalidArgument("asicp_wait: no solve in flight");
+  cudaStream_t st = c->stream;
+  c->in_flight = false;
+  CUDA_OK(cudaStreamSynchronize(st));
   const int J = c->J;
-  std::vector<double> theta(7 * static_cast<size_t>(J)), floss(J);
-  std::vector<int> ffree(J), conv(J);
-  unsigned long long stats[kStats];
-  CUDA_OK(cudaMemcpyAsync(theta.data(), c->S.theta, theta.size() * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(floss.data(), c->S.final_loss, floss.size() * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(ffree.data(), c->S.final_free, ffree.size() * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(conv.data(), c->S.converged, conv.size() * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(stats, c->S.stats, sizeof(stats), cudaMemcpyDeviceToHost, st));
-  int refine_total = 0;
-  CUDA_OK(cudaMemcpyAsync(&refine_total, c->S.refine_count, 4, cudaMemcpyDeviceToHost, st));
+  const double* theta = c->host.theta;
+  const double* floss = c->host.floss;
+  const int* ffree = c->host.ffree;
+  const int* conv = c->host.conv;
+  const unsigned long long* stats = c->host.stats;
   const size_t rows = static_cast<size_t>(c->k_max) * J;
   if (c->record_trace && rows) {
     if (out->trace_theta)
@@ -732,9 +782,9 @@ void run(asicp_ctx* c, asicp_solution* out) {
       CUDA_OK(cudaMemcpyAsync(out->trace_loss, c->S.trace_loss, rows * 8, cudaMemcpyDeviceToHost, st));
     if (out->trace_in_collision)
       CUDA_OK(cudaMemcpyAsync(out->trace_in_collision, c->S.trace_col, rows * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
   }
-  CUDA_OK(cudaStreamSynchronize(st));
-  if (refine_total > c->S.refine_cap) throw DeviceError("asicp: FP64 refine list overflow");
+  if (*c->host.refine_total > c->S.refine_cap) throw DeviceError("asicp: FP64 refine list overflow");
 
   float ms = 0.0f;
   CUDA_OK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
@@ -780,7 +830,7 @@ void run(asicp_ctx* c, asicp_solution* out) {
   out->nn_full_refines = static_cast<int64_t>(stats[1]);
   out->nn_queries = static_cast<int64_t>(stats[2]);
   out->nn_pool_ties = static_cast<int64_t>(stats[3]);
-  std::memcpy(c->raw_stats, stats, sizeof(stats));
+  std::memcpy(c->raw_stats, stats, sizeof(c->raw_stats));
   out->nn_pairs = static_cast<double>(stats[4]);
   s.nn_pairs = static_cast<double>(stats[12]);  // pairs of the event-timed (forward/final) filter launches
 }
@@ -860,12 +910,28 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
 
 int asicp_prepare(asicp_ctx* ctx, const asicp_problem* problem, char* err, size_t errlen) {
   if (!ctx || !problem) return ASICP_INVALID_ARGUMENT;
-  return guarded(err, errlen, [&] { prepare(ctx, *problem); });
+  return guarded(err, errlen, [&] {
+    if (ctx->in_flight) throw InvalidArgument("asicp_prepare: a solve is in flight (call asicp_wait)");
+    prepare(ctx, *problem);
+  });
 }
 
 int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen) {
   if (!ctx || !solution) return ASICP_INVALID_ARGUMENT;
-  return guarded(err, errlen, [&] { run(ctx, solution); });
+  return guarded(err, errlen, [&] {
+    launch(ctx);
+    finish(ctx, solution);
+  });
+}
+
+int asicp_run_async(asicp_ctx* ctx, char* err, size_t errlen) {
+  if (!ctx) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] { launch(ctx); });
+}
+
+int asicp_wait(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen) {
+  if (!ctx || !solution) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] { finish(ctx, solution); });
 }
 
 int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution, char* err,

@@ -400,6 +400,17 @@ class Solver:
         _check(self.lib.asicp_run(self.ctx, C.byref(self._bufs.struct), err, 512), err)
         return self._bufs.solution(self._cp.k_stein)
 
+    def run_async(self) -> None:
+        """Enqueue the prepared solve on this context's stream and return
+        (asicp_run_async); collect it with `wait`."""
+        err = C.create_string_buffer(512)
+        _check(self.lib.asicp_run_async(self.ctx, err, 512), err)
+
+    def wait(self) -> GraspSolution:
+        err = C.create_string_buffer(512)
+        _check(self.lib.asicp_wait(self.ctx, C.byref(self._bufs.struct), err, 512), err)
+        return self._bufs.solution(self._cp.k_stein)
+
     def optimize(self, problem: GraspProblem | CProblem) -> GraspSolution:
         self.prepare(problem)
         return self.run()

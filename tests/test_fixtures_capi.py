@@ -119,3 +119,20 @@ def test_kg3_fixture_shape():
     assert v2.n_preshapes == 3 and fx2.J == 12 and fx2.k_max == 100 and fx2.k_stein == 38
     for i in range(3):
         assert max(v2.sdf_grids[i].dims[:]) == 64
+
+
+def test_partial_view_and_batch_fixtures():
+    """cfg3 (noisy 40 %-occluded single view, 20k points) and cfg4 (the
+    11-object batch) fixture shapes; deterministic per seed."""
+    a = fixtures.config(3, seed=0, particles_per_preshape=4).problem()
+    b = fixtures.config(3, seed=0, particles_per_preshape=4).problem()
+    assert a.object_cloud.shape == (20000, 3)
+    assert np.array_equal(a.object_cloud, b.object_cloud)
+    assert len(a.preshapes) == 3 and a.k_max == 40 and a.k_stein == 15
+    assert not np.array_equal(a.object_cloud, fixtures.config(3, seed=1, particles_per_preshape=4).problem().object_cloud)
+    clouds = [fixtures.config(4, seed=o, particles_per_preshape=4).problem().object_cloud for o in range(11)]
+    for c in clouds:
+        assert c.shape == (10000, 3) and c[:, 2].min() >= -1e-12  # standing on the table plane
+    assert len({c.tobytes() for c in clouds}) == 11
+    full = fixtures.config(4, seed=0)
+    assert full.J == 3 * 1024 and full.problem().stein.step_scale == 64.0 / 1024

@@ -202,3 +202,21 @@ def test_cfg2_reduced_matches_port(solver, seed):
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)
+
+
+@pytest.mark.parametrize("cfg,seed,ppp,k_max", [(3, 0, 8, 12), (3, 2, 6, 24), (4, 3, 8, 12), (4, 6, 16, 40),
+                                                 (4, 8, 8, 12)])
+def test_partial_view_and_batch_objects_match_port(solver, cfg, seed, ppp, k_max):
+    """cfg3 (noisy occluded scan) and cfg4 batch objects (box / sphere / blob)
+    at reduced particle counts, full trace against the C restatement."""
+    from oracle import ref
+
+    if not ref.port_available():
+        pytest.skip("oracle port not built")
+    fx = fixtures.config(cfg, seed=seed, particles_per_preshape=ppp)
+    fx.set(k_max=k_max, k_stein=min(15, k_max // 2), anneal_period_total=k_max, record_trace=1)
+    want = ref.port_optimize_grasp(fx)
+    got = solver.optimize(fx)
+    np.testing.assert_array_equal(got.trace_in_collision, want.trace_in_collision)
+    assert np.array_equal(got.trace_theta, want.trace_theta)
+    assert_same_solution(got, want)
