@@ -181,6 +181,28 @@ int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen
 int asicp_run_async(asicp_ctx* ctx, char* err, size_t errlen);
 int asicp_wait(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen);
 
+/* Particle sharding within a population (no reference
+ * counterpart — the reference runs one process).  Every rank prepares the SAME
+ * full problem; rank r owns global particles [r J / R, (r + 1) J / R) and,
+ * each Stein iteration, all-gathers the population's poses and drifts (the
+ * median bandwidth and the Stein sums then read the whole population in the
+ * reference order).  After the final ranking the particle summaries are
+ * gathered, so every rank's asicp_solution is the full, unsharded answer.
+ *
+ * NCCL backend (one process per GPU): rank 0 makes the 128-byte id, the
+ * caller broadcasts it, then every rank calls asicp_set_partition_nccl
+ * (collective).  Group backend: contexts of one process, one host thread per
+ * rank, exchanging through host memory.  Setting or clearing a partition
+ * drops the prepared problem. */
+typedef struct asicp_group asicp_group;
+int asicp_nccl_unique_id(unsigned char* id /* 128 bytes */, char* err, size_t errlen);
+int asicp_set_partition_nccl(asicp_ctx* ctx, int rank, int world, const unsigned char* id, char* err,
+                             size_t errlen);
+asicp_group* asicp_group_create(int world);
+void asicp_group_destroy(asicp_group* group);
+int asicp_set_partition_group(asicp_ctx* ctx, asicp_group* group, int rank, char* err, size_t errlen);
+int asicp_clear_partition(asicp_ctx* ctx);
+
 /* prepare + run: the drop-in for graspmatch::optimize_grasp. */
 int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution,
                          char* err, size_t errlen);

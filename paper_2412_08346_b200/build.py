@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # built without FMA); the FP32 NN filter requests its FMAs explicitly.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3",
               "-diag-suppress", "177", f"-I{ROOT / 'include'}"]
-SOURCES = ["kernels.cu", "nn.cu", "minibatch.cu", "solver.cu", "fixtures.cu"]
+SOURCES = ["kernels.cu", "nn.cu", "minibatch.cu", "exchange.cu", "solver.cu", "fixtures.cu"]
 
 
 def _nvcc() -> str:
@@ -57,7 +57,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -847,6 +847,21 @@ asicp_fixture* asicp_fx_config(int cfg, uint64_t seed, int64_t ppp, int64_t n_ob
     s.k_stein = 15;
     s.k_max = 40;
     s.step_scale = std::min(1.0, 64.0 / static_cast<double>(count));
+  } else if (cfg == 5) {
+    // cfg5 scaling sweep: ONE KG3 preshape with 16384 particles (one Stein
+    // population, sharded over GPUs by particle) against a synthetic cylinder
+    // of n_object points (10k .. 200k), 40 iterations (15 Stein).
+    const int n = static_cast<int>(n_object > 0 ? n_object : 10000);
+    s.object = cylinder_cloud(0.04, 0.15, n, seed + 1);
+    s.com = centroid(s.object);
+    s.scene = with_table(s.object);
+    const size_t count = ppp > 0 ? static_cast<size_t>(ppp) : 16384;
+    s.grippers.push_back(kg3(0.10));
+    s.voxels.push_back(0.005);
+    s.inits.push_back(fib_inits(count, 6, 0.25, s.com));
+    s.k_stein = 15;
+    s.k_max = 40;
+    s.step_scale = std::min(1.0, 64.0 / static_cast<double>(count));
   } else {
     return nullptr;
   }

@@ -473,7 +473,8 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
 // (nth_element at M/2, optim.cpp:141-142: an exact order statistic).
 __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) {
   const int pop = blockIdx.x;
-  const int b = P.pop_off[pop], K = P.pop_off[pop + 1] - b;
+  if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // no local particle reads h
+  const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
   if (K < 1) return;
   if (P.bandwidth_mode == 1) {
     if (threadIdx.x == 0) S.h[pop] = P.fixed_bandwidth;
@@ -518,7 +519,7 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
           ++i;
         }
         const int jj = i + 1 + static_cast<int>(p - row_start);
-        const double d2 = sqnorm(sub(pose_t(th_of(S.theta, b + i)), pose_t(th_of(S.theta, b + jj))));
+        const double d2 = sqnorm(sub(pose_t(th_of(S.theta_all, b + i)), pose_t(th_of(S.theta_all, b + jj))));
         const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
         if (keys != nullptr) keys[p] = key;
         if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
@@ -553,9 +554,11 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
 constexpr int kSvgdJ = 32;
 __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState S, double eta) {
   const int pop = blockIdx.y;
-  const int b = P.pop_off[pop], K = P.pop_off[pop + 1] - b;
+  const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;  // own (local) rows
+  const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;   // partners (global)
   const int j0 = blockIdx.x * kSvgdJ;
-  if (j0 >= K) return;
+  if (j0 >= Kl) return;
+  const int own0 = P.j_lo + lb - b;  // position of local row lb within the population
   __shared__ double kv[kSvgdJ][kSvgdJ + 1];   // rbf value [i][j]
   __shared__ double kq[kSvgdJ][kSvgdJ + 1];   // |q_i . q_j|
   __shared__ double ti[kSvgdJ][7];            // partner poses
@@ -564,8 +567,8 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
   __shared__ double dir[kSvgdJ][7];
   const int tid = threadIdx.x;
   const int jl = tid / 7, comp = tid % 7;
-  const int nj = min(kSvgdJ, K - j0);
-  for (int e = tid; e < nj * 7; e += blockDim.x) tj[e / 7][e % 7] = S.theta[7 * (b + j0 + e / 7) + e % 7];
+  const int nj = min(kSvgdJ, Kl - j0);
+  for (int e = tid; e < nj * 7; e += blockDim.x) tj[e / 7][e % 7] = S.theta[7 * (lb + j0 + e / 7) + e % 7];
   const double h = S.h[pop];
   const double two_h = 2.0 / h;
   double acc = 0.0;
@@ -573,8 +576,8 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
     const int ni = min(kSvgdJ, K - i0);
     __syncthreads();
     for (int e = tid; e < ni * 7; e += blockDim.x) {
-      ti[e / 7][e % 7] = S.theta[7 * (b + i0 + e / 7) + e % 7];
-      di[e / 7][e % 7] = S.drift[7 * (b + i0 + e / 7) + e % 7];
+      ti[e / 7][e % 7] = S.theta_all[7 * (b + i0 + e / 7) + e % 7];
+      di[e / 7][e % 7] = S.drift_all[7 * (b + i0 + e / 7) + e % 7];
     }
     __syncthreads();
     for (int e = tid; e < ni * nj; e += blockDim.x) {
@@ -588,7 +591,7 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
     }
     __syncthreads();
     if (jl < nj) {
-      const int jg = j0 + jl;
+      const int jg = own0 + j0 + jl;
       for (int ii = 0; ii < ni; ++ii) {
         const double d = di[ii][comp];
         if (i0 + ii == jg) {
@@ -606,8 +609,7 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
   if (jl < nj) dir[jl][comp] = acc;
   __syncthreads();
   if (tid < nj) {
-    const int jg = b + j0 + tid;
-    double* out = S.theta_next + 7 * jg;
+    double* out = S.theta_next + 7 * (lb + j0 + tid);
     for (int a = 0; a < 3; ++a) out[a] = tj[tid][a] + eta * dir[tid][a];
     const Q4 qn = normalized(Q4{tj[tid][3] + eta * dir[tid][3], tj[tid][4] + eta * dir[tid][4],
                                 tj[tid][5] + eta * dir[tid][5], tj[tid][6] + eta * dir[tid][6]});
@@ -660,6 +662,54 @@ __global__ void bookkeeping_kernel(DevProblem P, DevState S, int stein_phase, in
     S.prev_loss[j] = S.loss[j];
   }
   S.active[j] = (next_stein || !S.converged[j]) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Particle-sharding exchange: every Stein iteration each
+// rank contributes its rows' [theta, drift]; the gathered block is scattered
+// into global order so median/svgd read the whole population exactly as the
+// unsharded solve does.
+// ---------------------------------------------------------------------------
+__global__ void pack_stein_kernel(DevProblem P, DevState S, double* send) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.J) return;
+  for (int a = 0; a < 7; ++a) {
+    send[14 * j + a] = S.theta[7 * j + a];
+    send[14 * j + 7 + a] = S.drift[7 * j + a];
+  }
+}
+
+__global__ void unpack_stein_kernel(const double* gathered, double* theta_all, double* drift_all, int J_glob,
+                                    int world, int rows_per_rank) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= world * rows_per_rank) return;
+  const int r = row / rows_per_rank, i = row % rows_per_rank;
+  const int lo = static_cast<int>(static_cast<int64_t>(r) * J_glob / world);
+  const int hi = static_cast<int>(static_cast<int64_t>(r + 1) * J_glob / world);
+  if (i >= hi - lo) return;
+  const double* src = gathered + 14 * static_cast<int64_t>(row);
+  for (int a = 0; a < 7; ++a) {
+    theta_all[7 * (lo + i) + a] = src[a];
+    drift_all[7 * (lo + i) + a] = src[7 + a];
+  }
+}
+
+__global__ void pack_final_kernel(DevProblem P, DevState S, double* send, int stride, int k_max, int with_trace) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.J) return;
+  double* o = send + static_cast<int64_t>(stride) * j;
+  for (int a = 0; a < 7; ++a) o[a] = S.theta[7 * j + a];
+  o[7] = S.final_loss[j];
+  o[8] = S.final_free[j];
+  o[9] = S.converged[j];
+  if (!with_trace) return;
+  for (int k = 0; k < k_max; ++k) {
+    const int64_t r = static_cast<int64_t>(k) * P.J + j;
+    double* t = o + 10 + 9 * k;
+    for (int a = 0; a < 7; ++a) t[a] = S.trace_theta[7 * r + a];
+    t[7] = S.trace_loss[r];
+    t[8] = S.trace_col[r];
+  }
 }
 
 __global__ void copy_theta_kernel(double* dst, const double* src, int n) {
@@ -768,9 +818,23 @@ void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t 
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {
   trace_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, k);
 }
-void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, int max_pop,
-                 cudaStream_t st) {
+void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st) {
   drift_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, gamma, n_ref);
+}
+void launch_pack_stein(const DevProblem& P, const DevState& S, double* send, cudaStream_t st) {
+  pack_stein_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send);
+}
+void launch_unpack_stein(const double* gathered, double* theta_all, double* drift_all, int J_glob, int world,
+                         int rows_per_rank, cudaStream_t st) {
+  const int rows = world * rows_per_rank;
+  unpack_stein_kernel<<<(rows + 127) / 128, 128, 0, st>>>(gathered, theta_all, drift_all, J_glob, world,
+                                                          rows_per_rank);
+}
+void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int stride, int k_max, int with_trace,
+                       cudaStream_t st) {
+  pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
+}
+void launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, cudaStream_t st) {
   median_kernel<<<P.n_pop, 1024, 0, st>>>(P, S);
   dim3 grid((max_pop + kSvgdJ - 1) / kSvgdJ, P.n_pop);
   svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);

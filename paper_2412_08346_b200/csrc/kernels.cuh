@@ -37,6 +37,12 @@ struct DevProblem {
   const int* pop_off;       // population -> first particle (n_pop + 1)
   const double* pop_logk1;  // log(K + 1) per population (host std::log)
   const long long* med_off; // population -> offset of its median keys in DevState::med_keys (-1: none)
+  // Particle sharding: this context owns global particles
+  // [j_lo, j_lo + J); populations span gpop_off in the global order, whose
+  // poses and drifts the exchange gathers into DevState::theta_all/drift_all.
+  // Unsharded: j_lo = 0, gpop_off = pop_off, theta_all = theta.
+  const int* gpop_off;      // population -> first global particle (n_pop + 1)
+  int j_lo;
   double center[3];         // FP32 re-centring origin of the forward match (object centroid)
   double B_obj;             // max |r - center| over R (with slack)
   double com[3];
@@ -65,6 +71,8 @@ struct DevState {
   double* grad;        // J x 7 likelihood gradient
   double* prior;       // J x 7 prior log-gradient
   double* drift;       // J x 7
+  const double* theta_all;  // global J x 7 poses (SVGD partners / median)
+  const double* drift_all;  // global J x 7 drifts
   double* h;           // per population bandwidth
   unsigned long long* med_keys;  // cached squared-distance bit patterns for the median select
   double* S64;         // transformed contact surface, padded rows x 3
@@ -126,8 +134,18 @@ bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t 
 int minibatch_smem_cap();
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
-void launch_svgd(const DevProblem& P, DevState& S, double gamma, double n_ref, double eta, int max_pop,
-                 cudaStream_t st);
+void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st);
+void launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, cudaStream_t st);
+// Particle-sharding exchange helpers: pack local rows [theta(7), drift(7)]
+// into `send` (stride 14 doubles), and scatter a gathered world x rows_per_rank
+// block back into global order (rank r's rows start at floor(r * J_glob / world)).
+void launch_pack_stein(const DevProblem& P, const DevState& S, double* send, cudaStream_t st);
+void launch_unpack_stein(const double* gathered, double* theta_all, double* drift_all, int J_glob, int world,
+                         int rows_per_rank, cudaStream_t st);
+// Final-summary pack: [theta(7), final_loss, final_free, converged] + trace
+// (k_max x [theta(7), loss, in_collision]) per local row, stride `stride`.
+void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int stride, int k_max, int with_trace,
+                       cudaStream_t st);
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st);
 void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st);

@@ -10,6 +10,7 @@
 #include "asicp.h"
 #include "asicp_debug.h"
 #include "common.cuh"
+#include "exchange.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
 
@@ -20,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -124,6 +126,15 @@ struct asicp_ctx {
   uint64_t seed = 0;
   int nchunks_max = 1;
 
+  // Particle sharding within populations (asicp_set_partition_*): this ctx
+  // owns global particles [j_lo, j_lo + J) of J_glob; rows_per_rank pads the
+  // allgather blocks to equal size.  Unsharded: xchg null, J_glob = J.
+  std::unique_ptr<asicp::Exchange> xchg;
+  int J_glob = 0, j_lo = 0, rows_per_rank = 0, final_stride = 0;
+  Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d;
+  double* host_gath = nullptr;
+  size_t host_gath_bytes = 0;
+
   DevProblem P{};
   DevState S{};
 
@@ -181,9 +192,22 @@ struct asicp_ctx {
     host = Staging{};
   }
 
+  void ensure_gath(size_t bytes) {
+    if (bytes <= host_gath_bytes) return;
+    if (host_gath) cudaFreeHost(host_gath);
+    host_gath = nullptr;
+    host_gath_bytes = 0;
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&host_gath), bytes));
+    host_gath_bytes = bytes;
+  }
+
   ~asicp_ctx() {
     if (in_flight && stream) cudaStreamSynchronize(stream);
     free_staging();
+    if (host_gath) cudaFreeHost(host_gath);
+    xchg.reset();
+    Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend, &xrecv, &fsend, &frecv, &gpop_off_d};
+    for (Buf* b : shard_bufs) b->release();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto& e : nn_events) {
       cudaEventDestroy(e.first);
@@ -386,31 +410,55 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   for (const Grid& g : grids)
     c->max_coarse = std::max(c->max_coarse, g.cdims[0] * g.cdims[1] * g.cdims[2]);
 
-  // Particles (preshape-major flattening, grasp.cpp:135-145).
-  std::vector<int> part_pre, part_pop, pop_off(n_pre + 1, 0);
+  // Particles (preshape-major flattening, grasp.cpp:135-145).  Sharded, this
+  // ctx keeps the contiguous slice [lo, hi) = [r J / R, (r + 1) J / R) of the
+  // global order; each particle's RNG stream stays seeded by its GLOBAL index
+  // (seed + j, grasp.cpp:148-151) through the seed offset below.
+  std::vector<int> gpop_off(n_pre + 1, 0);
+  int64_t Jg = 0;
+  for (int i = 0; i < n_pre; ++i) {
+    gpop_off[i] = static_cast<int>(Jg);
+    Jg += p.init_counts[i];
+  }
+  gpop_off[n_pre] = static_cast<int>(Jg);
+  const int world = c->xchg ? c->xchg->world : 1, rank = c->xchg ? c->xchg->rank : 0;
+  const int lo = static_cast<int>(static_cast<int64_t>(rank) * Jg / world);
+  const int hi = static_cast<int>(static_cast<int64_t>(rank + 1) * Jg / world);
+  require(hi > lo, "asicp: particle partition leaves a rank without particles (fewer particles than ranks)");
+  std::vector<int> part_pre, part_pop, pop_off(n_pre + 1, 0), part_pre_glob;
   std::vector<int64_t> part_surf_off;
   std::vector<double> logk1(n_pre);
   int64_t so = 0;
   for (int i = 0; i < n_pre; ++i) {
     pop_off[i] = static_cast<int>(part_pre.size());
+    int local = 0;
     for (int64_t k = 0; k < p.init_counts[i]; ++k) {
+      const int64_t g = gpop_off[i] + k;
+      part_pre_glob.push_back(i);
+      if (g < lo || g >= hi) continue;
       part_pre.push_back(i);
       part_pop.push_back(i);
       part_surf_off.push_back(so);
       so += (p.preshapes[i].n_surface + kSubRows - 1) / kSubRows * kSubRows;  // rows padded to the subtile
+      ++local;
     }
-    logk1[i] = std::log(static_cast<double>(p.init_counts[i]) + 1.0);  // optim.cpp:143
-    c->max_pop = std::max(c->max_pop, static_cast<int>(p.init_counts[i]));
+    logk1[i] = std::log(static_cast<double>(p.init_counts[i]) + 1.0);  // optim.cpp:143 (global K)
+    c->max_pop = std::max(c->max_pop, local);
   }
   pop_off[n_pre] = static_cast<int>(part_pre.size());
   part_surf_off.push_back(so);
   const int J = static_cast<int>(part_pre.size());
   c->J = J;
+  c->J_glob = static_cast<int>(Jg);
+  c->j_lo = lo;
+  c->seed = p.seed + static_cast<uint64_t>(lo);
+  c->rows_per_rank = static_cast<int>((Jg + world - 1) / world);
   c->total_surf = so;
-  c->part_pre = part_pre;
+  c->part_pre = part_pre_glob;
   upload(c->part_pre_d, part_pre.data(), part_pre.size(), st);
   upload(c->part_pop, part_pop.data(), part_pop.size(), st);
   upload(c->pop_off, pop_off.data(), pop_off.size(), st);
+  upload(c->gpop_off_d, gpop_off.data(), gpop_off.size(), st);
   upload(c->pop_logk1, logk1.data(), logk1.size(), st);
   // Median-select key cache: one slice of K(K-1)/2 keys per population when
   // the total stays modest (otherwise the select recomputes keys per pass).
@@ -428,7 +476,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c->med_off_d, med_off.data(), med_off.size(), st);
   const bool med_cached = med_total > 0 && med_total <= (32ll << 20);
   upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
-  c->init_theta.assign(p.init_poses, p.init_poses + 7 * J);
+  c->init_theta.assign(p.init_poses + 7 * static_cast<int64_t>(lo), p.init_poses + 7 * static_cast<int64_t>(hi));
   upload(c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
 
   // Schedules (host-exact: llround / fmod / pow of the reference).
@@ -510,6 +558,19 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   }
   c->final_loss.ensure(Jz * 8);
   c->final_free.ensure(Jz * 4);
+  if (c->xchg) {
+    const size_t rows = static_cast<size_t>(c->rows_per_rank), wr = static_cast<size_t>(world) * rows;
+    c->theta_all.ensure(static_cast<size_t>(Jg) * 7 * 8);
+    c->drift_all.ensure(static_cast<size_t>(Jg) * 7 * 8);
+    c->xsend.ensure(rows * 14 * 8);
+    c->xrecv.ensure(wr * 14 * 8);
+    c->final_stride = 10 + (c->record_trace ? 9 * c->k_max : 0);
+    c->fsend.ensure(rows * c->final_stride * 8);
+    c->frecv.ensure(wr * c->final_stride * 8);
+    // Padding rows of the send blocks are never read back, but keep them defined.
+    CUDA_OK(cudaMemsetAsync(c->xsend.p, 0, c->xsend.bytes, st));
+    CUDA_OK(cudaMemsetAsync(c->fsend.p, 0, c->fsend.bytes, st));
+  }
 
   // Device views.
   DevProblem& P = c->P;
@@ -536,6 +597,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.pop_off = c->pop_off.as<int>();
   P.pop_logk1 = c->pop_logk1.as<double>();
   P.med_off = c->med_off_d.as<long long>();
+  P.gpop_off = c->gpop_off_d.as<int>();
+  P.j_lo = lo;
   for (int a = 0; a < 3; ++a) {
     P.center[a] = center[a];
     P.com[a] = p.com[a];
@@ -566,6 +629,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.grad = c->grad.as<double>();
   S.prior = c->prior.as<double>();
   S.drift = c->drift.as<double>();
+  S.theta_all = c->xchg ? c->theta_all.as<double>() : S.theta;
+  S.drift_all = c->xchg ? c->drift_all.as<double>() : S.drift;
   S.h = c->h.as<double>();
   S.med_keys = med_cached ? c->med_keys.as<unsigned long long>() : nullptr;
   S.S64 = c->S64.as<double>();
@@ -695,7 +760,16 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
       ++c->launches;
     }
     if (stein) {
-      launch_svgd(P, S, c->gammas[k], c->n_ref, c->eta_stein, c->max_pop, st);
+      launch_drift(P, S, c->gammas[k], c->n_ref, st);
+      if (c->xchg) {
+        // The population's poses and drifts from every rank, in global order.
+        launch_pack_stein(P, S, c->xsend.as<double>(), st);
+        c->xchg->allgather(c->xsend.p, c->xrecv.p, static_cast<size_t>(c->rows_per_rank) * 14 * 8, st);
+        launch_unpack_stein(c->xrecv.as<double>(), c->theta_all.as<double>(), c->drift_all.as<double>(), c->J_glob,
+                            c->xchg->world, c->rows_per_rank, st);
+        c->launches += 2;
+      }
+      launch_stein_update(P, S, c->eta_stein, c->max_pop, st);
       c->launches += 4;
     } else {
       launch_sgd(P, S, st);
@@ -713,6 +787,13 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
   enqueue_nn(c, fin, 0, capture);
   launch_cost(P, S, 1, st);
   c->launches += 3;
+  if (c->xchg) {
+    // Every rank receives every particle's summary (and trace): the solution
+    // each rank returns is the whole population's.
+    launch_pack_final(P, S, c->fsend.as<double>(), c->final_stride, c->k_max, c->record_trace, st);
+    c->xchg->allgather(c->fsend.p, c->frecv.p, static_cast<size_t>(c->rows_per_rank) * c->final_stride * 8, st);
+    ++c->launches;
+  }
   CUDA_OK(cudaGetLastError());
 }
 
@@ -729,7 +810,7 @@ void launch(asicp_ctx* c) {
   }
   c->nn_events.clear();
   CUDA_OK(cudaEventRecord(c->ev0, st));
-  const bool graph = c->use_graph && !c->profile;
+  const bool graph = c->use_graph && !c->profile && (!c->xchg || c->xchg->capturable());
   if (graph) {
     if (!c->graph_valid) {
       cudaGraph_t g;
@@ -752,11 +833,17 @@ void launch(asicp_ctx* c) {
   CUDA_OK(cudaEventRecord(c->ev1, st));
 
   const size_t J = static_cast<size_t>(c->J);
-  c->ensure_staging(c->J);
-  CUDA_OK(cudaMemcpyAsync(c->host.theta, c->S.theta, 7 * J * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(c->host.floss, c->S.final_loss, J * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(c->host.ffree, c->S.final_free, J * 4, cudaMemcpyDeviceToHost, st));
-  CUDA_OK(cudaMemcpyAsync(c->host.conv, c->S.converged, J * 4, cudaMemcpyDeviceToHost, st));
+  c->ensure_staging(c->J_glob);
+  if (c->xchg) {
+    const size_t bytes = static_cast<size_t>(c->xchg->world) * c->rows_per_rank * c->final_stride * 8;
+    c->ensure_gath(bytes);
+    CUDA_OK(cudaMemcpyAsync(c->host_gath, c->frecv.p, bytes, cudaMemcpyDeviceToHost, st));
+  } else {
+    CUDA_OK(cudaMemcpyAsync(c->host.theta, c->S.theta, 7 * J * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(c->host.floss, c->S.final_loss, J * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(c->host.ffree, c->S.final_free, J * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(c->host.conv, c->S.converged, J * 4, cudaMemcpyDeviceToHost, st));
+  }
   CUDA_OK(cudaMemcpyAsync(c->host.stats, c->S.stats, kStats * 8, cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaMemcpyAsync(c->host.refine_total, c->S.refine_count, 4, cudaMemcpyDeviceToHost, st));
   c->in_flight = true;
@@ -768,14 +855,38 @@ void finish(asicp_ctx* c, asicp_solution* out) {
   cudaStream_t st = c->stream;
   c->in_flight = false;
   CUDA_OK(cudaStreamSynchronize(st));
-  const int J = c->J;
+  const int J = c->J_glob;
   const double* theta = c->host.theta;
   const double* floss = c->host.floss;
   const int* ffree = c->host.ffree;
   const int* conv = c->host.conv;
   const unsigned long long* stats = c->host.stats;
   const size_t rows = static_cast<size_t>(c->k_max) * J;
-  if (c->record_trace && rows) {
+  if (c->xchg) {
+    // Gathered summaries (rank-major blocks of rows_per_rank rows) -> global order.
+    const int world = c->xchg->world, stride = c->final_stride;
+    for (int r = 0; r < world; ++r) {
+      const int lo = static_cast<int>(static_cast<int64_t>(r) * J / world);
+      const int hi = static_cast<int>(static_cast<int64_t>(r + 1) * J / world);
+      for (int i = 0; i < hi - lo; ++i) {
+        const double* row = c->host_gath + (static_cast<size_t>(r) * c->rows_per_rank + i) * stride;
+        const int g = lo + i;
+        for (int a = 0; a < 7; ++a) c->host.theta[7 * g + a] = row[a];
+        c->host.floss[g] = row[7];
+        c->host.ffree[g] = static_cast<int>(row[8]);
+        c->host.conv[g] = static_cast<int>(row[9]);
+        if (!c->record_trace) continue;
+        for (int k = 0; k < c->k_max; ++k) {
+          const double* t = row + 10 + 9 * k;
+          const size_t tr = static_cast<size_t>(k) * J + g;
+          if (out->trace_theta)
+            for (int a = 0; a < 7; ++a) out->trace_theta[7 * tr + a] = t[a];
+          if (out->trace_loss) out->trace_loss[tr] = t[7];
+          if (out->trace_in_collision) out->trace_in_collision[tr] = static_cast<int32_t>(t[8]);
+        }
+      }
+    }
+  } else if (c->record_trace && rows) {
     if (out->trace_theta)
       CUDA_OK(cudaMemcpyAsync(out->trace_theta, c->S.trace_theta, rows * 7 * 8, cudaMemcpyDeviceToHost, st));
     if (out->trace_loss)
@@ -922,6 +1033,48 @@ int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen
     launch(ctx);
     finish(ctx, solution);
   });
+}
+
+int asicp_nccl_unique_id(unsigned char* id, char* err, size_t errlen) {
+  if (!id) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] { nccl_unique_id(id); });
+}
+
+static void reset_partition(asicp_ctx* ctx) {
+  if (ctx->in_flight) throw InvalidArgument("asicp_set_partition: a solve is in flight (call asicp_wait)");
+  ctx->xchg.reset();
+  ctx->prepared = false;
+  ctx->graph_valid = false;
+  ctx->graph_sig.clear();
+  if (ctx->graph_exec) {
+    cudaGraphExecDestroy(ctx->graph_exec);
+    ctx->graph_exec = nullptr;
+  }
+}
+
+int asicp_set_partition_nccl(asicp_ctx* ctx, int rank, int world, const unsigned char* id, char* err, size_t errlen) {
+  if (!ctx || !id || world < 1 || rank < 0 || rank >= world) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] {
+    reset_partition(ctx);
+    ctx->xchg = make_nccl_exchange(ctx->device, rank, world, id);
+  });
+}
+
+asicp_group* asicp_group_create(int world) { return world >= 1 ? new asicp_group(world) : nullptr; }
+
+void asicp_group_destroy(asicp_group* group) { delete group; }
+
+int asicp_set_partition_group(asicp_ctx* ctx, asicp_group* group, int rank, char* err, size_t errlen) {
+  if (!ctx || !group || rank < 0 || rank >= group->world) return ASICP_INVALID_ARGUMENT;
+  return guarded(err, errlen, [&] {
+    reset_partition(ctx);
+    ctx->xchg = make_group_exchange(group, rank);
+  });
+}
+
+int asicp_clear_partition(asicp_ctx* ctx) {
+  if (!ctx) return ASICP_INVALID_ARGUMENT;
+  return guarded(nullptr, 0, [&] { reset_partition(ctx); });
 }
 
 int asicp_run_async(asicp_ctx* ctx, char* err, size_t errlen) {

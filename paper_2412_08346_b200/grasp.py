@@ -400,6 +400,25 @@ class Solver:
         _check(self.lib.asicp_run(self.ctx, C.byref(self._bufs.struct), err, 512), err)
         return self._bufs.solution(self._cp.k_stein)
 
+    def set_partition_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Shard every population's particles over `world` ranks (one process
+        per GPU); collective — every rank calls it with rank 0's id."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        err = C.create_string_buffer(512)
+        _check(self.lib.asicp_set_partition_nccl(self.ctx, rank, world, unique_id, err, 512), err)
+        self._cp = None
+
+    def set_partition_group(self, group: "Group", rank: int) -> None:
+        """Shard with the contexts of this process (one host thread per rank)."""
+        err = C.create_string_buffer(512)
+        _check(self.lib.asicp_set_partition_group(self.ctx, group.handle, rank, err, 512), err)
+        self._cp = None
+
+    def clear_partition(self) -> None:
+        self.lib.asicp_clear_partition(self.ctx)
+        self._cp = None
+
     def run_async(self) -> None:
         """Enqueue the prepared solve on this context's stream and return
         (asicp_run_async); collect it with `wait`."""
@@ -419,6 +438,36 @@ class Solver:
         st = L.Stats()
         self.lib.asicp_get_stats(self.ctx, C.byref(st))
         return st
+
+
+class Group:
+    """An in-process exchange group for particle sharding (asicp_group)."""
+
+    def __init__(self, world: int):
+        self.lib = L.load()
+        self.world = world
+        self.handle = self.lib.asicp_group_create(world)
+        if not self.handle:
+            raise InvalidArgument("asicp_group_create: world must be >= 1")
+
+    def close(self):
+        if self.handle:
+            self.lib.asicp_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 makes it, the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    err = C.create_string_buffer(512)
+    _check(L.load().asicp_nccl_unique_id(buf, err, 512), err)
+    return buf.raw
 
 
 _DEFAULT: Solver | None = None

@@ -113,6 +113,26 @@ def solve_sharded(problems: Sequence[GraspProblem], solve_fn: Callable[[GraspPro
     return combine(problems, all_gather(solve_local(problems, solve_fn, rank, world)))
 
 
+def join_particle_partition(solver, rank: int, world: int, broadcast: Callable[[object], object]) -> bytes:
+    """Particle sharding within a population (cfg5): rank 0 makes the NCCL
+    unique id, `broadcast` (torch.distributed.broadcast_object_list from rank
+    0) hands it to every rank, and every rank joins the communicator with its
+    Solver (asicp_set_partition_nccl, collective).  Afterwards each rank
+    prepares the SAME full problem; the solver owns the particle slice
+    [r J / R, (r + 1) J / R) and returns the full answer on every rank."""
+    from .grasp import nccl_unique_id
+
+    uid = nccl_unique_id() if rank == 0 else None
+    uid = broadcast(uid)
+    solver.set_partition_nccl(rank, world, uid)
+    return uid
+
+
+def particle_slice(J: int, rank: int, world: int) -> tuple:
+    """The global particles a rank owns under particle sharding (solver.cu prepare)."""
+    return rank * J // world, (rank + 1) * J // world
+
+
 def combine(problems: Sequence[GraspProblem], gathered: list) -> list:
     """Per-object selection from the gathered unit summaries."""
     units = units_of(problems)
