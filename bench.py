@@ -8,7 +8,7 @@ step = one complete optimize_grasp solve: J * k_max = 76,800
 particle-iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload cfg2|cfg3|cfg4]
+                  [--workload cfg2|cfg3|cfg4|cfg5] [--n-object N]
 
 cfg2 / cfg3 at N > 1 run under torchrun, one rank per GPU; each rank solves its
 own object instance (object sharding: no data-path collective), so the scaling
@@ -21,6 +21,11 @@ the ranks by longest-processing-time (shard.py), each rank keeps its units
 device-resident and overlaps them on one GPU (batch.py), and the per-object
 answers are gathered and selected after the solves.  Total work is fixed, so
 the scaling is strong.
+
+cfg5 (BASELINE.json configs[4]) is one population of 16384 particles against
+an n-point cylinder (--n-object, default 10k): at N > 1 the particles are
+sharded over the ranks, which all-gather the population's poses and drifts
+over NCCL each Stein iteration (strong scaling).
 """
 from __future__ import annotations
 
@@ -48,7 +53,10 @@ WORKLOADS = {
                 "(15 Stein), SDF collision on"),
     "cfg4": (4, "cfg4: 11-object batch (cylinders/boxes/spheres/blobs, 10k pts) x 3 KG3 preshapes x 1024 "
                 "particles, 40 iters (15 Stein), (object, preshape) units sharded over ranks"),
+    "cfg5": (5, "cfg5: one KG3 preshape x 16384 particles (one Stein population) vs an n-pt cylinder, 40 iters "
+                "(15 Stein), particles sharded over ranks with an NCCL allgather per Stein iteration"),
 }
+CFG5_CPU_SAMPLE_PARTICLES = 2048
 N_BATCH_OBJECTS = 11
 
 
@@ -59,6 +67,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--n-object", type=int, default=0, help="cfg5 object cloud size (default 10000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -144,10 +153,15 @@ def cpu_reference(fixture, threads: int):
     return dt, sol
 
 
-def sample_fixture(workload: str, seed: int = 0):
-    """The bounded CPU-reference sample: one full solve of one object."""
+def sample_fixture(workload: str, n_object: int = 0, seed: int = 0):
+    """The bounded CPU-reference sample: one full solve of one object (cfg5:
+    the same object with 2048 of the 16384 particles — a smaller population
+    makes the reference's O(K^2) Stein step cheaper per particle, so the
+    sampled rate flatters the CPU)."""
     from paper_2412_08346_b200 import fixtures
 
+    if workload == "cfg5":
+        return fixtures.config(5, seed=seed, particles_per_preshape=CFG5_CPU_SAMPLE_PARTICLES, n_object=n_object)
     return fixtures.config(WORKLOADS[workload][0], seed=seed)
 
 
@@ -161,7 +175,7 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
         return 0
     threads = os.cpu_count() or 1
-    fx = sample_fixture(args.workload)
+    fx = sample_fixture(args.workload, args.n_object)
     pits = fx.J * fx.k_max
     for _ in range(args.warmup):
         cpu_reference(fx, threads)
@@ -176,7 +190,7 @@ def run_reference_arm(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if args.workload == "cfg4" else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if args.workload in ("cfg4", "cfg5") else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(args.workload, fx, world),
         "solve_latency_ms": ms,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
@@ -193,7 +207,11 @@ def config_dict(workload, fx, world):
          "n_scene": int(v.n_scene), "n_surface": int(v.preshapes[0].n_surface),
          "sdf_dims": list(v.sdf_grids[0].dims),
          "l2": "flushed (256 MiB write) before every timed step"}
-    if workload == "cfg4":
+    if workload == "cfg5":
+        d.update({"parallelism": f"particle-shard x{world} (NCCL allgather of [theta, drift] per Stein iteration)"
+                                 if world > 1 else "1 GPU",
+                  "step": "one full optimize_grasp solve of the 16384-particle population"})
+    elif workload == "cfg4":
         d.update({"objects": N_BATCH_OBJECTS, "units": 3 * N_BATCH_OBJECTS,
                   "parallelism": f"(object, preshape) units, LPT over {world} GPU(s), overlapped streams per GPU",
                   "step": "all 11 objects solved (33 units) + per-object selection"})
@@ -304,9 +322,21 @@ def main():
         launches_of = runner.launches
     else:
         cfg = WORKLOADS[args.workload][0]
-        fx = fixtures.config(cfg, seed=rank)  # object instance per rank (object sharding)
-        pits_total = world * fx.J * fx.k_max
         solver = Solver(device=local, stream=main_stream.cuda_stream)
+        if args.workload == "cfg5":
+            # One population sharded by particle: every rank prepares the same problem.
+            fx = fixtures.config(5, seed=0, n_object=args.n_object)
+            pits_total = fx.J * fx.k_max
+            if world > 1:
+                def broadcast(obj):
+                    box = [obj]
+                    dist.broadcast_object_list(box, src=0)
+                    return box[0]
+
+                shard.join_particle_partition(solver, rank, world, broadcast)
+        else:
+            fx = fixtures.config(cfg, seed=rank)  # object instance per rank (object sharding)
+            pits_total = world * fx.J * fx.k_max
         solver.prepare(fx)
         holder = {}
 
@@ -385,7 +415,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "strong" if batch else "weak",
+            "scaling": "strong" if args.workload in ("cfg4", "cfg5") else "weak",
             "vs_baseline": None, "dtype": "f64 (FP32-certified NN filter)", "data": "synthetic",
             "config": config_dict(args.workload, fx, world),
             "solve_latency_ms": ms_max,
@@ -413,10 +443,12 @@ def main():
 
                 if ref.available():
                     threads = os.cpu_count() or 1
-                    sfx = sample_fixture(args.workload)
+                    sfx = sample_fixture(args.workload, args.n_object)
                     spits = sfx.J * sfx.k_max
                     dt, rs = cpu_reference(sfx, threads)
-                    if batch:
+                    if args.workload == "cfg5":
+                        same = None  # the sample is a smaller population than the bench's
+                    elif batch:
                         same = bool(rs.final_loss == result[0]["final_loss"]
                                     and np.array_equal(rs.theta, result[0]["theta"]))
                     else:
@@ -424,7 +456,8 @@ def main():
                                     and rs.final_loss == result.final_loss)
                     line["cpu_baseline"] = {
                         "value": spits / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                        "sample": f"one full {args.workload} solve of object 0 ({spits} particle-iterations), "
+                        "sample": f"one full {args.workload} solve of object 0 ({sfx.J} particles, {spits} "
+                                  f"particle-iterations), "
                                   f"oracle/_ref graspmatch::optimize_grasp workers={threads}",
                         "latency_ms": dt * 1e3,
                         "bit_identical": same,

@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
   if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // no local particle reads h
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
   if (K < 1) return;
+  if (K >= kMedBigK && P.bandwidth_mode != 1) return;  // med_*_kernel (below)
   if (P.bandwidth_mode == 1) {
     if (threadIdx.x == 0) S.h[pop] = P.fixed_bandwidth;
     return;
@@ -543,6 +544,143 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
     const double median = __longlong_as_double(static_cast<long long>(s_prefix));
     const double h = median / P.pop_logk1[pop];
     S.h[pop] = h < 1e-6 ? 1e-6 : h;  // std::max(h, 1e-6)
+  }
+}
+
+// Large populations (K >= kMedBigK, e.g. cfg5's 16384 particles: 134M pair
+// keys): the same exact radix select spread over the whole GPU.  Six passes
+// of 12/12/12/12/12/4 bits; every pass recomputes the keys tile by tile
+// (128 x 128 blocks of the upper triangle, partner poses in shared memory —
+// FP64 math is cheaper than re-reading a cached 1 GB key array), counts the
+// keys matching the selected prefix into a per-CTA shared histogram with
+// warp-aggregated atomics, and flushes it to a global histogram; a one-CTA
+// select kernel then picks the digit holding rank M/2.  The key multiset and
+// the order statistic are those of the single-CTA kernel.
+constexpr int kMedTile = 128;
+constexpr int kMedBins = 4096;
+
+__device__ __forceinline__ bool med_big(const DevProblem& P, int pop, int& b, int& K) {
+  if (P.pop_off[pop + 1] == P.pop_off[pop] || P.bandwidth_mode == 1) return false;
+  b = P.gpop_off[pop];
+  K = P.gpop_off[pop + 1] - b;
+  return K >= kMedBigK;
+}
+
+__global__ void med_init_kernel(DevProblem P, DevState S) {
+  const int pop = blockIdx.x;
+  int b, K;
+  if (!med_big(P, pop, b, K)) return;
+  for (int i = threadIdx.x; i < kMedBins; i += blockDim.x) S.med_hist[pop * kMedBins + i] = 0;
+  if (threadIdx.x == 0) {
+    MedState& m = S.med_state[pop];
+    m.prefix = 0;
+    m.mask = 0;
+    m.rank = static_cast<long long>(K) * (K - 1) / 2 / 2;
+  }
+}
+
+__global__ void __launch_bounds__(256) med_hist_kernel(DevProblem P, DevState S, int shift, int bits) {
+  const int pop = blockIdx.y;
+  int b, K;
+  if (!med_big(P, pop, b, K)) return;
+  __shared__ unsigned int hist[kMedBins];
+  __shared__ double ta[kMedTile][3], tb[kMedTile][3];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kMedBins; i += blockDim.x) hist[i] = 0;
+  const unsigned long long prefix = S.med_state[pop].prefix, mask = S.med_state[pop].mask;
+  const unsigned int dmask = (1u << bits) - 1u;
+  const int nb = (K + kMedTile - 1) / kMedTile;
+  const long long tiles = static_cast<long long>(nb) * (nb + 1) / 2;
+  for (long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    int bi = 0;
+    long long rem = tile;
+    while (rem >= nb - bi) {
+      rem -= nb - bi;
+      ++bi;
+    }
+    const int bj = bi + static_cast<int>(rem);
+    const int ni = min(kMedTile, K - bi * kMedTile), nj = min(kMedTile, K - bj * kMedTile);
+    __syncthreads();
+    for (int e = tid; e < kMedTile * 3; e += blockDim.x) {
+      const int r = e / 3, a = e % 3;
+      ta[r][a] = r < ni ? S.theta_all[7 * (b + bi * kMedTile + r) + a] : 0.0;
+      tb[r][a] = r < nj ? S.theta_all[7 * (b + bj * kMedTile + r) + a] : 0.0;
+    }
+    __syncthreads();
+    for (int e = tid; e < kMedTile * kMedTile; e += blockDim.x) {  // uniform trip count per warp
+      const int ii = e / kMedTile, jj = e % kMedTile;
+      bool hit = ii < ni && jj < nj && (bi < bj || ii < jj);
+      unsigned int digit = 0;
+      if (hit) {
+        const double d2 = sqnorm(sub(V3{ta[ii][0], ta[ii][1], ta[ii][2]}, V3{tb[jj][0], tb[jj][1], tb[jj][2]}));
+        const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
+        hit = (key & mask) == prefix;
+        digit = static_cast<unsigned int>(key >> shift) & dmask;
+      }
+      const unsigned int active = __ballot_sync(0xffffffffu, hit);
+      if (hit) {
+        const unsigned int peers = __match_any_sync(active, digit);
+        if (__ffs(peers) - 1 == lane) atomicAdd(&hist[digit], static_cast<unsigned int>(__popc(peers)));
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kMedBins; i += blockDim.x)
+    if (hist[i]) atomicAdd(&S.med_hist[pop * kMedBins + i], hist[i]);
+}
+
+__global__ void __launch_bounds__(1024) med_select_kernel(DevProblem P, DevState S, int shift, int bits,
+                                                          int last) {
+  const int pop = blockIdx.x;
+  int b, K;
+  if (!med_big(P, pop, b, K)) return;
+  unsigned int* hist = S.med_hist + pop * kMedBins;
+  const int nbins = 1 << bits;
+  constexpr int kPer = kMedBins / 1024;
+  __shared__ long long part[1024];
+  __shared__ int s_digit;
+  __shared__ long long s_below;
+  const int tid = threadIdx.x;
+  long long mine = 0;
+  for (int k = 0; k < kPer; ++k) {
+    const int bin = tid * kPer + k;
+    if (bin < nbins) mine += hist[bin];
+  }
+  part[tid] = mine;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive scan
+    const long long v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  const long long rank = S.med_state[pop].rank;
+  const long long before = tid ? part[tid - 1] : 0;
+  if (rank >= before && rank < part[tid]) {
+    long long acc = before;
+    for (int k = 0; k < kPer; ++k) {
+      const int bin = tid * kPer + k;
+      const long long c = bin < nbins ? hist[bin] : 0;
+      if (rank < acc + c) {
+        s_digit = bin;
+        s_below = acc;
+        break;
+      }
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < kMedBins; i += blockDim.x) hist[i] = 0;
+  if (tid == 0) {
+    MedState& m = S.med_state[pop];
+    m.rank = rank - s_below;
+    m.prefix |= static_cast<unsigned long long>(s_digit) << shift;
+    m.mask |= static_cast<unsigned long long>(nbins - 1) << shift;
+    if (last) {
+      const double median = __longlong_as_double(static_cast<long long>(m.prefix));
+      const double h = median / P.pop_logk1[pop];
+      S.h[pop] = h < 1e-6 ? 1e-6 : h;  // std::max(h, 1e-6)
+    }
   }
 }
 
@@ -834,11 +972,22 @@ void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int
                        cudaStream_t st) {
   pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
 }
-void launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, cudaStream_t st) {
+int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int big_grid, cudaStream_t st) {
+  int n = 3;
   median_kernel<<<P.n_pop, 1024, 0, st>>>(P, S);
+  if (big_grid > 0) {
+    med_init_kernel<<<P.n_pop, 256, 0, st>>>(P, S);
+    const int shifts[6] = {52, 40, 28, 16, 4, 0}, bits[6] = {12, 12, 12, 12, 12, 4};
+    for (int pass = 0; pass < 6; ++pass) {
+      med_hist_kernel<<<dim3(big_grid, P.n_pop), 256, 0, st>>>(P, S, shifts[pass], bits[pass]);
+      med_select_kernel<<<P.n_pop, 1024, 0, st>>>(P, S, shifts[pass], bits[pass], pass == 5 ? 1 : 0);
+    }
+    n += 13;
+  }
   dim3 grid((max_pop + kSvgdJ - 1) / kSvgdJ, P.n_pop);
   svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
   copy_theta_kernel<<<(7 * P.J + 255) / 256, 256, 0, st>>>(S.theta, S.theta_next, 7 * P.J);
+  return n;
 }
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st) {
   sgd_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S);

@@ -58,8 +58,17 @@ struct DevProblem {
   double conv_thr;
 };
 
+// Populations at least this large take the grid-wide median select.
+constexpr int kMedBigK = 2048;
+struct MedState {
+  unsigned long long prefix, mask;
+  long long rank;
+};
+
 // Mutable solver state (device pointers).
 struct DevState {
+  unsigned int* med_hist;  // n_pop x 4096 (grid-wide median select)
+  MedState* med_state;     // n_pop
   double* theta;       // J x 7
   double* theta_next;  // J x 7 (SVGD double buffer)
   double* loss;
@@ -135,7 +144,9 @@ int minibatch_smem_cap();
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
 void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st);
-void launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, cudaStream_t st);
+// big_grid > 0: some population has K >= kMedBigK; the grid-wide select runs
+// with big_grid CTAs per population (returns the launch count).
+int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int big_grid, cudaStream_t st);
 // Particle-sharding exchange helpers: pack local rows [theta(7), drift(7)]
 // into `send` (stride 14 doubles), and scatter a gathered world x rows_per_rank
 // block back into global order (rank r's rows start at floor(r * J_glob / world)).

@@ -131,7 +131,8 @@ struct asicp_ctx {
   // allgather blocks to equal size.  Unsharded: xchg null, J_glob = J.
   std::unique_ptr<asicp::Exchange> xchg;
   int J_glob = 0, j_lo = 0, rows_per_rank = 0, final_stride = 0;
-  Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d;
+  Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d, med_hist, med_state;
+  int med_big_grid = 0;
   double* host_gath = nullptr;
   size_t host_gath_bytes = 0;
 
@@ -206,7 +207,7 @@ struct asicp_ctx {
     free_staging();
     if (host_gath) cudaFreeHost(host_gath);
     xchg.reset();
-    Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend, &xrecv, &fsend, &frecv, &gpop_off_d};
+    Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend, &xrecv, &fsend, &frecv, &gpop_off_d, &med_hist, &med_state};
     for (Buf* b : shard_bufs) b->release();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto& e : nn_events) {
@@ -464,15 +465,28 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   // the total stays modest (otherwise the select recomputes keys per pass).
   std::vector<long long> med_off(n_pre, -1);
   long long med_total = 0;
-  for (int i = 0; i < n_pre; ++i) med_total += p.init_counts[i] * (p.init_counts[i] - 1) / 2;
+  long long big_tiles = 0;
+  for (int i = 0; i < n_pre; ++i) {
+    const long long K = p.init_counts[i];
+    if (K < kMedBigK) {
+      med_total += K * (K - 1) / 2;
+    } else {  // grid-wide select (kernels.cu med_*_kernel): 128 x 128 tiles of the triangle
+      const long long nb = (K + 127) / 128;
+      big_tiles = std::max(big_tiles, nb * (nb + 1) / 2);
+    }
+  }
+  c->med_big_grid = static_cast<int>(std::min<long long>(big_tiles, 8ll * c->num_sms));
   if (med_total > 0 && med_total <= (32ll << 20)) {
     long long o = 0;
     for (int i = 0; i < n_pre; ++i) {
+      if (p.init_counts[i] >= kMedBigK) continue;
       med_off[i] = o;
       o += p.init_counts[i] * (p.init_counts[i] - 1) / 2;
     }
     c->med_keys.ensure(static_cast<size_t>(med_total) * 8);
   }
+  c->med_hist.ensure(static_cast<size_t>(n_pre) * 4096 * 4);
+  c->med_state.ensure(static_cast<size_t>(n_pre) * sizeof(MedState));
   upload(c->med_off_d, med_off.data(), med_off.size(), st);
   const bool med_cached = med_total > 0 && med_total <= (32ll << 20);
   upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
@@ -525,10 +539,13 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->pool32.ensure(jobj * 16);
   if (static_cast<size_t>(c->n_obj) * 4 > static_cast<size_t>(minibatch_smem_cap()))
     c->fy_scratch.ensure(Jz * static_cast<size_t>(c->n_obj) * 4);
-  // Parallel Fisher-Yates scratch (5 int arrays per particle) when it stays
-  // under 1 GiB; the serial kernel covers the rest.
+  // Parallel Fisher-Yates scratch (5 int arrays per particle) when it takes at
+  // most a quarter of the free HBM; the serial kernel covers the rest.
+  size_t free_b = 0, total_b = 0;
+  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
   const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
-  const bool fy_par_on = fy_par_bytes <= (1ull << 30) && c->n_obj <= 12 * 1024 * 4;
+  const bool fy_par_on = (fy_par_bytes <= c->fy_par.bytes || fy_par_bytes <= free_b / 4) &&
+                         c->n_obj <= 12 * 1024 * 4;
   if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
   // Work items: forward <= base_items * nchunks; reverse <= J * ceil(n_scene / 256).
   c->items0.ensure((static_cast<size_t>(base_items) * c->nchunks_max + Jz) * sizeof(NnItem));
@@ -632,6 +649,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.theta_all = c->xchg ? c->theta_all.as<double>() : S.theta;
   S.drift_all = c->xchg ? c->drift_all.as<double>() : S.drift;
   S.h = c->h.as<double>();
+  S.med_hist = c->med_hist.as<unsigned int>();
+  S.med_state = c->med_state.as<MedState>();
   S.med_keys = med_cached ? c->med_keys.as<unsigned long long>() : nullptr;
   S.S64 = c->S64.as<double>();
   S.Sq32 = c->Sq32.as<float4>();
@@ -769,8 +788,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
                             c->xchg->world, c->rows_per_rank, st);
         c->launches += 2;
       }
-      launch_stein_update(P, S, c->eta_stein, c->max_pop, st);
-      c->launches += 4;
+      c->launches += 1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->med_big_grid, st);
     } else {
       launch_sgd(P, S, st);
       ++c->launches;

@@ -220,3 +220,18 @@ def test_partial_view_and_batch_objects_match_port(solver, cfg, seed, ppp, k_max
     np.testing.assert_array_equal(got.trace_in_collision, want.trace_in_collision)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)
+
+
+def test_large_population_grid_median_matches_port(solver):
+    """A population above kMedBigK (2048) takes the grid-wide median select;
+    2100 particles leave ragged 128-row tiles.  Full trace against the C port."""
+    from oracle import ref
+
+    if not ref.port_available():
+        pytest.skip("oracle port not built")
+    fx = fixtures.config(5, seed=2, particles_per_preshape=2100, n_object=500)
+    fx.set(k_max=5, k_stein=3, anneal_period_total=5, record_trace=1)  # T >= C = 5 cycles
+    want = ref.port_optimize_grasp(fx)
+    got = solver.optimize(fx)
+    assert np.array_equal(got.trace_theta, want.trace_theta)
+    assert_same_solution(got, want)

@@ -107,3 +107,12 @@ def test_partition_needs_a_particle_per_rank():
         s.prepare(fx)
     s.close()
     group.close()
+
+
+def test_group_sharding_large_population(solver):
+    """cfg5 shape above the grid-wide median threshold, sharded over 2 ranks."""
+    fx = fixtures.config(5, seed=1, particles_per_preshape=2600, n_object=4000).set(
+        k_max=6, k_stein=5, anneal_period_total=6, record_trace=1)
+    want = solver.optimize(fx)
+    for got in sharded_solve(fx, 2):
+        assert_identical(got, want)
