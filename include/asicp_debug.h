@@ -34,6 +34,12 @@ double asicp_dbg_ffma_tflops(int iters);
 struct asicp_ctx;
 int asicp_dbg_raw_stats(struct asicp_ctx* ctx, uint64_t* out);
 
+/* Per-iteration NN work of the last asicp_run: for k = 0..k_max (k_max = the
+ * final ranking) out[4k + 0/1] = forward/reverse (query, candidate) pairs,
+ * out[4k + 2/3] = forward/reverse queries.  Copies min(n, 4 (k_max + 1))
+ * entries; returns 4 (k_max + 1), or -1 (no prepared problem / in flight). */
+int64_t asicp_dbg_iter_stats(struct asicp_ctx* ctx, uint64_t* out, int64_t n);
+
 /* The device minibatch sampler (mt19937_64 + Lemire + partial Fisher-Yates,
  * spatial_index.cpp:111-123) on one stream seeded with `seed`: `calls`
  * consecutive draws of ms[c] indices from [0, n), written back to back.

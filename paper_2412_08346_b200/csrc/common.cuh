@@ -30,6 +30,24 @@ __device__ __forceinline__ float nn_margin(double A, double B) {
   return __double2float_ru(2.0 * (e32 + e64));
 }
 
+// Forward NN candidates (the object cloud and the minibatch pools) are stored
+// pair-interleaved: candidates 2p and 2p + 1 occupy two float4s,
+// (x0, x1, y0, y1) and (z0, z1, w0, w1), so one LDS.128 yields ready-made
+// register pairs for the packed FFMA2 of the NN filter.  16 B per candidate
+// as before; splits and tiles start at even candidates.
+__host__ __device__ __forceinline__ int64_t pc_index(int64_t c) { return (c >> 1) * 8 + (c & 1); }
+__device__ __forceinline__ float4 pc_get(const float4* base, int64_t c) {
+  const float* f = reinterpret_cast<const float*>(base) + pc_index(c);
+  return make_float4(f[0], f[2], f[4], f[6]);
+}
+__device__ __forceinline__ void pc_put(float4* base, int64_t c, float4 v) {
+  float* f = reinterpret_cast<float*>(base) + pc_index(c);
+  f[0] = v.x;
+  f[2] = v.y;
+  f[4] = v.z;
+  f[6] = v.w;
+}
+
 // True contact-surface size of particle j (surface rows are padded to kSub).
 __device__ __forceinline__ int surf_count(const DevProblem& P, int j) {
   const int pre = P.part_pre[j];

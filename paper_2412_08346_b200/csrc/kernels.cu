@@ -343,10 +343,10 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
   for (int i = threadIdx.x; i < mt::kN; i += blockDim.x) gst[i] = st[i];
   if (threadIdx.x == 0) S.rng_mti[j] = s_mti;
   __syncthreads();
-  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
-  for (int i = threadIdx.x; i < m; i += blockDim.x) pool32[i] = P.obj_cand[pool[i]];
+  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;  // pair-interleaved (pc_*)
+  for (int i = threadIdx.x; i < m; i += blockDim.x) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
   for (int i = m + threadIdx.x; i < round_up(m, kSub); i += blockDim.x)
-    pool32[i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
 }
 
 // ---------------------------------------------------------------------------
@@ -469,8 +469,50 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
   for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
 }
 
-// One CTA per population: 8 radix passes of 8 bits over the K(K-1)/2 keys
-// (nth_element at M/2, optim.cpp:141-142: an exact order statistic).
+// Bitonic sort of n (a power of two) keys in shared memory by the whole CTA.
+__device__ void block_bitonic_sort(unsigned long long* s, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const unsigned long long a = s[i], c = s[ixj];
+          const bool asc = (i & k) == 0;
+          if ((a > c) == asc) {
+            s[i] = c;
+            s[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Row-major position p of the strict upper triangle of a K x K matrix -> (i, j).
+__device__ __forceinline__ void tri_index(long long p, int K, int* i_out, int* j_out) {
+  const double a = 2.0 * K - 1.0;
+  int i = static_cast<int>((a - sqrt(fmax(a * a - 8.0 * static_cast<double>(p), 0.0))) * 0.5);
+  i = max(0, min(i, K - 2));
+  auto start = [&](int r) { return static_cast<long long>(r) * (2ll * K - r - 1) / 2; };
+  while (i > 0 && start(i) > p) --i;
+  while (i < K - 2 && start(i + 1) <= p) ++i;
+  *i_out = i;
+  *j_out = i + 1 + static_cast<int>(p - start(i));
+}
+
+constexpr int kMedSample = 2048;  // sampled keys that bracket the median
+constexpr int kMedMid = 8192;     // keys the bracket may hold (sorted in shared memory)
+constexpr int kMedDelta = 96;     // bracket half-width in sample ranks (~4 sigma at 2048 samples)
+constexpr int kMedSmallSmem = (kMedSample + kMedMid) * 8;
+
+// One CTA per population (K < kMedBigK).  Fast path: sort a 2048-key sample
+// (bitonic, shared memory), take the bracket [lo, hi] of sample ranks around
+// M/2, count the keys below lo and gather the keys inside the bracket in one
+// pass, sort those and read rank M/2 directly — exact whenever the bracket
+// holds rank M/2 and at most 8192 keys (always when M <= 8192).  Otherwise
+// the 8-bit radix select below (nth_element at M/2, optim.cpp:141-142: an
+// exact order statistic either way).
 __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) {
   const int pop = blockIdx.x;
   if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // no local particle reads h
@@ -488,11 +530,85 @@ __global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) 
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long s_prefix, s_mask;
   __shared__ long long s_rank;
+  __shared__ int s_nmid;
+  __shared__ unsigned long long s_clo;
   const long long M = static_cast<long long>(K) * (K - 1) / 2;
+  const long long r = M / 2;
+  auto key_at = [&](int i, int jj) {
+    const double d2 = sqnorm(sub(pose_t(th_of(S.theta_all, b + i)), pose_t(th_of(S.theta_all, b + jj))));
+    return static_cast<unsigned long long>(__double_as_longlong(d2));
+  };
+  {
+    extern __shared__ unsigned long long med_dyn[];
+    unsigned long long* smp = med_dyn;
+    unsigned long long* mid = med_dyn + kMedSample;
+    unsigned long long lo = 0, hi = ~0ull;
+    if (threadIdx.x == 0) {
+      s_nmid = 0;
+      s_clo = 0;
+    }
+    if (M > kMedMid) {
+      for (int s = threadIdx.x; s < kMedSample; s += blockDim.x) {
+        int i, jj;
+        tri_index((2ll * s + 1) * M / (2ll * kMedSample), K, &i, &jj);
+        smp[s] = key_at(i, jj);
+      }
+      __syncthreads();
+      block_bitonic_sort(smp, kMedSample);
+      const long long rs = r * kMedSample / M;
+      if (rs - kMedDelta >= 0) lo = smp[rs - kMedDelta];
+      if (rs + kMedDelta < kMedSample) hi = smp[rs + kMedDelta];
+    }
+    __syncthreads();
+    unsigned long long clo = 0;
+    const int lane = threadIdx.x & 31;
+    int i = 0;
+    long long row_start = 0;
+    for (long long p0 = 0; p0 < M; p0 += blockDim.x) {  // uniform trip count: full-warp ballots
+      const long long p = p0 + threadIdx.x;
+      bool in = false;
+      unsigned long long key = 0;
+      if (p < M) {
+        while (p >= row_start + (K - 1 - i)) {
+          row_start += K - 1 - i;
+          ++i;
+        }
+        key = key_at(i, i + 1 + static_cast<int>(p - row_start));
+        clo += key < lo ? 1 : 0;
+        in = key >= lo && key <= hi;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      int base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_nmid, __popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (in) {
+        const int slot = base + __popc(bal & ((1u << lane) - 1u));
+        if (slot < kMedMid) mid[slot] = key;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) clo += __shfl_down_sync(0xffffffffu, clo, off);
+    if (lane == 0 && clo) atomicAdd(&s_clo, clo);
+    __syncthreads();
+    const int nmid = s_nmid;
+    const long long c_lo = static_cast<long long>(s_clo);
+    if (c_lo <= r && r < c_lo + nmid && nmid <= kMedMid) {
+      int n2 = 2;
+      while (n2 < nmid) n2 <<= 1;
+      for (int e = nmid + threadIdx.x; e < n2; e += blockDim.x) mid[e] = ~0ull;
+      __syncthreads();
+      block_bitonic_sort(mid, n2);
+      if (threadIdx.x == 0) {
+        const double median = __longlong_as_double(static_cast<long long>(mid[r - c_lo]));
+        const double h = median / P.pop_logk1[pop];
+        S.h[pop] = h < 1e-6 ? 1e-6 : h;  // std::max(h, 1e-6)
+      }
+      return;
+    }
+  }
   if (threadIdx.x == 0) {
     s_prefix = 0;
     s_mask = 0;
-    s_rank = M / 2;
+    s_rank = r;
   }
   // Keys are computed once (row-major over the upper triangle) into the
   // population's slice of S.med_keys when it has one, then re-read by the
@@ -758,6 +874,115 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
   }
 }
 
+// Split form for small populations (the fused kernel above has only K/32
+// CTAs per population): (1) every (partner i, own j) kernel value pair
+// (rbf, |q_i . q_j|) in a grid of 32 x 32 tiles, into S.kmat; (2) the ordered
+// accumulation — one warp per pose component, one lane per own particle, the
+// same left-to-right sums and update as svgd_kernel.
+__global__ void __launch_bounds__(256) svgd_kmat_kernel(DevProblem P, DevState S) {
+  const int pop = blockIdx.z;
+  const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;
+  const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
+  const int j0 = blockIdx.x * kSvgdJ, i0 = blockIdx.y * kSvgdJ;
+  if (j0 >= Kl || i0 >= K) return;
+  __shared__ double ti[kSvgdJ][7], tj[kSvgdJ][7];
+  const int nj = min(kSvgdJ, Kl - j0), ni = min(kSvgdJ, K - i0);
+  for (int e = threadIdx.x; e < kSvgdJ * 7; e += blockDim.x) {
+    const int r = e / 7, a = e % 7;
+    ti[r][a] = r < ni ? S.theta_all[7 * (b + i0 + r) + a] : 0.0;
+    tj[r][a] = r < nj ? S.theta[7 * (lb + j0 + r) + a] : 0.0;
+  }
+  __syncthreads();
+  const double h = S.h[pop];
+  double2* km = S.kmat + P.kofs[pop];
+  for (int e = threadIdx.x; e < kSvgdJ * kSvgdJ; e += blockDim.x) {
+    const int ii = e / kSvgdJ, jj = e % kSvgdJ;
+    if (ii >= ni || jj >= nj) continue;
+    const V3 a = V3{ti[ii][0], ti[ii][1], ti[ii][2]};
+    const V3 c = V3{tj[jj][0], tj[jj][1], tj[jj][2]};
+    const double kv = glibc_exp(-sqnorm(sub(a, c)) / h);  // rbf_kernel (optim.cpp:120-125)
+    const double dq = ((ti[ii][3] * tj[jj][3] + ti[ii][4] * tj[jj][4]) + ti[ii][5] * tj[jj][5]) +
+                      ti[ii][6] * tj[jj][6];
+    km[static_cast<int64_t>(i0 + ii) * Kl + j0 + jj] = make_double2(kv, fabs(dq));  // rotation_kernel (:127-131)
+  }
+}
+
+__global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevState S, double eta) {
+  const int pop = blockIdx.y;
+  const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;
+  const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
+  const int j0 = blockIdx.x * kSvgdJ;
+  if (j0 >= Kl) return;
+  __shared__ double dir[kSvgdJ][7];
+  __shared__ double2 kt[kSvgdJ][kSvgdJ];  // [partner][own] of the current 32-partner tile
+  __shared__ double dt[kSvgdJ][7], tt[kSvgdJ][7];
+  constexpr int kT = kSvgdJ * 7;
+  constexpr int kPer = (kSvgdJ * kSvgdJ + kT - 1) / kT;
+  const int tid = threadIdx.x;
+  const int comp = tid / 32, jl = tid % 32;
+  const int nj = min(kSvgdJ, Kl - j0);
+  const int jg = P.j_lo + lb - b + j0 + jl;  // own position within the population
+  const double two_h = 2.0 / S.h[pop];
+  const double own = jl < nj ? S.theta[7 * (lb + j0 + jl) + comp] : 0.0;
+  const double2* km = S.kmat + P.kofs[pop];
+  // The next tile is fetched into registers while the current one is summed.
+  double2 rk[kPer];
+  double rd = 0.0, rt = 0.0;
+  auto fetch = [&](int i0) {
+    const int ni = min(kSvgdJ, K - i0);
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kT, ii = e / kSvgdJ, jj = e % kSvgdJ;
+      rk[u] = (e < kSvgdJ * kSvgdJ && ii < ni && jj < nj) ? km[static_cast<int64_t>(i0 + ii) * Kl + j0 + jj]
+                                                          : make_double2(0.0, 0.0);
+    }
+    const int r = tid / 7, a = tid % 7;
+    rd = r < ni ? S.drift_all[7 * (b + i0 + r) + a] : 0.0;
+    rt = r < ni ? S.theta_all[7 * (b + i0 + r) + a] : 0.0;
+  };
+  fetch(0);
+  double acc = 0.0;
+  for (int i0 = 0; i0 < K; i0 += kSvgdJ) {
+    __syncthreads();  // the previous tile is consumed
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + u * kT;
+      if (e < kSvgdJ * kSvgdJ) kt[e / kSvgdJ][e % kSvgdJ] = rk[u];
+    }
+    dt[tid / 7][tid % 7] = rd;
+    tt[tid / 7][tid % 7] = rt;
+    __syncthreads();
+    if (i0 + kSvgdJ < K) fetch(i0 + kSvgdJ);
+    const int ni = min(kSvgdJ, K - i0);
+    for (int ii = 0; ii < ni; ++ii) {
+      const double d = dt[ii][comp];
+      if (i0 + ii == jg) {
+        acc = acc - d;  // analytic self-term (optim.cpp:206-212)
+      } else if (comp < 3) {
+        const double v = kt[ii][jl].x;
+        acc = acc + (-d) * v;
+        acc = acc + (two_h * (own - tt[ii][comp])) * v;
+      } else {
+        acc = acc + (-d) * kt[ii][jl].y;
+      }
+    }
+  }
+  if (jl < nj) dir[jl][comp] = acc;
+  __syncthreads();
+  if (threadIdx.x < nj) {
+    const int j = threadIdx.x;
+    const double* tj = S.theta + 7 * (lb + j0 + j);
+    double* out = S.theta_next + 7 * (lb + j0 + j);
+    for (int a = 0; a < 3; ++a) out[a] = tj[a] + eta * dir[j][a];
+    const Q4 qn = normalized(Q4{tj[3] + eta * dir[j][3], tj[4] + eta * dir[j][4], tj[5] + eta * dir[j][5],
+                                tj[6] + eta * dir[j][6]});
+    out[3] = qn.w;
+    out[4] = qn.x;
+    out[5] = qn.y;
+    out[6] = qn.z;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K7: SGD update (optim.cpp:108-114) for non-frozen particles.
 // ---------------------------------------------------------------------------
@@ -800,6 +1025,59 @@ __global__ void bookkeeping_kernel(DevProblem P, DevState S, int stein_phase, in
     S.prev_loss[j] = S.loss[j];
   }
   S.active[j] = (next_stein || !S.converged[j]) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Collision pre-test bounds of one SDF grid, computed at prepare time: the
+// Lipschitz bound lip = max |node difference| / voxel along any axis, vmax =
+// max |value| (both by atomicMax on the bit patterns of non-negative
+// doubles, which order like the values), and the coarse grid: block
+// (bx, by, bz) covers cells [4b, 4b + 4) per axis and holds the max over the
+// nodes [4b - 1, 4b + 5] (dilated by one node).
+// ---------------------------------------------------------------------------
+__global__ void grid_bounds_kernel(Grid* grids, int gi, const float* values, float* coarse) {
+  Grid& g = grids[gi];
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+  const float* v = values + g.values_offset;
+  const int64_t nodes = static_cast<int64_t>(nx) * ny * nz;
+  const int64_t nblocks = static_cast<int64_t>(g.cdims[0]) * g.cdims[1] * g.cdims[2];
+  double lip = 0.0, vmax = 0.0;
+  for (int64_t id = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; id < nodes;
+       id += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int iz = static_cast<int>(id % nz), iy = static_cast<int>((id / nz) % ny),
+              ix = static_cast<int>(id / (static_cast<int64_t>(ny) * nz));
+    const double x = v[id];
+    vmax = fmax(vmax, fabs(x));
+    double d = 0.0;
+    if (ix + 1 < nx) d = fmax(d, fabs(x - static_cast<double>(v[id + static_cast<int64_t>(ny) * nz])));
+    if (iy + 1 < ny) d = fmax(d, fabs(x - static_cast<double>(v[id + nz])));
+    if (iz + 1 < nz) d = fmax(d, fabs(x - static_cast<double>(v[id + 1])));
+    lip = fmax(lip, d / g.voxel);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lip = fmax(lip, __shfl_xor_sync(0xffffffffu, lip, o));
+    vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(reinterpret_cast<unsigned long long*>(&g.lip), static_cast<unsigned long long>(__double_as_longlong(lip)));
+    atomicMax(reinterpret_cast<unsigned long long*>(&g.vmax),
+              static_cast<unsigned long long>(__double_as_longlong(vmax)));
+  }
+  for (int64_t b = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; b < nblocks;
+       b += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int bz = static_cast<int>(b % g.cdims[2]), by = static_cast<int>((b / g.cdims[2]) % g.cdims[1]),
+              bx = static_cast<int>(b / (static_cast<int64_t>(g.cdims[1]) * g.cdims[2]));
+    float m = -INFINITY;
+    for (int ix = max(0, kCoarse * bx - 1); ix <= min(nx - 1, kCoarse * bx + kCoarse + 1); ++ix)
+      for (int iy = max(0, kCoarse * by - 1); iy <= min(ny - 1, kCoarse * by + kCoarse + 1); ++iy)
+        for (int iz = max(0, kCoarse * bz - 1); iz <= min(nz - 1, kCoarse * bz + kCoarse + 1); ++iz)
+          m = fmaxf(m, v[(static_cast<int64_t>(ix) * ny + iy) * nz + iz]);
+    coarse[g.coarse_offset + b] = m;
+  }
+}
+
+void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st) {
+  for (int g = 0; g < n_grids; ++g) grid_bounds_kernel<<<296, 256, 0, st>>>(grids, g, values, coarse);
 }
 
 // ---------------------------------------------------------------------------
@@ -972,9 +1250,15 @@ void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int
                        cudaStream_t st) {
   pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
 }
-int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int big_grid, cudaStream_t st) {
+int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
+                        cudaStream_t st) {
+  static const bool attrs = [] {
+    cudaFuncSetAttribute(median_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmallSmem);
+    return true;
+  }();
+  (void)attrs;
   int n = 3;
-  median_kernel<<<P.n_pop, 1024, 0, st>>>(P, S);
+  median_kernel<<<P.n_pop, 1024, kMedSmallSmem, st>>>(P, S);
   if (big_grid > 0) {
     med_init_kernel<<<P.n_pop, 256, 0, st>>>(P, S);
     const int shifts[6] = {52, 40, 28, 16, 4, 0}, bits[6] = {12, 12, 12, 12, 12, 4};
@@ -985,7 +1269,13 @@ int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_po
     n += 13;
   }
   dim3 grid((max_pop + kSvgdJ - 1) / kSvgdJ, P.n_pop);
-  svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
+  if (S.kmat) {
+    svgd_kmat_kernel<<<dim3(grid.x, (max_gpop + kSvgdJ - 1) / kSvgdJ, P.n_pop), 256, 0, st>>>(P, S);
+    svgd_acc_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
+    ++n;
+  } else {
+    svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
+  }
   copy_theta_kernel<<<(7 * P.J + 255) / 256, 256, 0, st>>>(S.theta, S.theta_next, 7 * P.J);
   return n;
 }

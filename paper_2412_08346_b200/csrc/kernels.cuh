@@ -43,6 +43,7 @@ struct DevProblem {
   // Unsharded: j_lo = 0, gpop_off = pop_off, theta_all = theta.
   const int* gpop_off;      // population -> first global particle (n_pop + 1)
   int j_lo;
+  const long long* kofs;    // population -> offset of its K x K_local block in DevState::kmat (split SVGD)
   double center[3];         // FP32 re-centring origin of the forward match (object centroid)
   double B_obj;             // max |r - center| over R (with slack)
   double com[3];
@@ -59,7 +60,7 @@ struct DevProblem {
 };
 
 // Populations at least this large take the grid-wide median select.
-constexpr int kMedBigK = 2048;
+constexpr int kMedBigK = 320;
 struct MedState {
   unsigned long long prefix, mask;
   long long rank;
@@ -67,6 +68,7 @@ struct MedState {
 
 // Mutable solver state (device pointers).
 struct DevState {
+  double2* kmat;           // split SVGD: (rbf, |q.q|) per (partner, own) pair, or null
   unsigned int* med_hist;  // n_pop x 4096 (grid-wide median select)
   MedState* med_state;     // n_pop
   double* theta;       // J x 7
@@ -105,6 +107,7 @@ struct DevState {
   int* item_count[2];  // J + 1 each
   int* item_off[2];    // J + 1 each
   int* item_counter;   // 2 ints
+  int* nn_dyn;         // device-chosen forward split: [0] splits, [1] forward items
   void* scan_tmp;
   size_t scan_tmp_bytes;
   NnPartial* partials; // padded surface rows x max chunks
@@ -116,6 +119,7 @@ struct DevState {
   int* refine_count;
   int refine_cap;
   unsigned long long* stats;  // [0] windows > 1, [1] full refines, [2] queries, [3] canonical-order ties, [4] pairs
+  unsigned long long* iter_stats;  // per iteration k (k_max = final): [4k + list] pairs, [4k + 2 + list] queries
   double* trace_theta;
   double* trace_loss;
   int* trace_col;
@@ -127,13 +131,14 @@ struct NnPlan {
   int kind;      // 0 iteration match, 2 final ranking
   int pooled;    // forward candidates are the particle's minibatch pool
   int m;         // forward candidate count
-  int nchunks;   // forward candidate chunks (split-K)
-  int chunk;     // candidates per chunk (multiple of kNnTile)
+  int nchunks;   // upper bound on forward candidate splits (split-K); the device picks <= this
+  int target_items;  // forward items the device split aims for (fills the persistent grid)
   int fp64_mode; // resolve every query by FP64 brute force (validation mode)
   int max_ns;    // largest contact surface (merge grid)
   int iter;      // iteration index (diagnostic counters)
 };
 
+void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st);
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st);
 void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);
@@ -146,7 +151,10 @@ void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
 void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st);
 // big_grid > 0: some population has K >= kMedBigK; the grid-wide select runs
 // with big_grid CTAs per population (returns the launch count).
-int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int big_grid, cudaStream_t st);
+// S.kmat != null selects the split SVGD (kmat + accumulate kernels);
+// max_pop / max_gpop: largest local / global population.
+int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
+                        cudaStream_t st);
 // Particle-sharding exchange helpers: pack local rows [theta(7), drift(7)]
 // into `send` (stride 14 doubles), and scatter a gathered world x rows_per_rank
 // block back into global order (rank r's rows start at floor(r * J_glob / world)).

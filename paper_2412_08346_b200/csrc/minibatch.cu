@@ -167,10 +167,12 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P,
   }
   for (int i = tid; i < mt::kN; i += kMbThreads) gst[i] = st[i];
   if (tid == 0) S.rng_mti[j] = s_mti;
-  // Gather the FP32 candidates in sample order (+inf padded to the subtile).
+  // Gather the FP32 candidates in sample order (+inf padded to the subtile),
+  // pair-interleaved like the object cloud (common.cuh pc_*).
   float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
-  for (int i = tid; i < m; i += kMbThreads) pool32[i] = P.obj_cand[pool[i]];
-  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads) pool32[i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+  for (int i = tid; i < m; i += kMbThreads) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
+  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads)
+    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
 }
 
 template <int ITEMS>

@@ -5,11 +5,13 @@
 // replacing the per-call kd-trees of spatial_index.cpp:14-105.
 //
 // FP32 filter, FP64 decision:
-//   * a work item is (particle, <= 1024 queries, a split of the candidates);
-//     the split is consumed in sub-chunks of <= 2048 candidates that are
-//     loaded whole into shared memory by TMA bulk copies (cp.async.bulk +
-//     mbarrier, one 4 KB tile per stage) and read with broadcast LDS.128;
-//   * each thread holds Q queries in registers; one (query, candidate) pair
+//   * forward / final work item: (particle, <= 1024 queries, a split of the
+//     candidates); the number of splits is picked on the device per round
+//     (fwd_split) so that few matching particles still fill the grid; a split
+//     is consumed in sub-chunks of <= 2048 candidates loaded whole into shared
+//     memory by TMA bulk copies (cp.async.bulk + mbarrier, one 4 KB tile per
+//     stage) and read with broadcast LDS.128;
+//   * each thread holds 8 queries in registers; one (query, candidate) pair
 //     is 3 FFMA + 1 FMNMX (the expansion form |b|^2 - 2 a.b), branch-free;
 //   * every 32 candidates (a subtile) each query folds the subtile minimum into
 //     a running top-3 of subtile minima (b1 <= b2 <= b3, subtiles s1, s2);
@@ -17,11 +19,12 @@
 //     (p - q).squaredNorm(), ties to the lowest position (spatial_index.cpp:
 //     69-83) — is provably in {d32 <= b1 + 2E} (2E = the query's margin).  The
 //     subtiles s1 (and s2 when b2 is inside the margin) are rescanned from
-//     shared memory for the position of b1 and the window count; b3 inside the
-//     margin or a window of two or more makes the query "ambiguous";
-//   * the running (best value, position, ambiguous) state carries across
-//     sub-chunks and splits; an unambiguous query is certified, an ambiguous
-//     one is decided by a full FP64 rescan with the reference formula.
+//     shared memory for the position of b1 and the window members;
+//   * the running (best value, position) state carries across sub-chunks; a
+//     window of one is certified, larger windows keep their members in a
+//     pooled list and are decided in FP64 with the reference formula (after
+//     the split merge); overflowing windows take a full FP64 rescan;
+//   * reverse match: warp items (nn_rev_kernel, below).
 #include "common.cuh"
 
 #include <cub/device/device_scan.cuh>
@@ -32,23 +35,34 @@
 namespace asicp {
 
 constexpr int kFwdQ = 8;                     // forward / final: 8 queries per thread
-constexpr int kRevQ = 2;                     // reverse (few colliding points): 2
 constexpr int kFwdQB = kNnThreads * kFwdQ;   // queries per forward item
-constexpr int kRevQB = kNnThreads * kRevQ;   // queries per reverse item
 constexpr int kNnSmem = kNnStages * kNnTile * 16;
+constexpr int kMinChunk = 2 * kNnTile;       // smallest candidate split
 
 // ---------------------------------------------------------------------------
-// Work planning: per particle item counts -> exclusive scans -> item lists.
+// Work planning: per particle counts -> exclusive scans -> item lists.
+// Forward: count = query blocks; the split factor is chosen on the device
+// from the total T so that T x splits ~ plan.target_items (few matching
+// particles -> many splits per particle), capped by plan.nchunks and by
+// kMinChunk candidates per split.  Reverse: warp items of kRevWQ points.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_out, int* chunk_out) {
+  int nch = T > 0 ? min(plan.nchunks, max(1, ceil_div(plan.target_items, T))) : 1;
+  nch = max(1, min(nch, plan.m / kMinChunk));
+  const int chunk = round_up(ceil_div(plan.m, nch), kNnTile);
+  *chunk_out = chunk;
+  *nch_out = ceil_div(plan.m, chunk);
+}
+
 __global__ void nn_count_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j > P.J) return;
   int fwd = 0, rev = 0;
   if (j < P.J && (plan.kind == 2 || S.active[j])) {
     if (plan.kind != 2 && S.n_col[j] > 0)
-      rev = ceil_div(S.n_col[j], kRevQB);
+      rev = ceil_div(S.n_col[j], kRevWQ);
     else
-      fwd = ceil_div(surf_count(P, j), kFwdQB) * plan.nchunks;
+      fwd = ceil_div(surf_count(P, j), kFwdQB);
   }
   S.item_count[0][j] = fwd;
   S.item_count[1][j] = rev;
@@ -57,6 +71,13 @@ __global__ void nn_count_kernel(DevProblem P, DevState S, NnPlan plan) {
 __global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
+  int nch, chunk;
+  const int T = S.item_off[0][P.J];
+  fwd_split(T, plan, &nch, &chunk);
+  if (j == 0) {
+    S.nn_dyn[0] = nch;
+    S.nn_dyn[1] = T * nch;
+  }
   const int64_t so = P.part_surf_off[j];
   const int ns = surf_count(P, j);
   if (S.item_count[1][j] > 0) {
@@ -65,37 +86,39 @@ __global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
     int w = S.item_off[1][j];
     for (int b = 0; b < S.item_count[1][j]; ++b) {
       NnItem it;
-      it.q = S.col_q + row + b * kRevQB;
-      it.nq = min(kRevQB, nq - b * kRevQB);
+      it.q = S.col_q + row + b * kRevWQ;
+      it.nq = min(kRevWQ, nq - b * kRevWQ);
       it.c = S.Sc32 + so;
       it.nc = ns;
       it.c_base = 0;
       it.kind = 1;
       it.owner = j;
-      it.q_first = b * kRevQB;
+      it.q_first = b * kRevWQ;
       it.chunk = 0;
       it.nchunks = 1;
+      it.slot = 0;
       S.items[1][w++] = it;
     }
   }
   if (S.item_count[0][j] > 0) {
     const float4* cands = plan.pooled ? S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad : P.obj_cand;
-    int w = S.item_off[0][j];
-    for (int b = 0; b < ceil_div(ns, kFwdQB); ++b)
-      for (int s = 0; s < plan.nchunks; ++s) {
+    const int qb0 = S.item_off[0][j];
+    for (int b = 0; b < S.item_count[0][j]; ++b)
+      for (int s = 0; s < nch; ++s) {
         NnItem it;
         it.q = S.Sq32 + so + b * kFwdQB;
         it.nq = min(kFwdQB, ns - b * kFwdQB);
-        const int c0 = s * plan.chunk;
+        const int c0 = s * chunk;
         it.c = cands + c0;
-        it.nc = min(plan.chunk, plan.m - c0);
+        it.nc = min(chunk, plan.m - c0);
         it.c_base = c0;
         it.kind = plan.kind;
         it.owner = j;
         it.q_first = b * kFwdQB;
         it.chunk = s;
-        it.nchunks = plan.nchunks;
-        S.items[0][w++] = it;
+        it.nchunks = nch;
+        it.slot = qb0 + b;
+        S.items[0][(qb0 + b) * nch + s] = it;
       }
   }
 }
@@ -240,12 +263,39 @@ __device__ __forceinline__ float d32(float qx, float qy, float qz, float4 v) {
   return __fmaf_rn(qx, v.x, __fmaf_rn(qy, v.y, __fmaf_rn(qz, v.z, v.w)));
 }
 
+// Packed FP32 pairs (sm_100 FFMA2): two queries share one instruction; a
+// scalar candidate operand is broadcast to both lanes (ptxas folds the
+// {v, v} pair into a .F32 broadcast operand).  Each lane is an IEEE fma, so
+// the values equal d32() bit for bit.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float half2f(f32x2 v, int k) {
+  float lo, hi;
+  up2(v, lo, hi);
+  return (k & 1) ? hi : lo;
+}
+
 // ---------------------------------------------------------------------------
 // The filter kernel (persistent over one work list).
 // ---------------------------------------------------------------------------
+// 4 CTAs (16 warps) per SM: with the packed FFMA2 main loop the kernel fits
+// 128 registers without spilling, and the extra warps hide the FFMA2 / LDS
+// latencies that stall a 2-CTA configuration.
 template <int Q>
 #ifndef ASICP_NN_MINBLOCKS
-#define ASICP_NN_MINBLOCKS 1
+#define ASICP_NN_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
     nn_filter_kernel(DevProblem P, DevState S, NnPlan plan, int list) {
@@ -262,7 +312,7 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int n_items = S.item_off[list][P.J];
+  const int n_items = list == 0 ? S.nn_dyn[1] : S.item_off[list][P.J];
   const NnItem* items = S.items[list];
   uint32_t phases = 0;  // bit s: parity of the next completion of stage s
   for (;;) {
@@ -277,6 +327,9 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
       atomicAdd(S.stats + 4, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
       if (list == 0)
         atomicAdd(S.stats + 12, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
+      unsigned long long* is = S.iter_stats + 4 * plan.iter + list;
+      atomicAdd(is, static_cast<unsigned long long>(w.nq) * static_cast<unsigned long long>(w.nc));
+      if (w.chunk == 0) atomicAdd(is + 2, static_cast<unsigned long long>(w.nq));
     }
     // Running state lives in shared memory (touched once per sub-chunk), which
     // keeps the hot loop's register footprint down.
@@ -322,31 +375,41 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
           float tm[Q];
 #pragma unroll
           for (int k = 0; k < Q; ++k) tm[k] = INFINITY;
-          // Two candidates per step, each FMA stage issued across all Q
-          // queries before the next, so 2Q independent chains are in flight
-          // (same arithmetic as d32(): fma(qx,vx, fma(qy,vy, fma(qz,vz, w)))).
-#pragma unroll 4
-          for (int c = 0; c < kSub; c += 2) {
-            const float4 v0 = sp[c];
-            const float4 v1 = sp[c + 1];
-            float d0[Q], d1[Q];
+          // Candidates are pair-interleaved (pc_index): one LDS.128 gives the
+          // (x0, x1, y0, y1) pairs, the next (z0, z1, w0, w1).  Each packed
+          // FFMA2 evaluates two candidates for one query (query coordinate
+          // broadcast); per lane the arithmetic is d32():
+          // fma(qx,vx, fma(qy,vy, fma(qz,vz, w))).  Four candidates per step,
+          // each FMA stage issued across all Q queries before the next.
+#pragma unroll 2
+          for (int c = 0; c < kSub; c += 4) {
+            const float4 a0 = sp[c], c0 = sp[c + 1];  // candidates c, c+1
+            const float4 a1 = sp[c + 2], c1 = sp[c + 3];  // candidates c+2, c+3
+            const f32x2 x0 = pk2(a0.x, a0.y), y0 = pk2(a0.z, a0.w), z0 = pk2(c0.x, c0.y), w0 = pk2(c0.z, c0.w);
+            const f32x2 x1 = pk2(a1.x, a1.y), y1 = pk2(a1.z, a1.w), z1 = pk2(c1.x, c1.y), w1 = pk2(c1.z, c1.w);
+            f32x2 d0[Q], d1[Q];
 #pragma unroll
             for (int k = 0; k < Q; ++k) {
-              d0[k] = __fmaf_rn(qz[k], v0.z, v0.w);
-              d1[k] = __fmaf_rn(qz[k], v1.z, v1.w);
+              d0[k] = ffma2(z0, pk2(qz[k], qz[k]), w0);
+              d1[k] = ffma2(z1, pk2(qz[k], qz[k]), w1);
             }
 #pragma unroll
             for (int k = 0; k < Q; ++k) {
-              d0[k] = __fmaf_rn(qy[k], v0.y, d0[k]);
-              d1[k] = __fmaf_rn(qy[k], v1.y, d1[k]);
+              d0[k] = ffma2(y0, pk2(qy[k], qy[k]), d0[k]);
+              d1[k] = ffma2(y1, pk2(qy[k], qy[k]), d1[k]);
             }
 #pragma unroll
             for (int k = 0; k < Q; ++k) {
-              d0[k] = __fmaf_rn(qx[k], v0.x, d0[k]);
-              d1[k] = __fmaf_rn(qx[k], v1.x, d1[k]);
+              d0[k] = ffma2(x0, pk2(qx[k], qx[k]), d0[k]);
+              d1[k] = ffma2(x1, pk2(qx[k], qx[k]), d1[k]);
             }
 #pragma unroll
-            for (int k = 0; k < Q; ++k) tm[k] = fminf(tm[k], fminf(d0[k], d1[k]));
+            for (int k = 0; k < Q; ++k) {
+              float l0, h0, l1, h1;
+              up2(d0[k], l0, h0);
+              up2(d1[k], l1, h1);
+              tm[k] = fminf(fminf(tm[k], fminf(l0, h0)), fminf(l1, h1));
+            }
           }
           const int sid = t * (kNnTile / kSub) + sub;
 #pragma unroll
@@ -379,7 +442,7 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
           const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
           const float4* sp = tiles + sid * kSub;
           for (int c = 0; c < kSub; ++c) {
-            const float d = d32(qx[k], qy[k], qz[k], sp[c]);
+            const float d = d32(qx[k], qy[k], qz[k], pc_get(sp, c));
             if (d <= thr) {
               const int p = base + sid * kSub + c;
               if (np < kWinCap) {
@@ -458,11 +521,10 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
           }
         }
       } else {
-        const int64_t rows = P.part_surf_off[P.J];
         NnPartial pr;
         pr.b1 = B1(k);
         pr.pos = p1;
-        S.partials[static_cast<int64_t>(w.chunk) * rows + P.part_surf_off[w.owner] + qlocal] = pr;
+        S.partials[(static_cast<int64_t>(w.slot) * w.nchunks + w.chunk) * kFwdQB + qi] = pr;
       }
     }
   }
@@ -473,16 +535,19 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
 // split was itself unambiguous.
 __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
   const int j = blockIdx.y;
+  const int nch = S.nn_dyn[0];
+  if (nch <= 1) return;  // single split: the filter emitted directly
   if (plan.kind != 2 && (!S.active[j] || S.n_col[j] > 0)) return;
   const int64_t so = P.part_surf_off[j];
   const int ns = surf_count(P, j);
   const int qlocal = blockIdx.x * blockDim.x + threadIdx.x;
   if (qlocal >= ns) return;
-  const int64_t rows = P.part_surf_off[P.J];
+  const NnPartial* parts =
+      S.partials + static_cast<int64_t>(S.item_off[0][j] + qlocal / kFwdQB) * nch * kFwdQB + qlocal % kFwdQB;
   float b1 = INFINITY;
   int best = 0;
-  for (int s = 0; s < plan.nchunks; ++s) {
-    const NnPartial p = S.partials[s * rows + so + qlocal];
+  for (int s = 0; s < nch; ++s) {
+    const NnPartial p = parts[s * kFwdQB];
     if (p.b1 < b1) {
       b1 = p.b1;
       best = p.pos;
@@ -494,7 +559,7 @@ __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
   }
   const float thr = __fadd_ru(b1, S.Sq32[so + qlocal].w);
   int reach = 0;
-  for (int s = 0; s < plan.nchunks; ++s) reach += S.partials[s * rows + so + qlocal].b1 <= thr ? 1 : 0;
+  for (int s = 0; s < nch; ++s) reach += parts[s * kFwdQB].b1 <= thr ? 1 : 0;
   if (reach == 1 && !(best & kAmbiguous)) {
     S.res_fwd[so + qlocal] = best;  // certified
     return;
@@ -504,8 +569,8 @@ __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
   int pos[kMax];
   int n = 0;
   bool ok = true;
-  for (int s = 0; s < plan.nchunks && ok; ++s) {
-    const NnPartial p = S.partials[s * rows + so + qlocal];
+  for (int s = 0; s < nch && ok; ++s) {
+    const NnPartial p = parts[s * kFwdQB];
     if (p.b1 > thr) continue;
     int m = 0;
     ok = win_collect(S, p.pos, thr, pos + n, &m, kMax - n) && ok;
@@ -554,6 +619,115 @@ __global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
 }
 
 // ---------------------------------------------------------------------------
+// Reverse match (collision_loss_and_gradients, grasp.cpp:68-84): each
+// colliding scene point against the particle's transformed contact surface.
+// Colliding points are few per particle (tens to hundreds), so work items are
+// per WARP: <= 32 points of one particle, one per lane, against the particle's
+// <= ~1k candidates read through L1 (broadcast loads).  Same filter and
+// certification as nn_filter_kernel with a single split: the window members
+// are listed on the spot and decided in FP64 at once.
+// ---------------------------------------------------------------------------
+constexpr int kRevWarps = 4;
+constexpr int kRevThreads = 32 * kRevWarps;
+constexpr int kRevMaxC = 1024;  // candidates staged per warp (16 KB); larger surfaces read L1
+constexpr int kRevSmem = kRevWarps * kRevMaxC * 16;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevState S, NnPlan plan) {
+  extern __shared__ __align__(16) float4 rev_smem[];
+  const int lane = threadIdx.x & 31;
+  float4* stage = rev_smem + (threadIdx.x >> 5) * kRevMaxC;
+  const int n_items = S.item_off[1][P.J];
+  // Items cost about the same (<= 32 points x one contact surface): a static
+  // warp-stride assignment, no shared counter for thousands of warps to hit.
+  // The item's candidates are staged into the warp's shared slice with one
+  // round of cp.async (every load in flight at once) before the scan.
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += nwarps) {
+    const NnItem w = S.items[1][it];
+    const int ncp = round_up(w.nc, kSub);
+    const bool staged = ncp <= kRevMaxC;
+    __syncwarp();  // the previous item's rescans are done with the slice
+    if (staged) {
+      for (int c = lane; c < ncp; c += 32) cp_async16(stage + c, w.c + c);
+      cp_async_wait_all();
+      __syncwarp();
+    }
+    const float4* cand = staged ? stage : w.c;
+    if (lane == 0) {
+      const unsigned long long pairs = static_cast<unsigned long long>(w.nq) * w.nc;
+      atomicAdd(S.stats + 2, static_cast<unsigned long long>(w.nq));
+      atomicAdd(S.stats + 4, pairs);
+      atomicAdd(S.iter_stats + 4 * plan.iter + 1, pairs);
+      atomicAdd(S.iter_stats + 4 * plan.iter + 3, static_cast<unsigned long long>(w.nq));
+    }
+    const bool has = lane < w.nq;
+    const float4 q = has ? w.q[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nsub = ceil_div(w.nc, kSub);  // candidate rows are +inf padded to the subtile
+    float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
+    int s1 = 0, s2 = 0;
+    for (int sub = 0; sub < nsub; ++sub) {
+      const float4* sp = cand + sub * kSub;
+      float t0 = INFINITY, t1 = INFINITY, t2 = INFINITY, t3 = INFINITY;
+#pragma unroll
+      for (int c = 0; c < kSub; c += 4) {
+        const float4 v0 = sp[c], v1 = sp[c + 1], v2 = sp[c + 2], v3 = sp[c + 3];
+        t0 = fminf(t0, __fmaf_rn(q.x, v0.x, __fmaf_rn(q.y, v0.y, __fmaf_rn(q.z, v0.z, v0.w))));
+        t1 = fminf(t1, __fmaf_rn(q.x, v1.x, __fmaf_rn(q.y, v1.y, __fmaf_rn(q.z, v1.z, v1.w))));
+        t2 = fminf(t2, __fmaf_rn(q.x, v2.x, __fmaf_rn(q.y, v2.y, __fmaf_rn(q.z, v2.z, v2.w))));
+        t3 = fminf(t3, __fmaf_rn(q.x, v3.x, __fmaf_rn(q.y, v3.y, __fmaf_rn(q.z, v3.z, v3.w))));
+      }
+      const float tm = fminf(fminf(t0, t1), fminf(t2, t3));
+      // Running top-3 of subtile minima (strict < keeps the earliest).
+      const bool lt1 = tm < b1, lt2 = tm < b2;
+      b3 = lt2 ? b2 : fminf(b3, tm);
+      s2 = lt1 ? s1 : (lt2 ? sub : s2);
+      b2 = lt1 ? b1 : (lt2 ? tm : b2);
+      s1 = lt1 ? sub : s1;
+      b1 = lt1 ? tm : b1;
+    }
+    if (!has) continue;
+    const int qlocal = w.q_first + lane;
+    int* slot = S.res_rev + static_cast<int64_t>(w.owner) * P.n_scene + qlocal;
+    if (plan.fp64_mode) {
+      push_refine(S, 1, w.owner, qlocal, 0, plan.iter);
+      continue;
+    }
+    const float thr = __fadd_ru(b1, q.w);
+    bool ovf = b3 <= thr;
+    int pos[kWinCap];
+    int np = 0, pmin = -1;
+    const int nscan = b2 <= thr ? 2 : 1;
+    for (int r = 0; r < nscan; ++r) {
+      const int sid = r == 0 ? s1 : s2;
+      const float4* sp = cand + sid * kSub;
+      for (int c = 0; c < kSub; ++c) {
+        const float d = d32(q.x, q.y, q.z, sp[c]);
+        if (d <= thr) {
+          const int p = sid * kSub + c;
+          if (np < kWinCap) pos[np] = p;
+          ++np;
+          if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
+        }
+      }
+    }
+    ovf = ovf || np > kWinCap;
+    if (ovf) {
+      push_refine(S, 1, w.owner, qlocal, 1, plan.iter);
+    } else if (np == 1) {
+      *slot = pmin;  // certified
+    } else {
+      const NnGeom g = nn_geom(P, S, plan, 1, w.owner, qlocal);
+      *slot = nn_decide(g, pos, np, false, S.stats);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
@@ -578,7 +752,7 @@ int nn_smem_bytes() { return kNnSmem; }
 
 void nn_set_attrs() {
   cudaFuncSetAttribute(nn_filter_kernel<kFwdQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
-  cudaFuncSetAttribute(nn_filter_kernel<kRevQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
+  cudaFuncSetAttribute(nn_rev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRevSmem);
 }
 
 int nn_blocks_per_sm() {
@@ -595,7 +769,7 @@ int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, in
   ++n;
   if (ev_end) cudaEventRecord(ev_end, st);
   if (plan.kind == 0) {
-    nn_filter_kernel<kRevQ><<<grid, kNnThreads, kNnSmem, st>>>(P, S, plan, 1);
+    nn_rev_kernel<<<3 * refine_grid / 2, kRevThreads, kRevSmem, st>>>(P, S, plan);  // 3 CTAs per SM
     ++n;
   }
   if (plan.nchunks > 1) {

@@ -3,21 +3,20 @@
 // collision_loss_and_gradients grasp.cpp:68-84 / final ranking
 // grasp.cpp:263-281, replacing the kd-tree of spatial_index.cpp:14-105).
 //
-// FP32 filter, FP64 decision:
-//   * candidates are staged tile by tile into shared memory with TMA bulk
-//     copies (cp.async.bulk + mbarrier, 4-stage ring); every thread reads each
-//     candidate with one broadcast LDS.128;
-//   * each thread owns Q queries in registers; a (query, candidate) pair costs
-//     3 FFMA in the expansion form d = |b|^2 - 2 a.b (a, b re-centred at the
-//     object centroid) plus one FSETP against the query's running threshold;
-//   * the threshold is b1 + margin, where margin = 2E bounds the FP32 error of
-//     d (see DESIGN.md §NN certification); every candidate within the margin of
-//     the running minimum is kept in a per-query window list (shared memory);
+// FP32 filter, FP64 decision (nn.cu):
+//   * forward / final: CTA work items (particle, <= 1024 queries, candidate
+//     split); the split is staged whole into shared memory by TMA bulk copies
+//     and read with broadcast LDS.128; the number of splits adapts on the
+//     device to the number of particles that match in the iteration;
+//   * reverse: warp work items (particle, <= 32 colliding points) against the
+//     particle's contact surface read through L1;
+//   * a (query, candidate) pair is 3 FFMA in the expansion form
+//     d = |b|^2 - 2 a.b plus a min; each query keeps a running top-3 of
+//     32-candidate subtile minima;
 //   * the reference's answer (min FP64 (p - q).squaredNorm(), ties -> lowest
-//     position, spatial_index.cpp:70,83) is provably inside that window, so a
-//     window of one is certified and larger windows are decided in FP64 with
-//     the reference formula.  Overflowing windows fall back to a full FP64
-//     rescan.
+//     position, spatial_index.cpp:70,83) provably lies in {d <= b1 + margin};
+//     a window of one is certified, larger windows are decided in FP64 with
+//     the reference formula, overflowing windows by a full FP64 rescan.
 #pragma once
 
 #include <cstdint>
@@ -31,6 +30,7 @@ constexpr int kNnTile = 256;                    // candidates per TMA tile (4 KB
 constexpr int kNnStages = 8;                    // whole chunk resident: rescans read shared memory
 constexpr int kNnMaxChunk = kNnStages * kNnTile; // candidates per work item (2048, 32 KB)
 constexpr int kNnL = 4;                         // window list entries per query
+constexpr int kRevWQ = 32;                      // reverse: queries per warp item
 
 // One NN work item: a block of <= kNnQB queries against a contiguous
 // candidate chunk.
@@ -45,6 +45,7 @@ struct NnItem {
   int q_first;       // index of q[0] in the kind's query numbering
   int chunk;         // chunk index (0..S-1)
   int nchunks;       // S
+  int slot;          // forward: global query-block index (partials are [slot][chunk][query])
 };
 
 // Per (query, split) partial result: the split's best FP32 value and its

@@ -124,15 +124,15 @@ struct asicp_ctx {
   std::vector<int> part_pre;
   std::vector<double> init_theta;
   uint64_t seed = 0;
-  int nchunks_max = 1;
+  int target_items = 0;
 
   // Particle sharding within populations (asicp_set_partition_*): this ctx
   // owns global particles [j_lo, j_lo + J) of J_glob; rows_per_rank pads the
   // allgather blocks to equal size.  Unsharded: xchg null, J_glob = J.
   std::unique_ptr<asicp::Exchange> xchg;
   int J_glob = 0, j_lo = 0, rows_per_rank = 0, final_stride = 0;
-  Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d, med_hist, med_state;
-  int med_big_grid = 0;
+  Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d, med_hist, med_state, kofs_d, kmat;
+  int med_big_grid = 0, max_gpop = 0;
   double* host_gath = nullptr;
   size_t host_gath_bytes = 0;
 
@@ -146,7 +146,7 @@ struct asicp_ctx {
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
       item_count, item_off, item_counter, scan_tmp, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
-      stats, trace_theta,
+      stats, iter_stats, trace_theta,
       trace_loss, trace_col,
       final_loss, final_free;
 
@@ -207,7 +207,8 @@ struct asicp_ctx {
     free_staging();
     if (host_gath) cudaFreeHost(host_gath);
     xchg.reset();
-    Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend, &xrecv, &fsend, &frecv, &gpop_off_d, &med_hist, &med_state};
+    Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend,    &xrecv,  &fsend, &frecv,
+                         &gpop_off_d, &med_hist, &med_state, &kofs_d, &kmat};
     for (Buf* b : shard_bufs) b->release();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     for (auto& e : nn_events) {
@@ -223,7 +224,7 @@ struct asicp_ctx {
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
                   &item_counter, &scan_tmp,
-                  &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &trace_theta,
+                  &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &iter_stats, &trace_theta,
                   &trace_loss, &trace_col,
                   &final_loss, &final_free};
     for (Buf* b : all) b->release();
@@ -314,17 +315,27 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   for (int64_t i = 0; i < p.n_object; ++i)
     for (int a = 0; a < 3; ++a) center[a] += obj[3 * i + a];
   for (int a = 0; a < 3; ++a) center[a] /= static_cast<double>(p.n_object);
-  // Candidate rows are padded to the NN subtile with +inf (never selected).
+  // Candidate rows are padded to the NN subtile with +inf (never selected) and
+  // stored pair-interleaved (common.cuh pc_index).
   c->n_obj_pad = static_cast<int>((p.n_object + kSubRows - 1) / kSubRows * kSubRows);
-  std::vector<float4> cand(c->n_obj_pad, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
+  std::vector<float4> cand(c->n_obj_pad, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+  float* cf = reinterpret_cast<float*>(cand.data());
+  auto put = [&](int64_t i, float x, float y, float z, float w) {
+    float* f = cf + pc_index(i);
+    f[0] = x;
+    f[2] = y;
+    f[4] = z;
+    f[6] = w;
+  };
   double bmax = 0.0;
   for (int64_t i = 0; i < p.n_object; ++i) {
     const double bx = obj[3 * i] - center[0], by = obj[3 * i + 1] - center[1], bz = obj[3 * i + 2] - center[2];
     const float fx = static_cast<float>(bx), fy = static_cast<float>(by), fz = static_cast<float>(bz);
     const double dx = fx, dy = fy, dz = fz;
-    cand[i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, static_cast<float>(dx * dx + dy * dy + dz * dz));
+    put(i, -2.0f * fx, -2.0f * fy, -2.0f * fz, static_cast<float>(dx * dx + dy * dy + dz * dz));
     bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
   }
+  for (int64_t i = p.n_object; i < c->n_obj_pad; ++i) put(i, 0.0f, 0.0f, 0.0f, INFINITY);
   upload(c->obj64, obj.data(), obj.size(), st);
   upload(c->obj_cand, cand.data(), cand.size(), st);
   upload(c->scene64, p.scene_cloud, 3 * p.n_scene, st);
@@ -358,7 +369,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
 
   // SDF grids.
   std::vector<Grid> grids(p.n_sdf_grids);
-  std::vector<float> values, coarse;
+  std::vector<float> values;
+  int64_t coarse_total = 0;
   for (int64_t g = 0; g < p.n_sdf_grids; ++g) {
     const asicp_sdf_grid& s = p.sdf_grids[g];
     Grid& d = grids[g];
@@ -372,41 +384,19 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     d.values_offset = static_cast<int64_t>(values.size());
     const size_t total = static_cast<size_t>(s.dims[0]) * s.dims[1] * s.dims[2];
     values.insert(values.end(), s.values, s.values + total);
-    // Bounds for the collision kernel's FP32 pre-test.
-    double vmax = 0.0, dmax = 0.0;
-    const int nx = s.dims[0], ny = s.dims[1], nz = s.dims[2];
-    for (int ix = 0; ix < nx; ++ix)
-      for (int iy = 0; iy < ny; ++iy)
-        for (int iz = 0; iz < nz; ++iz) {
-          const size_t id = (static_cast<size_t>(ix) * ny + iy) * nz + iz;
-          const double v = s.values[id];
-          vmax = std::max(vmax, std::abs(v));
-          if (ix + 1 < nx) dmax = std::max(dmax, std::abs(v - s.values[id + static_cast<size_t>(ny) * nz]));
-          if (iy + 1 < ny) dmax = std::max(dmax, std::abs(v - s.values[id + nz]));
-          if (iz + 1 < nz) dmax = std::max(dmax, std::abs(v - s.values[id + 1]));
-        }
-    d.lip = dmax / s.voxel;
-    d.vmax = vmax;
-    // Coarse max grid: block b covers cells [4b, 4b+4) per axis; its value is
-    // the max over nodes [4b-1, 4b+5] (dilated by one node), so it bounds the
-    // trilinear value of any point whose cell is within one of the block.
+    // Bounds of the collision kernel's FP32 pre-test (lip, vmax and the
+    // dilated 4^3-block maxima) are computed on the device below.
+    d.lip = 0.0;
+    d.vmax = 0.0;
     for (int a = 0; a < 3; ++a) d.cdims[a] = (s.dims[a] - 1 + kCoarse - 1) / kCoarse;
-    d.coarse_offset = static_cast<int64_t>(coarse.size());
-    for (int bx = 0; bx < d.cdims[0]; ++bx)
-      for (int by = 0; by < d.cdims[1]; ++by)
-        for (int bz = 0; bz < d.cdims[2]; ++bz) {
-          float m = -INFINITY;
-          for (int ix = std::max(0, kCoarse * bx - 1); ix <= std::min(nx - 1, kCoarse * bx + kCoarse + 1); ++ix)
-            for (int iy = std::max(0, kCoarse * by - 1); iy <= std::min(ny - 1, kCoarse * by + kCoarse + 1); ++iy)
-              for (int iz = std::max(0, kCoarse * bz - 1); iz <= std::min(nz - 1, kCoarse * bz + kCoarse + 1);
-                   ++iz)
-                m = std::max(m, s.values[(static_cast<size_t>(ix) * ny + iy) * nz + iz]);
-          coarse.push_back(m);
-        }
+    d.coarse_offset = coarse_total;
+    coarse_total += static_cast<int64_t>(d.cdims[0]) * d.cdims[1] * d.cdims[2];
   }
   upload(c->grids, grids.data(), grids.size(), st);
   upload(c->sdf_values, values.data(), values.size(), st);
-  upload(c->sdf_coarse, coarse.data(), coarse.size(), st);
+  c->sdf_coarse.ensure(static_cast<size_t>(std::max<int64_t>(coarse_total, 1)) * sizeof(float));
+  launch_grid_bounds(c->grids.as<Grid>(), static_cast<int>(p.n_sdf_grids), c->sdf_values.as<float>(),
+                     c->sdf_coarse.as<float>(), st);
   c->max_coarse = 0;
   for (const Grid& g : grids)
     c->max_coarse = std::max(c->max_coarse, g.cdims[0] * g.cdims[1] * g.cdims[2]);
@@ -460,6 +450,19 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c->part_pop, part_pop.data(), part_pop.size(), st);
   upload(c->pop_off, pop_off.data(), pop_off.size(), st);
   upload(c->gpop_off_d, gpop_off.data(), gpop_off.size(), st);
+  // Split SVGD (kernel matrix, then ordered sums) while the K x K_local
+  // matrices stay under 8 M pairs (128 MB); the fused kernel otherwise.
+  std::vector<long long> kofs(n_pre, 0);
+  long long ktot = 0;
+  c->max_gpop = 0;
+  for (int i = 0; i < n_pre; ++i) {
+    kofs[i] = ktot;
+    ktot += static_cast<long long>(p.init_counts[i]) * (pop_off[i + 1] - pop_off[i]);
+    c->max_gpop = std::max(c->max_gpop, static_cast<int>(p.init_counts[i]));
+  }
+  const bool svgd_split = c->k_stein > 0 && ktot > 0 && ktot <= (8ll << 20);
+  if (svgd_split) c->kmat.ensure(static_cast<size_t>(ktot) * sizeof(double2));
+  upload(c->kofs_d, kofs.data(), kofs.size(), st);
   upload(c->pop_logk1, logk1.data(), logk1.size(), st);
   // Median-select key cache: one slice of K(K-1)/2 keys per population when
   // the total stays modest (otherwise the select recomputes keys per pass).
@@ -501,12 +504,14 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     c->gammas[k] = k < c->k_stein ? annealing(k, p.anneal_period_total, p.anneal_cycles, p.anneal_exponent) : 0.0;
   }
 
-  // Split-K factor for the forward match: enough work items to fill the
-  // persistent grid several times over.
+  // Forward work: base_items query blocks; the device splits the candidates
+  // so that (query blocks of the particles matching) x splits ~ target_items,
+  // i.e. the persistent grid gets several items per CTA in every iteration.
   int base_items = 0;
   for (int i = 0; i < n_pre; ++i)
     base_items += static_cast<int>(p.init_counts[i] * ((p.preshapes[i].n_surface + kNnQB - 1) / kNnQB));
-  c->nchunks_max = std::clamp((4 * c->nn_grid + base_items - 1) / std::max(base_items, 1), 1, c->max_chunks);
+  c->target_items = 4 * c->nn_grid;
+  const size_t fwd_slots = static_cast<size_t>(base_items) + c->target_items;  // >= T x splits
 
   // State buffers.
   const size_t Jz = static_cast<size_t>(J);
@@ -547,19 +552,20 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   const bool fy_par_on = (fy_par_bytes <= c->fy_par.bytes || fy_par_bytes <= free_b / 4) &&
                          c->n_obj <= 12 * 1024 * 4;
   if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
-  // Work items: forward <= base_items * nchunks; reverse <= J * ceil(n_scene / 256).
-  c->items0.ensure((static_cast<size_t>(base_items) * c->nchunks_max + Jz) * sizeof(NnItem));
-  c->items1.ensure((Jz * ((c->n_scene + 255) / 256) + Jz) * sizeof(NnItem));
+  // Work items: forward < base_items + target_items (T x splits, see
+  // fwd_split); reverse <= sum ceil(n_col / 32) <= J * ceil(n_scene / 32).
+  c->items0.ensure((fwd_slots + Jz) * sizeof(NnItem));
+  c->items1.ensure((Jz * ((c->n_scene + kRevWQ - 1) / kRevWQ) + Jz) * sizeof(NnItem));
   c->item_count.ensure(2 * (Jz + 1) * 4);
   c->item_off.ensure(2 * (Jz + 1) * 4);
-  c->item_counter.ensure(2 * 4);
+  c->item_counter.ensure(4 * 4);  // [0..1] item counters, [2..3] device split (nn_dyn)
   c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
-  c->partials.ensure(static_cast<size_t>(so) * c->nchunks_max * sizeof(NnPartial));
+  c->partials.ensure(fwd_slots * kNnQB * sizeof(NnPartial));
   // Ambiguous windows are rare (~0.3 % of queries); the pool covers 1/16 of all
-  // (row, split) slots with a 64 k floor, and an exhausted pool only means a
+  // (query, split) slots with a 64 k floor, and an exhausted pool only means a
   // full FP64 rescan for the affected queries.
-  const int amb_cap = static_cast<int>(std::min<size_t>(
-      std::max<size_t>(65536, (static_cast<size_t>(so) * c->nchunks_max + Jz * c->n_scene) / 16), 1u << 24));
+  const int amb_cap = static_cast<int>(
+      std::min<size_t>(std::max<size_t>(65536, fwd_slots * kNnQB / 16), 1u << 24));
   c->amb_pool.ensure(static_cast<size_t>(amb_cap) * kWinCap * sizeof(int2));
   c->amb_n.ensure(static_cast<size_t>(amb_cap) * sizeof(int));
   c->amb_count.ensure(sizeof(int));
@@ -567,6 +573,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->refine_list.ensure(refine_cap * sizeof(int4));
   c->refine_count.ensure(4);
   c->stats.ensure(kStats * sizeof(unsigned long long));
+  c->iter_stats.ensure(4 * static_cast<size_t>(c->k_max + 1) * sizeof(unsigned long long));
   if (c->record_trace) {
     const size_t rows = static_cast<size_t>(c->k_max) * Jz;
     c->trace_theta.ensure(std::max<size_t>(rows, 1) * 7 * 8);
@@ -616,6 +623,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.med_off = c->med_off_d.as<long long>();
   P.gpop_off = c->gpop_off_d.as<int>();
   P.j_lo = lo;
+  P.kofs = c->kofs_d.as<long long>();
   for (int a = 0; a < 3; ++a) {
     P.center[a] = center[a];
     P.com[a] = p.com[a];
@@ -649,6 +657,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.theta_all = c->xchg ? c->theta_all.as<double>() : S.theta;
   S.drift_all = c->xchg ? c->drift_all.as<double>() : S.drift;
   S.h = c->h.as<double>();
+  S.kmat = svgd_split ? c->kmat.as<double2>() : nullptr;
   S.med_hist = c->med_hist.as<unsigned int>();
   S.med_state = c->med_state.as<MedState>();
   S.med_keys = med_cached ? c->med_keys.as<unsigned long long>() : nullptr;
@@ -676,6 +685,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.item_off[0] = c->item_off.as<int>();
   S.item_off[1] = c->item_off.as<int>() + (Jz + 1);
   S.item_counter = c->item_counter.as<int>();
+  S.nn_dyn = c->item_counter.as<int>() + 2;
   S.scan_tmp = c->scan_tmp.p;
   S.scan_tmp_bytes = c->scan_tmp.bytes;
   S.partials = c->partials.as<NnPartial>();
@@ -687,6 +697,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.refine_count = c->refine_count.as<int>();
   S.refine_cap = static_cast<int>(refine_cap);
   S.stats = c->stats.as<unsigned long long>();
+  S.iter_stats = c->iter_stats.as<unsigned long long>();
   S.trace_theta = c->trace_theta.as<double>();
   S.trace_loss = c->trace_loss.as<double>();
   S.trace_col = c->trace_col.as<int>();
@@ -704,7 +715,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   };
   push(c->ms.data(), c->ms.size() * sizeof(int64_t));
   push(c->gammas.data(), c->gammas.size() * sizeof(double));
-  const int64_t extra[5] = {c->k_max, c->k_stein, c->record_trace, c->nchunks_max, static_cast<int64_t>(c->seed)};
+  const int64_t extra[5] = {c->k_max, c->k_stein, c->record_trace, c->max_chunks, static_cast<int64_t>(c->seed)};
   push(extra, sizeof(extra));
   push(&c->eta_stein, sizeof(double));
   if (sig != c->graph_sig) {
@@ -722,13 +733,10 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   plan.pooled = pooled ? 1 : 0;
   plan.m = static_cast<int>(m);
   plan.fp64_mode = c->nn_mode == 1 ? 1 : 0;
-  const int max_chunks = std::max(1, static_cast<int>((m + 2 * kNnTile - 1) / (2 * kNnTile)));
-  int nch = std::min(c->nchunks_max, max_chunks);
-  int chunk = static_cast<int>((m + nch - 1) / nch);
-  chunk = (chunk + kNnTile - 1) / kNnTile * kNnTile;
-  nch = static_cast<int>((m + chunk - 1) / chunk);
-  plan.nchunks = nch;
-  plan.chunk = chunk;
+  // Upper bound of the device-chosen split (nn.cu fwd_split): splits keep at
+  // least 2 tiles of candidates each.
+  plan.nchunks = std::max(1, std::min(c->max_chunks, static_cast<int>(m / (2 * kNnTile))));
+  plan.target_items = c->target_items;
   plan.max_ns = c->max_ns;
   return plan;
 }
@@ -759,6 +767,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
   CUDA_OK(cudaMemcpyAsync(S.theta, c->init_theta_d.p, static_cast<size_t>(c->J) * 7 * 8, cudaMemcpyDeviceToDevice,
                           st));
   CUDA_OK(cudaMemsetAsync(S.stats, 0, kStats * sizeof(unsigned long long), st));
+  CUDA_OK(cudaMemsetAsync(S.iter_stats, 0, c->iter_stats.bytes, st));
   launch_init_state(P, S, st);
   launch_seed_rng(P, S, c->seed, st);
   c->launches += 2;
@@ -788,7 +797,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
                             c->xchg->world, c->rows_per_rank, st);
         c->launches += 2;
       }
-      c->launches += 1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->med_big_grid, st);
+      c->launches += 1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->max_gpop, c->med_big_grid, st);
     } else {
       launch_sgd(P, S, st);
       ++c->launches;
@@ -1181,6 +1190,18 @@ int asicp_dbg_raw_stats(asicp_ctx* ctx, uint64_t* out16) {
   if (!ctx || !out16) return ASICP_INVALID_ARGUMENT;
   for (int i = 0; i < kStats; ++i) out16[i] = ctx->raw_stats[i];
   return ASICP_OK;
+}
+
+int64_t asicp_dbg_iter_stats(asicp_ctx* ctx, uint64_t* out, int64_t n) {
+  if (!ctx || !ctx->prepared) return -1;
+  const int64_t total = 4 * static_cast<int64_t>(ctx->k_max + 1);
+  if (out && n > 0) {
+    if (ctx->in_flight) return -1;
+    if (cudaMemcpy(out, ctx->iter_stats.p, static_cast<size_t>(std::min(n, total)) * 8, cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+      return -1;
+  }
+  return total;
 }
 
 void asicp_dbg_exp_host(const double* x, double* y, int64_t n) {

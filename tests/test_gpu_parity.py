@@ -229,8 +229,24 @@ def test_large_population_grid_median_matches_port(solver):
 
     if not ref.port_available():
         pytest.skip("oracle port not built")
-    fx = fixtures.config(5, seed=2, particles_per_preshape=2100, n_object=500)
+    fx = fixtures.config(5, seed=2, particles_per_preshape=2100, n_object=500)  # grid-wide median
     fx.set(k_max=5, k_stein=3, anneal_period_total=5, record_trace=1)  # T >= C = 5 cycles
+    want = ref.port_optimize_grasp(fx)
+    got = solver.optimize(fx)
+    assert np.array_equal(got.trace_theta, want.trace_theta)
+    assert_same_solution(got, want)
+
+
+@pytest.mark.parametrize("ppp", [250, 700])
+def test_mid_population_median_and_split_svgd_match_port(solver, ppp):
+    """K = 250 takes the sampled-bracket median (M > 8192) and the split SVGD;
+    K = 700 the grid-wide median.  Full trace against the C port."""
+    from oracle import ref
+
+    if not ref.port_available():
+        pytest.skip("oracle port not built")
+    fx = fixtures.config(5, seed=4, particles_per_preshape=ppp, n_object=600)
+    fx.set(k_max=6, k_stein=5, anneal_period_total=6, record_trace=1)
     want = ref.port_optimize_grasp(fx)
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
