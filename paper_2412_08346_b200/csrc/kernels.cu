@@ -469,199 +469,7 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
   for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
 }
 
-// Bitonic sort of n (a power of two) keys in shared memory by the whole CTA.
-__device__ void block_bitonic_sort(unsigned long long* s, int n) {
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const unsigned long long a = s[i], c = s[ixj];
-          const bool asc = (i & k) == 0;
-          if ((a > c) == asc) {
-            s[i] = c;
-            s[ixj] = a;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
-// Row-major position p of the strict upper triangle of a K x K matrix -> (i, j).
-__device__ __forceinline__ void tri_index(long long p, int K, int* i_out, int* j_out) {
-  const double a = 2.0 * K - 1.0;
-  int i = static_cast<int>((a - sqrt(fmax(a * a - 8.0 * static_cast<double>(p), 0.0))) * 0.5);
-  i = max(0, min(i, K - 2));
-  auto start = [&](int r) { return static_cast<long long>(r) * (2ll * K - r - 1) / 2; };
-  while (i > 0 && start(i) > p) --i;
-  while (i < K - 2 && start(i + 1) <= p) ++i;
-  *i_out = i;
-  *j_out = i + 1 + static_cast<int>(p - start(i));
-}
-
-constexpr int kMedSample = 2048;  // sampled keys that bracket the median
-constexpr int kMedMid = 8192;     // keys the bracket may hold (sorted in shared memory)
-constexpr int kMedDelta = 96;     // bracket half-width in sample ranks (~4 sigma at 2048 samples)
-constexpr int kMedSmallSmem = (kMedSample + kMedMid) * 8;
-
-// One CTA per population (K < kMedBigK).  Fast path: sort a 2048-key sample
-// (bitonic, shared memory), take the bracket [lo, hi] of sample ranks around
-// M/2, count the keys below lo and gather the keys inside the bracket in one
-// pass, sort those and read rank M/2 directly — exact whenever the bracket
-// holds rank M/2 and at most 8192 keys (always when M <= 8192).  Otherwise
-// the 8-bit radix select below (nth_element at M/2, optim.cpp:141-142: an
-// exact order statistic either way).
-__global__ void __launch_bounds__(1024) median_kernel(DevProblem P, DevState S) {
-  const int pop = blockIdx.x;
-  if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // no local particle reads h
-  const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
-  if (K < 1) return;
-  if (K >= kMedBigK && P.bandwidth_mode != 1) return;  // med_*_kernel (below)
-  if (P.bandwidth_mode == 1) {
-    if (threadIdx.x == 0) S.h[pop] = P.fixed_bandwidth;
-    return;
-  }
-  if (K < 2) {
-    if (threadIdx.x == 0) S.h[pop] = 1.0;
-    return;
-  }
-  __shared__ unsigned int hist[256];
-  __shared__ unsigned long long s_prefix, s_mask;
-  __shared__ long long s_rank;
-  __shared__ int s_nmid;
-  __shared__ unsigned long long s_clo;
-  const long long M = static_cast<long long>(K) * (K - 1) / 2;
-  const long long r = M / 2;
-  auto key_at = [&](int i, int jj) {
-    const double d2 = sqnorm(sub(pose_t(th_of(S.theta_all, b + i)), pose_t(th_of(S.theta_all, b + jj))));
-    return static_cast<unsigned long long>(__double_as_longlong(d2));
-  };
-  {
-    extern __shared__ unsigned long long med_dyn[];
-    unsigned long long* smp = med_dyn;
-    unsigned long long* mid = med_dyn + kMedSample;
-    unsigned long long lo = 0, hi = ~0ull;
-    if (threadIdx.x == 0) {
-      s_nmid = 0;
-      s_clo = 0;
-    }
-    if (M > kMedMid) {
-      for (int s = threadIdx.x; s < kMedSample; s += blockDim.x) {
-        int i, jj;
-        tri_index((2ll * s + 1) * M / (2ll * kMedSample), K, &i, &jj);
-        smp[s] = key_at(i, jj);
-      }
-      __syncthreads();
-      block_bitonic_sort(smp, kMedSample);
-      const long long rs = r * kMedSample / M;
-      if (rs - kMedDelta >= 0) lo = smp[rs - kMedDelta];
-      if (rs + kMedDelta < kMedSample) hi = smp[rs + kMedDelta];
-    }
-    __syncthreads();
-    unsigned long long clo = 0;
-    const int lane = threadIdx.x & 31;
-    int i = 0;
-    long long row_start = 0;
-    for (long long p0 = 0; p0 < M; p0 += blockDim.x) {  // uniform trip count: full-warp ballots
-      const long long p = p0 + threadIdx.x;
-      bool in = false;
-      unsigned long long key = 0;
-      if (p < M) {
-        while (p >= row_start + (K - 1 - i)) {
-          row_start += K - 1 - i;
-          ++i;
-        }
-        key = key_at(i, i + 1 + static_cast<int>(p - row_start));
-        clo += key < lo ? 1 : 0;
-        in = key >= lo && key <= hi;
-      }
-      const unsigned bal = __ballot_sync(0xffffffffu, in);
-      int base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_nmid, __popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (in) {
-        const int slot = base + __popc(bal & ((1u << lane) - 1u));
-        if (slot < kMedMid) mid[slot] = key;
-      }
-    }
-    for (int off = 16; off > 0; off >>= 1) clo += __shfl_down_sync(0xffffffffu, clo, off);
-    if (lane == 0 && clo) atomicAdd(&s_clo, clo);
-    __syncthreads();
-    const int nmid = s_nmid;
-    const long long c_lo = static_cast<long long>(s_clo);
-    if (c_lo <= r && r < c_lo + nmid && nmid <= kMedMid) {
-      int n2 = 2;
-      while (n2 < nmid) n2 <<= 1;
-      for (int e = nmid + threadIdx.x; e < n2; e += blockDim.x) mid[e] = ~0ull;
-      __syncthreads();
-      block_bitonic_sort(mid, n2);
-      if (threadIdx.x == 0) {
-        const double median = __longlong_as_double(static_cast<long long>(mid[r - c_lo]));
-        const double h = median / P.pop_logk1[pop];
-        S.h[pop] = h < 1e-6 ? 1e-6 : h;  // std::max(h, 1e-6)
-      }
-      return;
-    }
-  }
-  if (threadIdx.x == 0) {
-    s_prefix = 0;
-    s_mask = 0;
-    s_rank = r;
-  }
-  // Keys are computed once (row-major over the upper triangle) into the
-  // population's slice of S.med_keys when it has one, then re-read by the
-  // later passes from L2; without a slice every pass recomputes them.
-  unsigned long long* keys = S.med_keys && P.med_off[pop] >= 0 ? S.med_keys + P.med_off[pop] : nullptr;
-  for (int pass = 0; pass < 8; ++pass) {
-    const int shift = 56 - 8 * pass;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const unsigned long long prefix = s_prefix, mask = s_mask;
-    if (keys != nullptr && pass > 0) {
-      for (long long p = threadIdx.x; p < M; p += blockDim.x) {
-        const unsigned long long key = keys[p];
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-      }
-    } else {
-      // Row i of the triangle is handled by consecutive threads over j (no
-      // per-pair index arithmetic): rows are walked in order, each thread
-      // striding over the flattened position.
-      int i = 0;
-      long long row_start = 0;
-      for (long long p = threadIdx.x; p < M; p += blockDim.x) {
-        while (p >= row_start + (K - 1 - i)) {
-          row_start += K - 1 - i;
-          ++i;
-        }
-        const int jj = i + 1 + static_cast<int>(p - row_start);
-        const double d2 = sqnorm(sub(pose_t(th_of(S.theta_all, b + i)), pose_t(th_of(S.theta_all, b + jj))));
-        const unsigned long long key = static_cast<unsigned long long>(__double_as_longlong(d2));
-        if (keys != nullptr) keys[p] = key;
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long rank = s_rank;
-      int digit = 0;
-      for (; digit < 256; ++digit) {
-        if (rank < static_cast<long long>(hist[digit])) break;
-        rank -= hist[digit];
-      }
-      s_rank = rank;
-      s_prefix = prefix | (static_cast<unsigned long long>(digit) << shift);
-      s_mask = mask | (255ull << shift);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double median = __longlong_as_double(static_cast<long long>(s_prefix));
-    const double h = median / P.pop_logk1[pop];
-    S.h[pop] = h < 1e-6 ? 1e-6 : h;  // std::max(h, 1e-6)
-  }
-}
+// Small populations: median_kernel in median.cu.
 
 // Large populations (K >= kMedBigK, e.g. cfg5's 16384 particles: 134M pair
 // keys): the same exact radix select spread over the whole GPU.  Six passes
@@ -1252,13 +1060,8 @@ void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int
 }
 int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
                         cudaStream_t st) {
-  static const bool attrs = [] {
-    cudaFuncSetAttribute(median_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmallSmem);
-    return true;
-  }();
-  (void)attrs;
   int n = 3;
-  median_kernel<<<P.n_pop, 1024, kMedSmallSmem, st>>>(P, S);
+  launch_median_small(P, S, st);
   if (big_grid > 0) {
     med_init_kernel<<<P.n_pop, 256, 0, st>>>(P, S);
     const int shifts[6] = {52, 40, 28, 16, 4, 0}, bits[6] = {12, 12, 12, 12, 12, 4};

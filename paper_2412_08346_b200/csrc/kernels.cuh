@@ -36,7 +36,6 @@ struct DevProblem {
   const int* part_pop;      // particle -> population
   const int* pop_off;       // population -> first particle (n_pop + 1)
   const double* pop_logk1;  // log(K + 1) per population (host std::log)
-  const long long* med_off; // population -> offset of its median keys in DevState::med_keys (-1: none)
   // Particle sharding: this context owns global particles
   // [j_lo, j_lo + J); populations span gpop_off in the global order, whose
   // poses and drifts the exchange gathers into DevState::theta_all/drift_all.
@@ -85,7 +84,6 @@ struct DevState {
   const double* theta_all;  // global J x 7 poses (SVGD partners / median)
   const double* drift_all;  // global J x 7 drifts
   double* h;           // per population bandwidth
-  unsigned long long* med_keys;  // cached squared-distance bit patterns for the median select
   double* S64;         // transformed contact surface, padded rows x 3
   float4* Sq32;        // its FP32 forward queries (x, y, z, margin), object-centred
   float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred
@@ -149,6 +147,7 @@ int minibatch_smem_cap();
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);
 void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st);
+void launch_median_small(const DevProblem& P, DevState& S, cudaStream_t st);  // median.cu (K < kMedBigK)
 // big_grid > 0: some population has K >= kMedBigK; the grid-wide select runs
 // with big_grid CTAs per population (returns the launch count).
 // S.kmat != null selects the split SVGD (kmat + accumulate kernels);

@@ -441,16 +441,23 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
         for (int r = 0; r < nscan; ++r) {
           const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
           const float4* sp = tiles + sid * kSub;
-          for (int c = 0; c < kSub; ++c) {
-            const float d = d32(qx[k], qy[k], qz[k], pc_get(sp, c));
-            if (d <= thr) {
-              const int p = base + sid * kSub + c;
-              if (np < kWinCap) {
-                mpos[np] = p;
-                md[np] = d;
+          for (int c = 0; c < kSub; c += 2) {
+            // One interleaved pair (two LDS.128): candidates c and c + 1.
+            const float4 A = sp[c], B = sp[c + 1];
+            const float dd[2] = {d32(qx[k], qy[k], qz[k], make_float4(A.x, A.z, B.x, B.z)),
+                                 d32(qx[k], qy[k], qz[k], make_float4(A.y, A.w, B.y, B.w))};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float d = dd[h];
+              if (d <= thr) {
+                const int p = base + sid * kSub + c + h;
+                if (np < kWinCap) {
+                  mpos[np] = p;
+                  md[np] = d;
+                }
+                ++np;
+                if (d == b1[k] && (pmin < 0 || p < pmin)) pmin = p;
               }
-              ++np;
-              if (d == b1[k] && (pmin < 0 || p < pmin)) pmin = p;
             }
           }
         }

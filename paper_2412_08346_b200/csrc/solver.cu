@@ -141,7 +141,7 @@ struct asicp_ctx {
 
   // Device buffers.
   Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
-      part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, med_off_d, med_keys, scene32, sdf_coarse;
+      part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, scene32, sdf_coarse;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
@@ -218,8 +218,8 @@ struct asicp_ctx {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     Buf* all[] = {&obj64, &obj_cand, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
-                  &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d, &med_off_d,
-                  &med_keys, &scene32, &sdf_coarse, &theta,
+                  &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
+                  &scene32, &sdf_coarse, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
@@ -464,34 +464,19 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   if (svgd_split) c->kmat.ensure(static_cast<size_t>(ktot) * sizeof(double2));
   upload(c->kofs_d, kofs.data(), kofs.size(), st);
   upload(c->pop_logk1, logk1.data(), logk1.size(), st);
-  // Median-select key cache: one slice of K(K-1)/2 keys per population when
-  // the total stays modest (otherwise the select recomputes keys per pass).
-  std::vector<long long> med_off(n_pre, -1);
-  long long med_total = 0;
+  // Median select: populations below kMedBigK in one CTA (median.cu), larger
+  // ones grid-wide over 128 x 128 tiles of the pair triangle (kernels.cu).
   long long big_tiles = 0;
   for (int i = 0; i < n_pre; ++i) {
     const long long K = p.init_counts[i];
-    if (K < kMedBigK) {
-      med_total += K * (K - 1) / 2;
-    } else {  // grid-wide select (kernels.cu med_*_kernel): 128 x 128 tiles of the triangle
+    if (K >= kMedBigK) {
       const long long nb = (K + 127) / 128;
       big_tiles = std::max(big_tiles, nb * (nb + 1) / 2);
     }
   }
   c->med_big_grid = static_cast<int>(std::min<long long>(big_tiles, 8ll * c->num_sms));
-  if (med_total > 0 && med_total <= (32ll << 20)) {
-    long long o = 0;
-    for (int i = 0; i < n_pre; ++i) {
-      if (p.init_counts[i] >= kMedBigK) continue;
-      med_off[i] = o;
-      o += p.init_counts[i] * (p.init_counts[i] - 1) / 2;
-    }
-    c->med_keys.ensure(static_cast<size_t>(med_total) * 8);
-  }
   c->med_hist.ensure(static_cast<size_t>(n_pre) * 4096 * 4);
   c->med_state.ensure(static_cast<size_t>(n_pre) * sizeof(MedState));
-  upload(c->med_off_d, med_off.data(), med_off.size(), st);
-  const bool med_cached = med_total > 0 && med_total <= (32ll << 20);
   upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
   c->init_theta.assign(p.init_poses + 7 * static_cast<int64_t>(lo), p.init_poses + 7 * static_cast<int64_t>(hi));
   upload(c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
@@ -620,7 +605,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.part_pop = c->part_pop.as<int>();
   P.pop_off = c->pop_off.as<int>();
   P.pop_logk1 = c->pop_logk1.as<double>();
-  P.med_off = c->med_off_d.as<long long>();
   P.gpop_off = c->gpop_off_d.as<int>();
   P.j_lo = lo;
   P.kofs = c->kofs_d.as<long long>();
@@ -660,7 +644,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.kmat = svgd_split ? c->kmat.as<double2>() : nullptr;
   S.med_hist = c->med_hist.as<unsigned int>();
   S.med_state = c->med_state.as<MedState>();
-  S.med_keys = med_cached ? c->med_keys.as<unsigned long long>() : nullptr;
   S.S64 = c->S64.as<double>();
   S.Sq32 = c->Sq32.as<float4>();
   S.Sc32 = c->Sc32.as<float4>();
