@@ -194,6 +194,17 @@ int asicp_wait(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errle
  * (collective).  Group backend: contexts of one process, one host thread per
  * rank, exchanging through host memory.  Setting or clearing a partition
  * drops the prepared problem. */
+/* graspmatch::build_sdf(cloud, voxel, {padding, surface_band}) (sdf.hpp,
+ * sdf.cpp:48-175) on the ctx's device: exact FP64 node distances and the
+ * widest-path sign, bit-identical to the reference field.  Fills dims and
+ * meta = {origin x, y, z, voxel, boundary_max_abs}; values (dims[0] * dims[1]
+ * * dims[2] floats, x-major) only when non-NULL — call once with NULL to size
+ * the buffer.  padding < 0 selects the reference default (4 voxels).
+ * ASICP_INVALID_ARGUMENT with the reference message for a non-positive voxel
+ * or fewer than 4 / coplanar points. */
+int asicp_build_sdf(asicp_ctx* ctx, const double* cloud, int64_t n, double voxel, double padding, double band,
+                    int32_t* dims, double* meta, float* values, char* err, size_t errlen);
+
 typedef struct asicp_group asicp_group;
 int asicp_nccl_unique_id(unsigned char* id /* 128 bytes */, char* err, size_t errlen);
 int asicp_set_partition_nccl(asicp_ctx* ctx, int rank, int world, const unsigned char* id, char* err,

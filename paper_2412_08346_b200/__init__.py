@@ -21,6 +21,7 @@ from .grasp import (  # noqa: F401
     StackedSdf,
     SteinConfig,
     annealing,
+    build_sdf,
     minibatch_schedule,
     optimize_grasp,
 )

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 namespace asicp {
 
@@ -137,6 +138,11 @@ struct NnPlan {
 };
 
 void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st);
+// sdf_build.cu: graspmatch::build_sdf on the device (returns ASICP_OK or
+// ASICP_INVALID_ARGUMENT with the reference message in *err; throws on CUDA
+// errors).  values == null: geometry only (dims, meta = origin[3], voxel, 0).
+int build_sdf_device(int device, cudaStream_t st, const double* cloud, int64_t n, double voxel, double padding,
+                     double band, int32_t* dims, double* meta, float* values, std::string* err);
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st);
 void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);

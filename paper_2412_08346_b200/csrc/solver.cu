@@ -1045,6 +1045,18 @@ int asicp_run(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errlen
   });
 }
 
+int asicp_build_sdf(asicp_ctx* ctx, const double* cloud, int64_t n, double voxel, double padding, double band,
+                    int32_t* dims, double* meta, float* values, char* err, size_t errlen) {
+  if (!ctx || !cloud || !dims || !meta) return ASICP_INVALID_ARGUMENT;
+  int rc = ASICP_OK;
+  const int g = guarded(err, errlen, [&] {
+    std::string msg;
+    rc = build_sdf_device(ctx->device, ctx->stream, cloud, n, voxel, padding, band, dims, meta, values, &msg);
+    if (rc != ASICP_OK) throw InvalidArgument(msg);
+  });
+  return g;
+}
+
 int asicp_nccl_unique_id(unsigned char* id, char* err, size_t errlen) {
   if (!id) return ASICP_INVALID_ARGUMENT;
   return guarded(err, errlen, [&] { nccl_unique_id(id); });

@@ -400,6 +400,20 @@ class Solver:
         _check(self.lib.asicp_run(self.ctx, C.byref(self._bufs.struct), err, 512), err)
         return self._bufs.solution(self._cp.k_stein)
 
+    def build_sdf(self, cloud, voxel: float, padding: float = -1.0, surface_band: float = 0.003) -> SdfGrid:
+        """graspmatch::build_sdf (sdf.cpp:48-175) on this context's GPU."""
+        cloud = np.ascontiguousarray(np.asarray(cloud, dtype=np.float64).reshape(-1, 3))
+        dims = (C.c_int32 * 3)()
+        meta = (C.c_double * 5)()
+        err = C.create_string_buffer(512)
+        cp = cloud.ctypes.data_as(L.c_double_p)
+        _check(self.lib.asicp_build_sdf(self.ctx, cp, len(cloud), voxel, padding, surface_band, dims, meta, None, err,
+                                        512), err)
+        values = np.zeros(int(dims[0]) * int(dims[1]) * int(dims[2]), dtype=np.float32)
+        _check(self.lib.asicp_build_sdf(self.ctx, cp, len(cloud), voxel, padding, surface_band, dims, meta,
+                                        values.ctypes.data_as(L.c_float_p), err, 512), err)
+        return SdfGrid(np.array(meta[:3]), float(meta[3]), tuple(int(d) for d in dims), values, float(meta[4]))
+
     def set_partition_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
         """Shard every population's particles over `world` ranks (one process
         per GPU); collective — every rank calls it with rank 0's id."""
@@ -479,6 +493,14 @@ def optimize_grasp(problem: GraspProblem) -> GraspSolution:
     if _DEFAULT is None:
         _DEFAULT = Solver()
     return _DEFAULT.optimize(problem)
+
+
+def build_sdf(cloud, voxel: float, padding: float = -1.0, surface_band: float = 0.003) -> SdfGrid:
+    """graspmatch::build_sdf (sdf.hpp, sdf.cpp:48-175) on the B200."""
+    global _DEFAULT
+    if _DEFAULT is None:
+        _DEFAULT = Solver()
+    return _DEFAULT.build_sdf(cloud, voxel, padding, surface_band)
 
 
 def minibatch_schedule(k: int, k_max: int, n_ref: int) -> int:
