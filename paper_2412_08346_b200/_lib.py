@@ -27,6 +27,8 @@ ASICP_BANDWIDTH_FIXED = 1
 ASICP_OPT_NN_MODE = 1
 ASICP_OPT_USE_GRAPH = 2
 ASICP_OPT_PROFILE = 3
+ASICP_OPT_MAX_CHUNKS = 4
+ASICP_OPT_WINDOW_POOL = 5
 
 
 class SdfGrid(C.Structure):

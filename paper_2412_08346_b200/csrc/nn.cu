@@ -471,11 +471,21 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
           if (!keep_old && np == 1 && !ovf) {
             P1(k) = pmin;
           } else {
-            int blk = (run_p & kAmbiguous) ? (run_p & ~kAmbiguous) : win_alloc(S);
+            // The running window is certified (run_p a position), listed (a
+            // block of the pool) or listless (the pool ran out: kNoBlock).  A
+            // listless window that stays inside the new margin keeps the query
+            // listless; otherwise a fresh block takes the new members.
+            const bool was_amb = (run_p & kAmbiguous) != 0;
+            const bool old_listed = was_amb && (run_p & ~kAmbiguous) != kNoBlock;
+            int blk = -1;
+            if (old_listed)
+              blk = run_p & ~kAmbiguous;
+            else if (!(was_amb && keep_old))
+              blk = win_alloc(S);
             if (blk >= 0) {
-              if (!(run_p & kAmbiguous)) {
+              if (!old_listed) {
                 S.amb_n[blk] = 0;
-                if (keep_old) win_push(S, blk, run_p, run_b);
+                if (keep_old) win_push(S, blk, run_p, run_b);  // certified old best (was_amb is false here)
               } else if (!keep_old) {
                 S.amb_n[blk] = 0;
               }

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -110,6 +111,7 @@ struct asicp_ctx {
   int num_sms = 148;
   int nn_grid = 296;
   int max_chunks = 16;
+  int window_pool = 0;  // ASICP_OPT_WINDOW_POOL (0: automatic)
 
   // Prepared problem (host side).
   bool prepared = false;
@@ -546,11 +548,14 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->item_counter.ensure(4 * 4);  // [0..1] item counters, [2..3] device split (nn_dyn)
   c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
   c->partials.ensure(fwd_slots * kNnQB * sizeof(NnPartial));
-  // Ambiguous windows are rare (~0.3 % of queries); the pool covers 1/16 of all
-  // (query, split) slots with a 64 k floor, and an exhausted pool only means a
-  // full FP64 rescan for the affected queries.
-  const int amb_cap = static_cast<int>(
-      std::min<size_t>(std::max<size_t>(65536, fwd_slots * kNnQB / 16), 1u << 24));
+  // Ambiguous windows: ~0.3 % of queries on cfg2, but up to ~15 % for dense
+  // clouds matched from far (100k points, queries 25 cm out).  A (query,
+  // split) allocates at most one block while the pool lasts, so a quarter of
+  // all slots (64 k floor) keeps exhaustion — and with it the full FP64
+  // rescan of the affected queries — out of every tested workload.
+  const int amb_cap = c->window_pool > 0 ? c->window_pool
+                                         : static_cast<int>(std::min<size_t>(
+                                               std::max<size_t>(65536, fwd_slots * kNnQB / 4), 1u << 26));
   c->amb_pool.ensure(static_cast<size_t>(amb_cap) * kWinCap * sizeof(int2));
   c->amb_n.ensure(static_cast<size_t>(amb_cap) * sizeof(int));
   c->amb_count.ensure(sizeof(int));
@@ -751,20 +756,50 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
                           st));
   CUDA_OK(cudaMemsetAsync(S.stats, 0, kStats * sizeof(unsigned long long), st));
   CUDA_OK(cudaMemsetAsync(S.iter_stats, 0, c->iter_stats.bytes, st));
+  // ASICP_DEBUG_SYNC=1 (eager runs only): synchronise after every stage and
+  // name the stage a device fault surfaced in.
+  static const bool dbg_sync = [] {
+    const char* e = std::getenv("ASICP_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  int dbg_k = -1;
+  auto stage = [&](const char* name) {
+    if (!dbg_sync || capture) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      throw DeviceError(std::string("asicp: device fault after ") + name + " (iteration " + std::to_string(dbg_k) +
+                        "): " + cudaGetErrorString(e));
+  };
   launch_init_state(P, S, st);
   launch_seed_rng(P, S, c->seed, st);
   c->launches += 2;
+  stage("init");
   for (int k = 0; k < c->k_max; ++k) {
+    dbg_k = k;
     const bool stein = k < c->k_stein;
     const int64_t m = c->ms[k];
     const bool pooled = m < c->n_obj;
     launch_pose_prep(P, S, 0, st);
+    stage("pose_prep");
     launch_collide(P, S, 0, 0, st);
+    stage("collide");
     S.pool_map = pooled ? S.pool_idx : nullptr;
     NnPlan plan = make_plan(c, 0, m, pooled);
     plan.iter = k;
-    enqueue_nn(c, plan, pooled ? static_cast<int>(m) : 0, capture);
+    if (dbg_sync && !capture) {
+      launch_nn_plan(c->P, c->S, plan, st);
+      stage("nn_plan");
+      if (pooled) {
+        launch_minibatch(c->P, c->S, static_cast<int>(m), st);
+        stage("minibatch");
+      }
+      launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, nullptr, nullptr);
+      stage("nn");
+    } else {
+      enqueue_nn(c, plan, pooled ? static_cast<int>(m) : 0, capture);
+    }
     launch_cost(P, S, 0, st);
+    stage("cost");
     c->launches += 3;
     if (c->record_trace) {
       launch_trace(P, S, k, st);
@@ -781,21 +816,28 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
         c->launches += 2;
       }
       c->launches += 1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->max_gpop, c->med_big_grid, st);
+      stage("stein");
     } else {
       launch_sgd(P, S, st);
       ++c->launches;
     }
     launch_bookkeeping(P, S, stein ? 1 : 0, (k + 1) < c->k_stein ? 1 : 0, st);
     ++c->launches;
+    stage("bookkeeping");
   }
+  dbg_k = c->k_max;
   // Final ranking on the full reference cloud (grasp.cpp:260-281).
   S.pool_map = nullptr;
   launch_pose_prep(P, S, 1, st);
+  stage("final pose_prep");
   launch_collide(P, S, 1, 1, st);
+  stage("final collide");
   NnPlan fin = make_plan(c, 2, c->n_obj, false);
   fin.iter = c->k_max;
   enqueue_nn(c, fin, 0, capture);
+  stage("final nn");
   launch_cost(P, S, 1, st);
+  stage("final cost");
   c->launches += 3;
   if (c->xchg) {
     // Every rank receives every particle's summary (and trace): the solution
@@ -1013,6 +1055,10 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
       break;
     case ASICP_OPT_MAX_CHUNKS:
       ctx->max_chunks = std::max<int>(1, static_cast<int>(value));
+      break;
+    case ASICP_OPT_WINDOW_POOL:
+      ctx->window_pool = std::max<int>(0, static_cast<int>(value));
+      ctx->prepared = false;  // buffers are sized at prepare
       break;
     case ASICP_OPT_PROFILE:
       ctx->profile = static_cast<int>(value);

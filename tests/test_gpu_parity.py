@@ -251,3 +251,29 @@ def test_mid_population_median_and_split_svgd_match_port(solver, ppp):
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)
+
+
+@pytest.mark.parametrize("pool", [1, 64])
+def test_exhausted_window_pool_stays_exact(pool, oracle):
+    """With the ambiguous-window pool nearly empty, ambiguous queries go
+    listless and are settled by the full FP64 rescan — including windows that
+    carry over sub-chunks of a 10k-point cloud.  Still bit-identical."""
+    from oracle import ref
+    from paper_2412_08346_b200 import Solver
+
+    s = Solver(window_pool=pool)
+    fx = fixtures.desk(5).set(record_trace=1)
+    got = s.optimize(fx)
+    want = oracle.optimize_grasp(fx)
+    assert np.array_equal(got.trace_theta, want.trace_theta)
+    assert_same_solution(got, want)
+    if pool == 1:
+        assert got.diagnostics["nn_full_refines"] > 0  # the fallback really ran
+    if ref.port_available():
+        fx2 = fixtures.config(2, seed=3, particles_per_preshape=6).set(k_max=10, k_stein=5, anneal_period_total=10,
+                                                                       record_trace=1)
+        got2 = s.optimize(fx2)
+        want2 = ref.port_optimize_grasp(fx2)
+        assert np.array_equal(got2.trace_theta, want2.trace_theta)
+        assert_same_solution(got2, want2)
+    s.close()
