@@ -196,6 +196,7 @@ bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t 
   if (S.fy_par == nullptr) return false;
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
   if (m <= kMbThreads * 12) return launch_par<12>(P, S, m, st);
+  if (m <= kMbThreads * 20) return launch_par<20>(P, S, m, st);
   return false;
 }
 

@@ -536,8 +536,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   size_t free_b = 0, total_b = 0;
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
   const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
-  const bool fy_par_on = (fy_par_bytes <= c->fy_par.bytes || fy_par_bytes <= free_b / 4) &&
-                         c->n_obj <= 12 * 1024 * 4;
+  // (The parallel kernel takes draws of m <= 20480 per call; larger m and an
+  // absent scratch fall back to the serial kernel.)
+  const bool fy_par_on = fy_par_bytes <= c->fy_par.bytes || fy_par_bytes <= free_b / 4;
   if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
   // Work items: forward < base_items + target_items (T x splits, see
   // fwd_split); reverse <= sum ceil(n_col / 32) <= J * ceil(n_scene / 32).
