@@ -175,6 +175,186 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P,
     pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
 }
 
+// Same algorithm with the stable sort replaced by a counting sort in shared
+// memory (clouds of n <= kCountMax points): per-key counts, a block-wide
+// exclusive scan, an atomic scatter, and an insertion sort of each key group by
+// step (groups hold a handful of steps) — which yields exactly the stable
+// order.  O(n + m) shared-memory work instead of a multi-pass radix sort, and
+// no bound on m.
+constexpr int kCountMax = 49152;
+
+__device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, int j, int m, int n, int* jv,
+                                            uint64_t* st, uint64_t* st0, int* s_mti, int* s_mti0, int* s_reject) {
+  const int tid = threadIdx.x;
+  uint64_t* gst = S.rng_state + static_cast<int64_t>(j) * mt::kN;
+  for (int i = tid; i < mt::kN; i += kMbThreads) st[i] = st0[i] = gst[i];
+  if (tid == 0) {
+    *s_mti = *s_mti0 = S.rng_mti[j];
+    *s_reject = 0;
+  }
+  __syncthreads();
+  for (int i0 = 0; i0 < m;) {
+    if (*s_mti >= mt::kN) {
+      mt::twist_block(st);
+      if (tid == 0) *s_mti = 0;
+      __syncthreads();
+    }
+    const int mti = *s_mti;
+    const int cnt = min(mt::kN - mti, m - i0);
+    for (int t = tid; t < cnt; t += kMbThreads) {
+      uint64_t u;
+      if (!mt::lemire(mt::temper(st[mti + t]), static_cast<uint64_t>(n - (i0 + t)), &u)) *s_reject = 1;
+      jv[i0 + t] = i0 + t + static_cast<int>(u);
+    }
+    __syncthreads();
+    if (tid == 0) *s_mti = mti + cnt;
+    i0 += cnt;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m) {
+  const int j = blockIdx.x;
+  if (!S.active[j] || S.n_col[j] > 0) return;
+  extern __shared__ __align__(16) unsigned char dyn[];
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(dyn);  // n counters, then offsets
+  __shared__ uint64_t st[mt::kN];
+  __shared__ uint64_t st0[mt::kN];
+  __shared__ int s_mti, s_mti0, s_reject;
+  __shared__ unsigned int part[kMbThreads];
+  const int tid = threadIdx.x;
+  const int n = P.n_obj;
+  int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
+  int* jv = scratch;
+  int* skey = scratch + P.n_obj_pad;
+  int* sval = skey + P.n_obj_pad;
+  int* lk = sval + P.n_obj_pad;
+  int* ptr = lk + P.n_obj_pad;
+  int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
+  draws_block(P, S, j, m, n, jv, st, st0, &s_mti, &s_mti0, &s_reject);
+  if (s_reject) {
+    // Exact serial replay from the saved engine state (never seen in practice).
+    if (tid == 0) {
+      int* idx = skey;
+      for (int i = 0; i < n; ++i) idx[i] = i;
+      int mt_i = s_mti0;
+      for (int i = 0; i < m; ++i) {
+        uint64_t u, x;
+        do {
+          if (mt_i >= mt::kN) {
+            mt::twist_serial(st0);
+            mt_i = 0;
+          }
+          x = mt::temper(st0[mt_i++]);
+        } while (!mt::lemire(x, static_cast<uint64_t>(n - i), &u));
+        const int jj = i + static_cast<int>(u);
+        const int b = idx[jj];
+        idx[jj] = idx[i];
+        pool[i] = b;
+      }
+      for (int i = 0; i < mt::kN; ++i) st[i] = st0[i];
+      s_mti = mt_i;
+    }
+    __syncthreads();
+  } else {
+    // 2. Counting sort of (j_s, s) by key, stable.
+    for (int k = tid; k < n; k += kMbThreads) cnt[k] = 0;
+    __syncthreads();
+    for (int s = tid; s < m; s += kMbThreads) atomicAdd(&cnt[jv[s]], 1u);
+    __syncthreads();
+    const int per = (n + kMbThreads - 1) / kMbThreads;
+    const int k0 = tid * per, k1 = min(n, k0 + per);
+    unsigned int sum = 0;
+    for (int k = k0; k < k1; ++k) sum += cnt[k];
+    part[tid] = sum;
+    __syncthreads();
+    for (int off = 1; off < kMbThreads; off <<= 1) {  // inclusive scan of the segment sums
+      const unsigned int v = tid >= off ? part[tid - off] : 0u;
+      __syncthreads();
+      part[tid] += v;
+      __syncthreads();
+    }
+    unsigned int run = tid ? part[tid - 1] : 0u;
+    for (int k = k0; k < k1; ++k) {
+      const unsigned int c = cnt[k];
+      cnt[k] = run;
+      run += c;
+    }
+    __syncthreads();
+    for (int s = tid; s < m; s += kMbThreads) {
+      const int k = jv[s];
+      const unsigned int slot = atomicAdd(&cnt[k], 1u);
+      skey[slot] = k;
+      sval[slot] = s;
+    }
+    __syncthreads();
+    for (int t = tid; t < m; t += kMbThreads) {  // order each key group by step
+      const int k = skey[t];
+      if (t > 0 && skey[t - 1] == k) continue;
+      int e = t + 1;
+      while (e < m && skey[e] == k) ++e;
+      for (int a = t + 1; a < e; ++a) {
+        const int v = sval[a];
+        int b = a - 1;
+        while (b >= t && sval[b] > v) {
+          sval[b + 1] = sval[b];
+          --b;
+        }
+        sval[b + 1] = v;
+      }
+    }
+    for (int s = tid; s < m; s += kMbThreads) lk[s] = -1;
+    __syncthreads();
+    // 3.-6. as in minibatch_par_kernel.
+    for (int t = tid; t < m; t += kMbThreads) {
+      const int k = skey[t];
+      if (k < m && (t == m - 1 || skey[t + 1] != k)) lk[k] = t;
+    }
+    __syncthreads();
+    for (int s = tid; s < m; s += kMbThreads) {
+      const int t = lk[s];
+      int wl = -1;
+      if (t >= 0) {
+        if (sval[t] < s)
+          wl = sval[t];
+        else if (t > 0 && skey[t - 1] == s)
+          wl = sval[t - 1];
+      }
+      ptr[s] = wl < 0 ? s : wl;
+    }
+    __syncthreads();
+    int* a = ptr;
+    int* b = jv;
+    for (;;) {
+      int changed = 0;
+      for (int s = tid; s < m; s += kMbThreads) {
+        const int p = a[s];
+        const int q = a[p];
+        b[s] = q;
+        changed |= q != p;
+      }
+      const int any = __syncthreads_or(changed);
+      int* t = a;
+      a = b;
+      b = t;
+      if (!any) break;
+    }
+    for (int t = tid; t < m; t += kMbThreads) {
+      const int i = sval[t];
+      const int k = skey[t];
+      pool[i] = (t > 0 && skey[t - 1] == k) ? a[sval[t - 1]] : k;
+    }
+    __syncthreads();
+  }
+  uint64_t* gst = S.rng_state + static_cast<int64_t>(j) * mt::kN;
+  for (int i = tid; i < mt::kN; i += kMbThreads) gst[i] = st[i];
+  if (tid == 0) S.rng_mti[j] = s_mti;
+  float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
+  for (int i = tid; i < m; i += kMbThreads) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
+  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads)
+    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
+}
+
 template <int ITEMS>
 static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
   using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
@@ -194,6 +374,14 @@ static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st)
 // large for one CTA's sort); the caller then uses the serial kernel.
 bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
   if (S.fy_par == nullptr) return false;
+  if (P.n_obj <= kCountMax) {
+    static const bool attr = cudaFuncSetAttribute(minibatch_cnt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  kCountMax * 4) == cudaSuccess;
+    if (attr) {
+      minibatch_cnt_kernel<<<P.J, kMbThreads, static_cast<size_t>(P.n_obj) * 4, st>>>(P, S, m);
+      return true;
+    }
+  }
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
   if (m <= kMbThreads * 12) return launch_par<12>(P, S, m, st);
   if (m <= kMbThreads * 20) return launch_par<20>(P, S, m, st);

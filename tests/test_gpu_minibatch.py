@@ -1,9 +1,10 @@
 """Device minibatch sampler (mt19937_64 + Lemire + partial Fisher-Yates,
 rng.hpp:16-44 / spatial_index.cpp:111-123) against the reference draws.
 
-Covers every path: the parallel sort-and-pointer-jump kernel at its three
-sizes (m <= 4096, 12288, 20480 per CTA sort) and the serial swap kernel (larger
-m, or parallel disabled), over consecutive calls on one engine stream.
+Covers every path: the counting-sort kernel (clouds of <= 49152 points, any
+m), the radix-sort kernel at its three sizes (m <= 4096, 12288, 20480) for
+larger clouds, and the serial swap kernel (larger m, or parallel disabled),
+over consecutive calls on one engine stream.
 """
 import ctypes as C
 
@@ -15,7 +16,8 @@ from paper_2412_08346_b200 import _lib as L
 pytestmark = pytest.mark.gpu
 
 CASES = [(208, 10000, [1, 150, 300, 450, 2400, 4500, 5250, 10000]), (5, 1500, [844, 1500, 1500]),
-         (7, 30000, [3000, 12000, 16000, 20000, 24000]), (9, 50000, [30000]), (3, 64, [64, 64])]
+         (7, 30000, [3000, 12000, 16000, 20000, 24000]), (9, 50000, [30000]), (3, 64, [64, 64]),
+         (11, 60000, [3000, 9000, 15000, 22000])]
 
 
 def draws(seed, n, ms, parallel):
