@@ -207,6 +207,16 @@ int asicp_wait(asicp_ctx* ctx, asicp_solution* solution, char* err, size_t errle
 int asicp_build_sdf(asicp_ctx* ctx, const double* cloud, int64_t n, double voxel, double padding, double band,
                     int32_t* dims, double* meta, float* values, char* err, size_t errlen);
 
+/* graspmatch::export_trace (io.hpp:94, io.cpp:691-710): write a solution's
+ * per-iteration trace (record_trace) in the reference's 13-field text format
+ * — "iteration particle preshape phase loss in_collision tx ty tz qw qx qy qz",
+ * k-major like asicp_solution's trace arrays; phase = "stein" for
+ * iterations < k_stein, else "sgd".  Host-only (no ctx).  Errors:
+ * ASICP_INVALID_ARGUMENT "cannot write trace: <path>". */
+int asicp_export_trace(const char* path, int64_t k_max, int64_t n_particles, int64_t k_stein,
+                       const int64_t* particle_preshape, const double* trace_theta, const double* trace_loss,
+                       const int32_t* trace_in_collision, char* err, size_t errlen);
+
 typedef struct asicp_group asicp_group;
 int asicp_nccl_unique_id(unsigned char* id /* 128 bytes */, char* err, size_t errlen);
 int asicp_set_partition_nccl(asicp_ctx* ctx, int rank, int world, const unsigned char* id, char* err,

@@ -167,6 +167,21 @@ def port_available() -> bool:
     return PORT_PATH.exists()
 
 
+def desk_trace_file(path, seed: int = 0, n_init: int = 100, n_top: int = 6, k_max: int = 40, k_stein: int = 15,
+                    anneal_total: int = 40) -> None:
+    """The reference trace file (graspmatch::export_trace, io.cpp:691-710) of
+    the desk scenario, written by oracle/ref_trace_cli.py in a subprocess (the
+    library's static libstdc++ iostreams cannot share a process with numpy's
+    libstdc++)."""
+    import subprocess
+    import sys
+
+    rc = subprocess.run([sys.executable, str(HERE / "ref_trace_cli.py"), str(seed), str(n_init), str(n_top),
+                         str(k_max), str(k_stein), str(anneal_total), str(path)]).returncode
+    if rc != 0:
+        raise RuntimeError(f"reference export_trace failed ({rc})")
+
+
 def port_optimize_grasp(problem) -> GraspSolution:
     global _PORT
     if _PORT is None:

@@ -9,10 +9,12 @@
 #include "asicp.h"
 #include "graspmatch/geometry.hpp"
 #include "graspmatch/grasp.hpp"
+#include "graspmatch/io.hpp"
 #include "graspmatch/sdf.hpp"
 #include "graspmatch/spatial_index.hpp"
 #include "graspmatch/synthetic.hpp"
 
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -246,6 +248,44 @@ int ref_optimize_grasp(const asicp_problem* p, asicp_solution* out, char* err, s
     return ASICP_INVALID_ARGUMENT;
   } catch (const std::exception& e) {
     copy_err(e.what(), err, errlen);
+    return ASICP_DEVICE_ERROR;
+  }
+}
+
+// graspmatch::optimize_grasp with record_trace, then graspmatch::export_trace
+// (io.cpp:691-710) of its trace to `path` — the reference trace file.
+int ref_optimize_and_export_trace(const asicp_problem* p, const char* path, char* err, size_t errlen) {
+  try {
+    GraspProblem g = to_problem(*p);
+    g.record_trace = true;
+    const GraspSolution s = optimize_grasp(g);
+    export_trace(s.trace, path);
+    return ASICP_OK;
+  } catch (const InvalidArgument& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_DEVICE_ERROR;
+  }
+}
+
+// The desk scenario (synthetic.cpp) solved with the given schedule and its
+// trace exported by graspmatch::export_trace — callable without any other
+// C++ runtime in the process (the library links libstdc++ statically, and
+// its iostreams must not meet a second libstdc++, e.g. numpy's).
+int ref_desk_export_trace(uint64_t seed, int64_t n_init, int64_t n_top, int64_t k_max, int64_t k_stein,
+                          int64_t anneal_total, const char* path) {
+  try {
+    GraspProblem g = synthetic::desk_grasp_problem(seed, 0, static_cast<size_t>(n_init), static_cast<size_t>(n_top));
+    g.k_max = static_cast<size_t>(k_max);
+    g.k_stein = static_cast<size_t>(k_stein);
+    g.stein.annealing.period_total = static_cast<size_t>(anneal_total);
+    g.record_trace = true;
+    const GraspSolution s = optimize_grasp(g);
+    export_trace(s.trace, path);
+    return ASICP_OK;
+  } catch (const std::exception&) {
     return ASICP_DEVICE_ERROR;
   }
 }

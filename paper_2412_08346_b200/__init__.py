@@ -22,6 +22,7 @@ from .grasp import (  # noqa: F401
     SteinConfig,
     annealing,
     build_sdf,
+    export_trace,
     minibatch_schedule,
     optimize_grasp,
 )

@@ -130,7 +130,7 @@ class Stats(C.Structure):
 # Every symbol include/asicp.h + include/asicp_fixtures.h declare.
 EXPORTS = (
     "asicp_abi_version", "asicp_create", "asicp_destroy", "asicp_set_option", "asicp_prepare",
-    "asicp_run", "asicp_run_async", "asicp_wait", "asicp_optimize_grasp", "asicp_build_sdf", "asicp_nccl_unique_id",
+    "asicp_run", "asicp_run_async", "asicp_wait", "asicp_optimize_grasp", "asicp_build_sdf", "asicp_export_trace", "asicp_nccl_unique_id",
     "asicp_set_partition_nccl", "asicp_group_create", "asicp_group_destroy", "asicp_set_partition_group",
     "asicp_clear_partition", "asicp_get_stats", "asicp_minibatch_schedule",
     "asicp_annealing", "asicp_fx_desk", "asicp_fx_config", "asicp_fx_view", "asicp_fx_free",
@@ -150,6 +150,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.asicp_wait.argtypes = [C.c_void_p, C.POINTER(Solution), C.c_char_p, C.c_size_t]
     lib.asicp_build_sdf.argtypes = [C.c_void_p, c_double_p, C.c_int64, C.c_double, C.c_double, C.c_double, c_i32_p,
                                     c_double_p, c_float_p, C.c_char_p, C.c_size_t]
+    lib.asicp_export_trace.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int64, c_i64_p, c_double_p, c_double_p,
+                                       c_i32_p, C.c_char_p, C.c_size_t]
     lib.asicp_nccl_unique_id.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
     lib.asicp_set_partition_nccl.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t]
     lib.asicp_group_create.restype = C.c_void_p

@@ -497,6 +497,27 @@ def optimize_grasp(problem: GraspProblem) -> GraspSolution:
     return _DEFAULT.optimize(problem)
 
 
+def export_trace(solution: GraspSolution, path) -> None:
+    """graspmatch::export_trace (io.cpp:691-710) of a solution recorded with
+    record_trace: the reference's 13-field text format (host only)."""
+    lib = L.load()
+    if solution.trace_theta is None:
+        k_max, J = 0, len(solution.particle_loss)
+        th = np.zeros((0, 7))
+        loss = np.zeros(0)
+        col = np.zeros(0, dtype=np.int32)
+    else:
+        k_max, J = solution.trace_loss.shape
+        th = np.ascontiguousarray(solution.trace_theta, dtype=np.float64)
+        loss = np.ascontiguousarray(solution.trace_loss, dtype=np.float64)
+        col = np.ascontiguousarray(solution.trace_in_collision, dtype=np.int32)
+    pre = np.ascontiguousarray(solution.particle_preshape, dtype=np.int64)
+    err = C.create_string_buffer(512)
+    _check(lib.asicp_export_trace(str(path).encode(), k_max, J, solution.k_stein, pre.ctypes.data_as(L.c_i64_p),
+                                  th.ctypes.data_as(L.c_double_p), loss.ctypes.data_as(L.c_double_p),
+                                  col.ctypes.data_as(L.c_i32_p), err, 512), err)
+
+
 def build_sdf(cloud, voxel: float, padding: float = -1.0, surface_band: float = 0.003) -> SdfGrid:
     """graspmatch::build_sdf (sdf.hpp, sdf.cpp:48-175) on the B200."""
     global _DEFAULT
