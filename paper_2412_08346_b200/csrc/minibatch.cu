@@ -213,29 +213,40 @@ __device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, in
   }
 }
 
-__global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m) {
+// Shared-memory arena of the counting-sort kernel (ints): the key counters /
+// group ends (cnt, max(n, m)), the draws (jv, m), the sorted steps (sval, m),
+// the W pointers and the pointer-jump buffer (ptr, jb, m each).  Sorted keys
+// are jv[sval[t]].  When the arena does not fit, everything but cnt lives in
+// the particle's global scratch.
+__host__ __device__ __forceinline__ int64_t mb_arena_ints(int n, int m) {
+  return static_cast<int64_t>(n > m ? n : m) + 4ll * m;
+}
+constexpr int kMbArenaMax = 200 * 1024;  // bytes of dynamic shared memory
+
+__global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m, int in_smem) {
   const int j = blockIdx.x;
   if (!S.active[j] || S.n_col[j] > 0) return;
   extern __shared__ __align__(16) unsigned char dyn[];
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(dyn);  // n counters, then offsets
   __shared__ uint64_t st[mt::kN];
   __shared__ uint64_t st0[mt::kN];
   __shared__ int s_mti, s_mti0, s_reject;
   __shared__ unsigned int part[kMbThreads];
   const int tid = threadIdx.x;
   const int n = P.n_obj;
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(dyn);  // counters -> offsets -> group ends (lk)
+  int* lk = reinterpret_cast<int*>(dyn);
   int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
-  int* jv = scratch;
-  int* skey = scratch + P.n_obj_pad;
-  int* sval = skey + P.n_obj_pad;
-  int* lk = sval + P.n_obj_pad;
-  int* ptr = lk + P.n_obj_pad;
+  int* base = in_smem ? reinterpret_cast<int*>(dyn) + (n > m ? n : m) : scratch;
+  int* jv = base;
+  int* sval = jv + (in_smem ? m : P.n_obj_pad);
+  int* ptr = sval + (in_smem ? m : P.n_obj_pad);
+  int* jb = ptr + (in_smem ? m : P.n_obj_pad);
   int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
   draws_block(P, S, j, m, n, jv, st, st0, &s_mti, &s_mti0, &s_reject);
   if (s_reject) {
     // Exact serial replay from the saved engine state (never seen in practice).
     if (tid == 0) {
-      int* idx = skey;
+      int* idx = scratch;  // n ints of the global scratch (5 x n_pad per particle)
       for (int i = 0; i < n; ++i) idx[i] = i;
       int mt_i = s_mti0;
       for (int i = 0; i < m; ++i) {
@@ -281,18 +292,14 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
       run += c;
     }
     __syncthreads();
-    for (int s = tid; s < m; s += kMbThreads) {
-      const int k = jv[s];
-      const unsigned int slot = atomicAdd(&cnt[k], 1u);
-      skey[slot] = k;
-      sval[slot] = s;
-    }
+    for (int s = tid; s < m; s += kMbThreads) sval[atomicAdd(&cnt[jv[s]], 1u)] = s;
     __syncthreads();
-    for (int t = tid; t < m; t += kMbThreads) {  // order each key group by step
-      const int k = skey[t];
-      if (t > 0 && skey[t - 1] == k) continue;
+    // Order each key group by step (groups hold a handful of steps).
+    for (int t = tid; t < m; t += kMbThreads) {
+      const int k = jv[sval[t]];
+      if (t > 0 && jv[sval[t - 1]] == k) continue;
       int e = t + 1;
-      while (e < m && skey[e] == k) ++e;
+      while (e < m && jv[sval[e]] == k) ++e;
       for (int a = t + 1; a < e; ++a) {
         const int v = sval[a];
         int b = a - 1;
@@ -303,28 +310,32 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
         sval[b + 1] = v;
       }
     }
+    __syncthreads();
+    // 3. Last member of each key group (keys < m only matter for wl()); the
+    // counters are dead now, so their space holds lk.
     for (int s = tid; s < m; s += kMbThreads) lk[s] = -1;
     __syncthreads();
-    // 3.-6. as in minibatch_par_kernel.
     for (int t = tid; t < m; t += kMbThreads) {
-      const int k = skey[t];
-      if (k < m && (t == m - 1 || skey[t + 1] != k)) lk[k] = t;
+      const int k = jv[sval[t]];
+      if (k < m && (t == m - 1 || jv[sval[t + 1]] != k)) lk[k] = t;
     }
     __syncthreads();
+    // 4. wl(s) -> initial pointers.
     for (int s = tid; s < m; s += kMbThreads) {
       const int t = lk[s];
       int wl = -1;
       if (t >= 0) {
         if (sval[t] < s)
           wl = sval[t];
-        else if (t > 0 && skey[t - 1] == s)
+        else if (t > 0 && jv[sval[t - 1]] == s)
           wl = sval[t - 1];
       }
       ptr[s] = wl < 0 ? s : wl;
     }
     __syncthreads();
+    // 5. Pointer jumping to the chain roots (W).
     int* a = ptr;
-    int* b = jv;
+    int* b = jb;
     for (;;) {
       int changed = 0;
       for (int s = tid; s < m; s += kMbThreads) {
@@ -339,10 +350,11 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
       b = t;
       if (!any) break;
     }
+    // 6. pool[i] from the sorted predecessor within the key group.
     for (int t = tid; t < m; t += kMbThreads) {
       const int i = sval[t];
-      const int k = skey[t];
-      pool[i] = (t > 0 && skey[t - 1] == k) ? a[sval[t - 1]] : k;
+      const int k = jv[i];
+      pool[i] = (t > 0 && jv[sval[t - 1]] == k) ? a[sval[t - 1]] : k;
     }
     __syncthreads();
   }
@@ -376,9 +388,12 @@ bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t 
   if (S.fy_par == nullptr) return false;
   if (P.n_obj <= kCountMax) {
     static const bool attr = cudaFuncSetAttribute(minibatch_cnt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kCountMax * 4) == cudaSuccess;
+                                                  kMbArenaMax) == cudaSuccess;
     if (attr) {
-      minibatch_cnt_kernel<<<P.J, kMbThreads, static_cast<size_t>(P.n_obj) * 4, st>>>(P, S, m);
+      const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
+      const int in_smem = arena <= kMbArenaMax ? 1 : 0;
+      const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
+      minibatch_cnt_kernel<<<P.J, kMbThreads, smem, st>>>(P, S, m, in_smem);
       return true;
     }
   }
