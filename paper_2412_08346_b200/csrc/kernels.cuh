@@ -107,8 +107,6 @@ struct DevState {
   int* item_off[2];    // J + 1 each
   int* item_counter;   // 2 ints
   int* nn_dyn;         // device-chosen forward split: [0] splits, [1] forward items
-  void* scan_tmp;
-  size_t scan_tmp_bytes;
   NnPartial* partials; // padded surface rows x max chunks
   int2* amb_pool;      // ambiguous-window member lists (kWinCap entries per block)
   int* amb_n;          // members per block (> kWinCap: overflow)
@@ -178,7 +176,6 @@ double run_ffma_peak(int iters);
 
 // nn.cu
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st);
-size_t scan_temp_bytes(int n);
 int nn_smem_bytes();
 void nn_set_attrs();
 int nn_blocks_per_sm();

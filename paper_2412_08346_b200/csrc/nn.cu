@@ -11,8 +11,10 @@
 //     is consumed in sub-chunks of <= 2048 candidates loaded whole into shared
 //     memory by TMA bulk copies (cp.async.bulk + mbarrier, one 4 KB tile per
 //     stage) and read with broadcast LDS.128;
-//   * each thread holds 8 queries in registers; one (query, candidate) pair
-//     is 3 FFMA + 1 FMNMX (the expansion form |b|^2 - 2 a.b), branch-free;
+//   * each thread holds 8 queries in registers; candidates are stored
+//     pair-interleaved so one packed FFMA2 evaluates the expansion form
+//     |b|^2 - 2 a.b for two candidates (3 FFMA2 per 2 pairs + a 3-input
+//     min), branch-free;
 //   * every 32 candidates (a subtile) each query folds the subtile minimum into
 //     a running top-3 of subtile minima (b1 <= b2 <= b3, subtiles s1, s2);
 //   * after a sub-chunk, the reference's answer within it — min FP64
@@ -27,7 +29,6 @@
 //   * reverse match: warp items (nn_rev_kernel, below).
 #include "common.cuh"
 
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -40,7 +41,8 @@ constexpr int kNnSmem = kNnStages * kNnTile * 16;
 constexpr int kMinChunk = 2 * kNnTile;       // smallest candidate split
 
 // ---------------------------------------------------------------------------
-// Work planning: per particle counts -> exclusive scans -> item lists.
+// Work planning: per particle counts -> exclusive scans (nn_plan_kernel, one
+// CTA) -> item lists (nn_fill_kernel).
 // Forward: count = query blocks; the split factor is chosen on the device
 // from the total T so that T x splits ~ plan.target_items (few matching
 // particles -> many splits per particle), capped by plan.nchunks and by
@@ -52,20 +54,6 @@ __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_ou
   const int chunk = round_up(ceil_div(plan.m, nch), kNnTile);
   *chunk_out = chunk;
   *nch_out = ceil_div(plan.m, chunk);
-}
-
-__global__ void nn_count_kernel(DevProblem P, DevState S, NnPlan plan) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j > P.J) return;
-  int fwd = 0, rev = 0;
-  if (j < P.J && (plan.kind == 2 || S.active[j])) {
-    if (plan.kind != 2 && S.n_col[j] > 0)
-      rev = ceil_div(S.n_col[j], kRevWQ);
-    else
-      fwd = ceil_div(surf_count(P, j), kFwdQB);
-  }
-  S.item_count[0][j] = fwd;
-  S.item_count[1][j] = rev;
 }
 
 __global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
@@ -747,22 +735,60 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
-void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
-  nn_count_kernel<<<(P.J + 1 + 127) / 128, 128, 0, st>>>(P, S, plan);
-  for (int l = 0; l < 2; ++l) {
-    size_t bytes = S.scan_tmp_bytes;
-    cub::DeviceScan::ExclusiveSum(S.scan_tmp, bytes, S.item_count[l], S.item_off[l], P.J + 1, st);
+// Counts, exclusive scans and the per-round counter resets in one CTA (one
+// launch instead of a count kernel, two device scans and three memsets):
+// each thread owns a contiguous range of particles.
+constexpr int kPlanThreads = 1024;
+
+__global__ void __launch_bounds__(kPlanThreads) nn_plan_kernel(DevProblem P, DevState S, NnPlan plan) {
+  __shared__ int sf[kPlanThreads], sr[kPlanThreads];
+  const int tid = threadIdx.x;
+  const int per = ceil_div(P.J, kPlanThreads);
+  const int j0 = min(P.J, tid * per), j1 = min(P.J, j0 + per);
+  int cf = 0, cr = 0;
+  for (int j = j0; j < j1; ++j) {
+    int fwd = 0, rev = 0;
+    if (plan.kind == 2 || S.active[j]) {
+      if (plan.kind != 2 && S.n_col[j] > 0)
+        rev = ceil_div(S.n_col[j], kRevWQ);
+      else
+        fwd = ceil_div(surf_count(P, j), kFwdQB);
+    }
+    S.item_count[0][j] = fwd;
+    S.item_count[1][j] = rev;
+    cf += fwd;
+    cr += rev;
   }
-  nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
-  cudaMemsetAsync(S.item_counter, 0, 2 * sizeof(int), st);
-  cudaMemsetAsync(S.refine_count, 0, sizeof(int), st);
-  cudaMemsetAsync(S.amb_count, 0, sizeof(int), st);
+  sf[tid] = cf;
+  sr[tid] = cr;
+  __syncthreads();
+  for (int off = 1; off < kPlanThreads; off <<= 1) {  // inclusive scans of the range sums
+    const int vf = tid >= off ? sf[tid - off] : 0, vr = tid >= off ? sr[tid - off] : 0;
+    __syncthreads();
+    sf[tid] += vf;
+    sr[tid] += vr;
+    __syncthreads();
+  }
+  int of = tid ? sf[tid - 1] : 0, orr = tid ? sr[tid - 1] : 0;
+  for (int j = j0; j < j1; ++j) {
+    S.item_off[0][j] = of;
+    S.item_off[1][j] = orr;
+    of += S.item_count[0][j];
+    orr += S.item_count[1][j];
+  }
+  if (tid == 0) {
+    S.item_off[0][P.J] = sf[kPlanThreads - 1];
+    S.item_off[1][P.J] = sr[kPlanThreads - 1];
+    S.item_count[0][P.J] = S.item_count[1][P.J] = 0;
+    S.item_counter[0] = S.item_counter[1] = 0;
+    *S.refine_count = 0;
+    *S.amb_count = 0;
+  }
 }
 
-size_t scan_temp_bytes(int n) {
-  size_t bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, bytes, static_cast<int*>(nullptr), static_cast<int*>(nullptr), n);
-  return bytes;
+void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
+  nn_plan_kernel<<<1, kPlanThreads, 0, st>>>(P, S, plan);
+  nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
 }
 
 int nn_smem_bytes() { return kNnSmem; }

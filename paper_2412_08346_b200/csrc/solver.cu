@@ -147,7 +147,7 @@ struct asicp_ctx {
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
-      item_count, item_off, item_counter, scan_tmp, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
+      item_count, item_off, item_counter, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
       stats, iter_stats, trace_theta,
       trace_loss, trace_col,
       final_loss, final_free;
@@ -225,7 +225,7 @@ struct asicp_ctx {
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
-                  &item_counter, &scan_tmp,
+                  &item_counter,
                   &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &iter_stats, &trace_theta,
                   &trace_loss, &trace_col,
                   &final_loss, &final_free};
@@ -547,7 +547,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->item_count.ensure(2 * (Jz + 1) * 4);
   c->item_off.ensure(2 * (Jz + 1) * 4);
   c->item_counter.ensure(4 * 4);  // [0..1] item counters, [2..3] device split (nn_dyn)
-  c->scan_tmp.ensure(std::max<size_t>(scan_temp_bytes(J + 1), 16));
   c->partials.ensure(fwd_slots * kNnQB * sizeof(NnPartial));
   // Ambiguous windows: ~0.3 % of queries on cfg2, but up to ~15 % for dense
   // clouds matched from far (100k points, queries 25 cm out).  A (query,
@@ -675,8 +674,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.item_off[1] = c->item_off.as<int>() + (Jz + 1);
   S.item_counter = c->item_counter.as<int>();
   S.nn_dyn = c->item_counter.as<int>() + 2;
-  S.scan_tmp = c->scan_tmp.p;
-  S.scan_tmp_bytes = c->scan_tmp.bytes;
   S.partials = c->partials.as<NnPartial>();
   S.amb_pool = c->amb_pool.as<int2>();
   S.amb_n = c->amb_n.as<int>();
