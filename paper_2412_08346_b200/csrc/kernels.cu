@@ -134,6 +134,18 @@ __global__ void __launch_bounds__(kColThreads, 3) collide_kernel(DevProblem P, D
   }
   const float tn = fabsf(t32x) + fabsf(t32y) + fabsf(t32z) + fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) +
                    fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]);
+  // Box as centre +- half extent; cbox covers the rounding of cx, hx and of
+  // the |l - c| - h evaluation (a few ulps of the box coordinates).
+  float cx[3], hx[3];
+  for (int a = 0; a < 3; ++a) {
+    cx[a] = 0.5f * (lo[a] + hi[a]);
+    hx[a] = 0.5f * (hi[a] - lo[a]);
+  }
+  const float cbox = 1e-6f * (fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) + fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]));
+  const float d0 = 1e-6f * (1.0f + tn) + cbox;
+  // Largest float below coarse_cut: cm < coarse_cut  <=>  cm <= cut32.
+  float cut32 = static_cast<float>(coarse_cut);
+  if (static_cast<double>(cut32) >= coarse_cut) cut32 = nextafterf(cut32, -INFINITY);
   const bool cull_ok = P.contact_tolerance >= -g.boundary_max_abs;
   const float inv_vox = static_cast<float>(1.0 / g.voxel);
   const float tol32 = static_cast<float>(P.contact_tolerance);
@@ -156,12 +168,13 @@ __global__ void __launch_bounds__(kColThreads, 3) collide_kernel(DevProblem P, D
         const float lx = __fmaf_rn(r32[0], fx, __fmaf_rn(r32[1], fy, __fmaf_rn(r32[2], fz, t32x)));
         const float ly = __fmaf_rn(r32[3], fx, __fmaf_rn(r32[4], fy, __fmaf_rn(r32[5], fz, t32y)));
         const float lz = __fmaf_rn(r32[6], fx, __fmaf_rn(r32[7], fy, __fmaf_rn(r32[8], fz, t32z)));
-        // |l32 - l64| <= ~5u (|p|_1 + |t|_1) (+ the rounded box corners): d is >= 3x that.
-        const float d = 1e-6f * (1.0f + fabsf(fx) + fabsf(fy) + fabsf(fz) + tn);
-        const bool out_far = lx < lo[0] - d || lx > hi[0] + d || ly < lo[1] - d || ly > hi[1] + d ||
-                             lz < lo[2] - d || lz > hi[2] + d;
-        const bool in_far = lx >= lo[0] + d && lx <= hi[0] - d && ly >= lo[1] + d && ly <= hi[1] - d &&
-                            lz >= lo[2] + d && lz <= hi[2] - d;
+        // |l32 - l64| <= ~5u (|p|_1 + |t|_1) (+ the rounded box corners): d is
+        // >= 3x that (p.w = |p|_1, prepared on the host).
+        const float d = __fmaf_rn(1e-6f, p.w, d0);
+        // Signed distance outside the box along the worst axis (> 0: outside).
+        const float e = fmaxf(fmaxf(fabsf(lx - cx[0]) - hx[0], fabsf(ly - cx[1]) - hx[1]), fabsf(lz - cx[2]) - hx[2]);
+        const bool out_far = e > d;
+        const bool in_far = e < -d;
         if (out_far) {
           if (cull_ok) status = 0;  // value <= -boundary_max_abs <= contact_tolerance: never collides
         } else if (in_far) {
@@ -174,8 +187,10 @@ __global__ void __launch_bounds__(kColThreads, 3) collide_kernel(DevProblem P, D
           // Coarse bound: the FP64 cell is within one cell of this one, and its
           // trilinear value is a convex combination of nodes the dilated block
           // max covers — below the tolerance, the point cannot collide.
-          const float cm = coarse_s[((ix / kCoarse) * g.cdims[1] + iy / kCoarse) * g.cdims[2] + iz / kCoarse];
-          if (static_cast<double>(cm) < coarse_cut) return 0;
+          const float cm = coarse_s[((static_cast<unsigned>(ix) >> 2) * g.cdims[1] + (static_cast<unsigned>(iy) >> 2)) *
+                                        g.cdims[2] +
+                                    (static_cast<unsigned>(iz) >> 2)];  // kCoarse = 4
+          if (cm <= cut32) return 0;
           const float fxx = fminf(fmaxf(ux - ix, 0.0f), 1.0f), fyy = fminf(fmaxf(uy - iy, 0.0f), 1.0f),
                       fzz = fminf(fmaxf(uz - iz, 0.0f), 1.0f);
           const float* v0 = P.sdf_values + g.values_offset + (static_cast<int64_t>(ix) * g.dims[1] + iy) * g.dims[2] + iz;
@@ -357,11 +372,14 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
 // accumulated in pair order by 8 threads, exactly like the reference loops.
 // ---------------------------------------------------------------------------
 constexpr int kCostThreads = 256;
+constexpr int kCostChunk = 1024;             // pairs per chunk: a whole KG3 surface in one pass
+constexpr int kCostRow = kCostChunk + 1;     // +1 double: the 8 summing threads hit distinct banks
+constexpr int kCostSmem = 8 * kCostRow * 8;  // bytes
 
 __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevState S, int final_pass) {
   const int j = blockIdx.x;
   if (!final_pass && !S.active[j]) return;
-  __shared__ double terms[8][kCostThreads];
+  extern __shared__ double cost_terms[];  // [8][kCostRow]
   __shared__ double acc[8];
   const int pre = P.part_pre[j];
   const double* th = th_of(S.theta, j);
@@ -390,9 +408,10 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   }
   const int64_t row = static_cast<int64_t>(j) * P.n_scene;
   const int* pmap = final_pass ? nullptr : S.pool_map;
-  for (int c0 = 0; c0 < npairs; c0 += kCostThreads) {
-    const int i = c0 + threadIdx.x;
-    if (i < npairs) {
+  for (int c0 = 0; c0 < npairs; c0 += kCostChunk) {
+    const int n = min(kCostChunk, npairs - c0);
+    for (int e = threadIdx.x; e < n; e += kCostThreads) {
+      const int i = c0 + e;
       V3 src, tr, ref;
       if (reverse) {
         const int sidx = S.res_rev[row + i];
@@ -407,17 +426,19 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
         ref = load3(P.obj64, oi);
       }
       const V3 res = sub(tr, ref);
-      terms[0][threadIdx.x] = res.x;
-      terms[1][threadIdx.x] = res.y;
-      terms[2][threadIdx.x] = res.z;
-      for (int jj = 0; jj < 4; ++jj) terms[3 + jj][threadIdx.x] = dot(res, mul(dR[jj], src));
-      terms[7][threadIdx.x] = sqnorm(res);
+      cost_terms[0 * kCostRow + e] = res.x;
+      cost_terms[1 * kCostRow + e] = res.y;
+      cost_terms[2 * kCostRow + e] = res.z;
+      for (int jj = 0; jj < 4; ++jj) cost_terms[(3 + jj) * kCostRow + e] = dot(res, mul(dR[jj], src));
+      cost_terms[7 * kCostRow + e] = sqnorm(res);
     }
     __syncthreads();
     if (threadIdx.x < 8) {
-      const int n = min(kCostThreads, npairs - c0);
+      // The reference's running sums, in pair order (the critical path).
+      const double* tr = cost_terms + threadIdx.x * kCostRow;
       double a = acc[threadIdx.x];
-      for (int e = 0; e < n; ++e) a = a + terms[threadIdx.x][e];
+#pragma unroll 8
+      for (int e = 0; e < n; ++e) a = a + tr[e];
       acc[threadIdx.x] = a;
     }
     __syncthreads();
@@ -1037,7 +1058,10 @@ void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) 
   }
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
-  cost_kernel<<<P.J, kCostThreads, 0, st>>>(P, S, final_pass);
+  static const bool attr =
+      cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCostSmem) == cudaSuccess;
+  (void)attr;
+  cost_kernel<<<P.J, kCostThreads, kCostSmem, st>>>(P, S, final_pass);
 }
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {
   trace_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, k);

@@ -23,7 +23,7 @@ struct DevProblem {
   const double* obj64;      // R, n_obj x 3
   const float4* obj_cand;   // R as FP32 NN candidates (-2b, |b|^2), b = r - center
   const double* scene64;    // C, n_scene x 3
-  const float4* scene32;    // C rounded to FP32 (x, y, z, 0), for the collision pre-test
+  const float4* scene32;    // C rounded to FP32 (x, y, z, |p|_1 rounded up), for the collision pre-test
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
   const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
   const double* pre_tcp;    // preshape tcp, 3 per preshape

@@ -343,9 +343,15 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
     std::vector<float4> s32(p.n_scene);
-    for (int64_t i = 0; i < p.n_scene; ++i)
-      s32[i] = make_float4(static_cast<float>(p.scene_cloud[3 * i]), static_cast<float>(p.scene_cloud[3 * i + 1]),
-                           static_cast<float>(p.scene_cloud[3 * i + 2]), 0.0f);
+    for (int64_t i = 0; i < p.n_scene; ++i) {
+      // w = |p|_1 of the rounded point (rounded up): the collision pre-test's
+      // transform-error margin.
+      const float x = static_cast<float>(p.scene_cloud[3 * i]), y = static_cast<float>(p.scene_cloud[3 * i + 1]),
+                  z = static_cast<float>(p.scene_cloud[3 * i + 2]);
+      const double l1 = (std::fabs(static_cast<double>(x)) + std::fabs(static_cast<double>(y))) +
+                        std::fabs(static_cast<double>(z));
+      s32[i] = make_float4(x, y, z, std::nextafter(static_cast<float>(l1), INFINITY));
+    }
     upload(c->scene32, s32.data(), s32.size(), st);
   }
 
