@@ -35,3 +35,23 @@ def test_reference_acceptance_on_b200():
     r = _run("acceptance_tests_b200", 1800)
     assert r.returncode == 0, r.stdout
     assert "acceptance: 9/9 criteria passed" in r.stdout
+
+
+def test_reference_scenario_front_end_on_b200(tmp_path):
+    """the reference's scenario front end —
+    write_demo_scenario, load_scenario_config, run_scenario (cloud I/O, cached
+    collision fields, initial poses, export_trace), report_to_json — driving
+    the B200 optimize_grasp through the drop-in.  Report (wall_seconds zeroed)
+    and trace file must equal the reference's own run byte for byte."""
+    for name in ("scenario_ref", "scenario_b200"):
+        if not (REF / name).exists():
+            pytest.skip(f"{REF / name} not built (make -C oracle ref dropin)")
+    d, trace = tmp_path / "demo", tmp_path / "trace.txt"  # same paths: the report echoes them
+    ref = subprocess.run([str(REF / "scenario_ref"), str(d), str(trace)], capture_output=True, text=True, timeout=600)
+    ref_trace = trace.read_bytes()
+    b200 = subprocess.run([str(REF / "scenario_b200"), str(d), str(trace)], capture_output=True, text=True,
+                          timeout=600)
+    assert ref.returncode == 0 and b200.returncode == 0, ref.stderr + b200.stderr
+    assert '"pose"' in b200.stdout
+    assert b200.stdout == ref.stdout
+    assert trace.read_bytes() == ref_trace
