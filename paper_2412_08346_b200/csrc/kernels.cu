@@ -1043,24 +1043,24 @@ void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, c
   collide_kernel<<<P.J, kColThreads, smem, st>>>(P, S, all, count_only);
 }
 int minibatch_smem_cap() { return 160 * 1024; }
+
+// Opt-in shared-memory sizes of this file's kernels on the current device
+// (function attributes are per device: called for every context).
+void kernels_set_attrs() {
+  cudaFuncSetAttribute(minibatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, minibatch_smem_cap());
+  cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCostSmem);
+}
+
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
   if (launch_minibatch_par(P, S, m, st)) return;
   const size_t need = static_cast<size_t>(P.n_obj) * sizeof(int);
   if (need <= static_cast<size_t>(minibatch_smem_cap())) {
-    static bool attr_done = false;
-    if (!attr_done) {
-      cudaFuncSetAttribute(minibatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, minibatch_smem_cap());
-      attr_done = true;
-    }
     minibatch_kernel<true><<<P.J, 128, need, st>>>(P, S, m);
   } else {
     minibatch_kernel<false><<<P.J, 128, 0, st>>>(P, S, m);
   }
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
-  static const bool attr =
-      cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCostSmem) == cudaSuccess;
-  (void)attr;
   cost_kernel<<<P.J, kCostThreads, kCostSmem, st>>>(P, S, final_pass);
 }
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {

@@ -135,6 +135,15 @@ struct NnPlan {
   int iter;      // iteration index (diagnostic counters)
 };
 
+// Per-device kernel attributes (opt-in shared memory), set for every context.
+void kernels_set_attrs();
+void median_set_attrs();
+void minibatch_set_attrs();
+inline void set_all_kernel_attrs() {
+  kernels_set_attrs();
+  median_set_attrs();
+  minibatch_set_attrs();
+}
 void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st);
 // sdf_build.cu: graspmatch::build_sdf on the device (returns ASICP_OK or
 // ASICP_INVALID_ARGUMENT with the reference message in *err; throws on CUDA

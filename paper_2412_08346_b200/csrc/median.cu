@@ -183,12 +183,11 @@ __global__ void __launch_bounds__(kMedThreads) median_kernel(DevProblem P, DevSt
 
 }  // namespace
 
+void median_set_attrs() {
+  cudaFuncSetAttribute(median_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem);
+}
+
 void launch_median_small(const DevProblem& P, DevState& S, cudaStream_t st) {
-  static const bool attrs = [] {
-    cudaFuncSetAttribute(median_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMedSmem);
-    return true;
-  }();
-  (void)attrs;
   median_kernel<<<P.n_pop, kMedThreads, kMedSmem, st>>>(P, S);
 }
 

@@ -368,18 +368,23 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
 }
 
 template <int ITEMS>
+constexpr int par_smem() {
+  return static_cast<int>(sizeof(typename cub::BlockRadixSort<int, kMbThreads, ITEMS, int>::TempStorage));
+}
+
+template <int ITEMS>
 static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
-  using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
-  const int smem = static_cast<int>(sizeof(typename Sort::TempStorage));
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(minibatch_par_kernel<ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return false;
-    attr = true;
-  }
-  minibatch_par_kernel<ITEMS><<<P.J, kMbThreads, smem, st>>>(P, S, m);
+  minibatch_par_kernel<ITEMS><<<P.J, kMbThreads, par_smem<ITEMS>(), st>>>(P, S, m);
   return true;
+}
+
+// Opt-in shared-memory sizes on the current device (per context: function
+// attributes are per device).
+void minibatch_set_attrs() {
+  cudaFuncSetAttribute(minibatch_par_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<4>());
+  cudaFuncSetAttribute(minibatch_par_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<12>());
+  cudaFuncSetAttribute(minibatch_par_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<20>());
+  cudaFuncSetAttribute(minibatch_cnt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMbArenaMax);
 }
 
 // Returns false when the parallel path does not apply (no scratch, or m too
@@ -387,15 +392,11 @@ static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st)
 bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
   if (S.fy_par == nullptr) return false;
   if (P.n_obj <= kCountMax) {
-    static const bool attr = cudaFuncSetAttribute(minibatch_cnt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  kMbArenaMax) == cudaSuccess;
-    if (attr) {
-      const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
-      const int in_smem = arena <= kMbArenaMax ? 1 : 0;
-      const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
-      minibatch_cnt_kernel<<<P.J, kMbThreads, smem, st>>>(P, S, m, in_smem);
-      return true;
-    }
+    const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
+    const int in_smem = arena <= kMbArenaMax ? 1 : 0;
+    const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
+    minibatch_cnt_kernel<<<P.J, kMbThreads, smem, st>>>(P, S, m, in_smem);
+    return true;
   }
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
   if (m <= kMbThreads * 12) return launch_par<12>(P, S, m, st);

@@ -1035,6 +1035,7 @@ asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen) {
     }
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     nn_set_attrs();
+    set_all_kernel_attrs();
     CUDA_OK(cudaEventCreate(&c->ev0));
     CUDA_OK(cudaEventCreate(&c->ev1));
     c->nn_grid = c->num_sms * std::max(1, nn_blocks_per_sm());
@@ -1185,6 +1186,7 @@ int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t cal
   // One particle stream (seed), `calls` consecutive minibatch draws of sizes
   // ms[c]; pool indices written back to back into out.
   try {
+    set_all_kernel_attrs();
     DevProblem P{};
     DevState S{};
     P.J = 1;
