@@ -8,7 +8,7 @@ step = one complete optimize_grasp solve: J * k_max = 76,800
 particle-iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload cfg2|cfg3|cfg4|cfg5] [--n-object N]
+                  [--workload cfg2|cfg3|cfg4|cfg5|reg] [--n-object N] [--reg-batch B]
 
 cfg2 / cfg3 at N > 1 run under torchrun, one rank per GPU; each rank solves its
 own object instance (object sharding: no data-path collective), so the scaling
@@ -21,6 +21,9 @@ the ranks by longest-processing-time (shard.py), each rank keeps its units
 device-resident and overlaps them on one GPU (batch.py), and the per-object
 answers are gathered and selected after the solves.  Total work is fixed, so
 the scaling is strong.
+
+reg is a batch of register_sgd_icp problems (acceptance
+C2's inputs, one CTA each); metric registrations/s.
 
 cfg5 (BASELINE.json configs[4]) is one population of 16384 particles against
 an n-point cylinder (--n-object, default 10k): at N > 1 the particles are
@@ -66,7 +69,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["reg"])
+    ap.add_argument("--reg-batch", type=int, default=1184, help="reg: problems per GPU (default 8 per SM)")
     ap.add_argument("--n-object", type=int, default=0, help="cfg5 object cloud size (default 10000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -247,8 +251,195 @@ class Timer:
         return self.a.elapsed_time(self.b)
 
 
+REG_METRIC = "registrations/sec"
+REG_UNIT = "registrations/s"
+REG_DESC = ("reg: SURVEY.md §8(f) rank 4 — register_sgd_icp batch, acceptance C2 problems (500-pt box-surface "
+            "clouds displaced <= 0.2 m / 30 deg, Gauss-Newton rotation preconditioner, minibatch 100, 500 iterations)")
+
+
+def reg_problems(n: int):
+    """Problem i = C2 trial i % 20 (test_acceptance.cpp:256-282) with seed 1000 + i."""
+    from paper_2412_08346_b200 import fixtures
+
+    trials = [fixtures.c2_trial(t) for t in range(20)]
+    srcs = [trials[i % 20][0] for i in range(n)]
+    refs = [trials[i % 20][1] for i in range(n)]
+    inits = np.tile([0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0], (n, 1))
+    seeds = [1000 + i for i in range(n)]
+    return srcs, refs, inits, seeds
+
+
+def reg_cpu(srcs, refs, inits, seeds, cfg, threads: int):
+    """Reference register_sgd_icp (oracle/_ref) over the problems, `threads`
+    host threads (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import ref
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        out = list(ex.map(lambda i: ref.register_sgd_icp(srcs[i], refs[i], inits[i], cfg, seeds[i]),
+                          range(len(srcs))))
+    return time.perf_counter() - t0, out
+
+
+def reg_config(n: int, world: int):
+    return {"workload": REG_DESC, "problems_per_gpu": n, "n_source": 500, "n_reference": 500, "minibatch": 100,
+            "max_iterations": 500, "preconditioner": "kGaussNewtonRotation",
+            "parallelism": f"problem-shard x{world}" if world > 1 else "1 GPU",
+            "step": "one batched solve of every problem (one CTA per problem)",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+def run_registration(args):
+    """The §8(f) rank-4 row: batched SGD-ICP registration (csrc/register.cu)."""
+    rank, world, local = dist_env()
+    sys.path.insert(0, str(ROOT / "tests"))
+    from paper_2412_08346_b200 import PreconditionerMode, SgdConfig
+
+    cfg = SgdConfig(preconditioner_mode=PreconditionerMode.kGaussNewtonRotation, minibatch_size=100,
+                    max_iterations=500)
+    n = args.reg_batch
+    sample_n = min(n, 64)
+    threads = os.cpu_count() or 1
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import ref
+
+        if not ref.available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
+            return 0
+        srcs, refs, inits, seeds = reg_problems(sample_n)
+        for _ in range(args.warmup):
+            reg_cpu(srcs, refs, inits, seeds, cfg, threads)
+        times = [reg_cpu(srcs, refs, inits, seeds, cfg, threads)[0] for _ in range(args.steps)]
+        ms = 1e3 * float(np.mean(times))
+        value = sample_n / (ms * 1e-3)
+        sample = f"{sample_n} C2 registrations per step, graspmatch::register_sgd_icp on {threads} threads"
+        print(json.dumps({
+            "impl": "reference", "metric": REG_METRIC, "value": value, "unit": REG_UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": reg_config(sample_n, world),
+            "cpu_baseline": {"value": value, "unit": REG_UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": REG_UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
+        return 0
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2412_08346_b200 import RegistrationBatch, Solver, register_sgd_icp_batch
+    from paper_2412_08346_b200 import _lib as L
+    import ctypes as C
+
+    main_stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    srcs, refs, inits, seeds = reg_problems(n)
+    seeds = [s + rank * n for s in seeds]  # each rank its own problems (problem sharding, weak scaling)
+    solver = Solver(device=local, stream=main_stream.cuda_stream)
+    batch = RegistrationBatch(solver, srcs, refs, inits, seeds, cfg)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def all_max(x: float) -> float:
+        t = torch.tensor([x], device="cuda")
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        result = batch.run()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kern_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(main_stream)
+            result = batch.run()
+            ev[k][1].record(main_stream)
+            kern_ms.append(solver.stats().solve_ms)
+        barrier()
+    ms_max = all_max(float(np.mean([a.elapsed_time(b) for a, b in ev])))
+    value = world * n / (ms_max * 1e-3)
+
+    e2e_ms = []
+    for k in range(max(1, args.steps)):
+        barrier()
+        flush.fill_(k & 0xFF)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_res = register_sgd_icp_batch(srcs, refs, inits, cfg, seeds, solver=solver)
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_max = all_max(float(np.mean(e2e_ms)))
+    same_e2e = all(np.array_equal(a.theta, b.theta) for a, b in zip(result, e2e_res))
+
+    lib = L.load()
+    lib.asicp_dbg_dfma_tflops.restype = C.c_double
+    peak = float(lib.asicp_dbg_dfma_tflops(4000))
+    iters = sum(r.iterations for r in result)
+    pairs = float(iters) * 100 * 500  # (query, reference point) pairs of the brute-force NN
+    kms = float(np.mean(kern_ms))
+    achieved = 8.0 * pairs / (kms * 1e-3) / 1e12
+
+    if rank == 0:
+        line = {
+            "metric": REG_METRIC, "value": value, "unit": REG_UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": reg_config(n, world),
+            "registration_iterations_per_s": world * iters / (ms_max * 1e-3),
+            "e2e": {"value": world * n / (e2e_max * 1e-3), "unit": REG_UNIT,
+                    "h2d_bytes_per_step": batch.input_bytes, "d2h_bytes_per_step": batch.output_bytes,
+                    "latency_ms": e2e_max, "steps_ms": e2e_ms, "bit_identical_to_resident": same_e2e},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "roofline": {"bound": "fp64", "kernel": "register_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak > 0 else None,
+                         "peak_source": "DFMA microbenchmark on this GPU (asicp_dbg_dfma_tflops); the NN "
+                                        "cannot contract (bit-exactness), so 0.5 is its ceiling",
+                         "traffic": None, "kernel_ms": kms,
+                         "algorithmic": "8 FP64 FLOP x (batch point, reference point) pairs: "
+                                        "iterations x 100 x 500 per problem"},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle import ref
+
+                if ref.available():
+                    dt, rs = reg_cpu(srcs[:sample_n], refs[:sample_n], inits[:sample_n], seeds[:sample_n], cfg,
+                                     threads)
+                    same = all(np.array_equal(a.theta, b.theta) and a.final_loss == b.final_loss
+                               and a.iterations == b.iterations for a, b in zip(rs, result[:sample_n]))
+                    line["cpu_baseline"] = {
+                        "value": sample_n / dt, "unit": REG_UNIT, "cores": threads, "kind": "reference",
+                        "sample": f"the first {sample_n} problems, oracle/_ref graspmatch::register_sgd_icp on "
+                                  f"{threads} threads", "bit_identical": same}
+            except Exception as e:  # reported, never required
+                line["cpu_baseline"] = {"error": repr(e)}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if args.workload == "reg":
+        return run_registration(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     rank, world, local = dist_env()

@@ -226,6 +226,68 @@ void asicp_group_destroy(asicp_group* group);
 int asicp_set_partition_group(asicp_ctx* ctx, asicp_group* group, int rank, char* err, size_t errlen);
 int asicp_clear_partition(asicp_ctx* ctx);
 
+/* ------------------------------------------------------------------------
+ * SGD-ICP registration: the drop-in for
+ *   graspmatch::RegistrationResult graspmatch::register_sgd_icp(
+ *       const PointCloud& source, const PointCloud& reference,
+ *       const PoseParams& initial, const SgdConfig& cfg, std::uint64_t seed)
+ *   (/root/reference/proj/include/graspmatch/optim.hpp:170-176, defined at
+ *    /root/reference/proj/src/optim.cpp:274-321), bit-identical.
+ * ------------------------------------------------------------------------ */
+
+/* graspmatch::PreconditionerMode (optim.hpp:14-27) */
+#define ASICP_PRECOND_FIXED 0
+#define ASICP_PRECOND_GAUSS_NEWTON_ROTATION 1
+
+/* graspmatch::SgdConfig (optim.hpp:29-43), every field. */
+typedef struct asicp_sgd_config {
+  double learning_rate;
+  double A[49];                  /* row-major 7x7 */
+  int64_t max_iterations;
+  double convergence_threshold;  /* < 0 disables early stopping */
+  int32_t preconditioner_mode;   /* ASICP_PRECOND_* */
+  double gn_damping;
+  int64_t minibatch_size;
+} asicp_sgd_config;
+
+/* graspmatch::RegistrationResult (optim.hpp:163-168). */
+typedef struct asicp_registration {
+  double theta[7];
+  int64_t iterations;
+  double final_loss;
+  int32_t converged;
+} asicp_registration;
+
+/* One registration.  Errors (ASICP_INVALID_ARGUMENT, the reference message):
+ * "register_sgd_icp: empty cloud", SgdConfig::validate (kFixed only),
+ * "sample_minibatch: m out of range" (minibatch_size 0), "rotation_matrix:
+ * quaternion is not unit-norm" (initial pose, or a pose that left the unit
+ * sphere mid-run — the reference throws at that iteration too). */
+int asicp_register_sgd_icp(asicp_ctx* ctx, const double* source, int64_t n_source, const double* reference,
+                           int64_t n_reference, const double* initial /* 7 */, const asicp_sgd_config* cfg,
+                           uint64_t seed, asicp_registration* result, char* err, size_t errlen);
+
+/* A batch of independent registrations with one config (no reference
+ * counterpart: the reference calls register_sgd_icp once per problem, e.g.
+ * the 20 trials of test_acceptance.cpp:256-292).  Problem i registers
+ * sources[source_offsets[i] .. source_offsets[i+1]) (rows of 3 doubles) into
+ * references[reference_offsets[i] .. +1) from initial[7 i ..] with seeds[i];
+ * results[i] is exactly what register_sgd_icp returns for it.  Problems are
+ * validated in order; the first failure's message is returned. */
+int asicp_register_sgd_icp_batch(asicp_ctx* ctx, int64_t n_problems, const double* sources,
+                                 const int64_t* source_offsets, const double* references,
+                                 const int64_t* reference_offsets, const double* initial, const uint64_t* seeds,
+                                 const asicp_sgd_config* cfg, asicp_registration* results, char* err,
+                                 size_t errlen);
+
+/* The batch call split like asicp_prepare / asicp_run: validate + upload once,
+ * then solve the device-resident batch (repeatable; each run restarts from the
+ * uploaded initial poses and seeds). */
+int asicp_register_prepare(asicp_ctx* ctx, int64_t n_problems, const double* sources, const int64_t* source_offsets,
+                           const double* references, const int64_t* reference_offsets, const double* initial,
+                           const uint64_t* seeds, const asicp_sgd_config* cfg, char* err, size_t errlen);
+int asicp_register_run(asicp_ctx* ctx, asicp_registration* results, char* err, size_t errlen);
+
 /* prepare + run: the drop-in for graspmatch::optimize_grasp. */
 int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution,
                          char* err, size_t errlen);

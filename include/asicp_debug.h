@@ -25,6 +25,7 @@ int asicp_dbg_exp_device(const double* x, double* y, int64_t n);
  * `iters` iterations; returns achieved TFLOP/s (2 FLOP per FFMA), timed with
  * CUDA events, or a negative value on failure. */
 double asicp_dbg_ffma_tflops(int iters);
+double asicp_dbg_dfma_tflops(int iters);  /* FP64 DFMA throughput (TFLOP/s) */
 
 /* Raw NN counters of the last asicp_run: [0] windows decided in FP64, [1] full
  * FP64 rescans, [2] queries, [3] canonical-order ties, [4] pairs, [5..7] rescans

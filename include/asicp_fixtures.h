@@ -37,6 +37,10 @@ void asicp_fx_free(asicp_fixture* fx);
 
 /* Building blocks (for fixture parity tests). */
 void asicp_fx_cylinder_cloud(double radius, double height, int n, uint64_t seed, double* out);
+/* Acceptance C2 (test_acceptance.cpp:256-282) trial inputs: n-point source /
+ * reference clouds (n x 3 each) and the truth pose (7). */
+void asicp_fx_c2_trial(int trial, int n, double* source, double* reference, double* truth7);
+void asicp_fx_blob_cloud(int n, double radius, uint64_t seed, double* out);
 /* Returns the node count; dims/meta (origin xyz, voxel, boundary_max_abs)
  * filled; values written when non-NULL. */
 int64_t asicp_fx_build_sdf(const double* cloud, int64_t n, double voxel, double padding, double band,

@@ -498,3 +498,194 @@ int port_optimize_grasp(const asicp_problem* P, asicp_solution* out, char* err, 
   free(drift);
   return ASICP_OK;
 }
+
+/* ------------------------------------------------------------------------
+ * graspmatch::register_sgd_icp (optim.cpp:274-321), both preconditioners.
+ * ------------------------------------------------------------------------ */
+
+/* SgdConfig::validate (optim.cpp:10-15) via the shim's isApprox / LLT. */
+static double a7_norm(const double* A, int transposed) {
+  double s = 0.0;
+  for (int j = 0; j < 7; ++j)
+    for (int i = 0; i < 7; ++i) {
+      const double v = transposed ? A[7 * j + i] : A[7 * i + j];
+      s = (i == 0 && j == 0) ? v * v : s + v * v;
+    }
+  return sqrt(s);
+}
+static const char* sgd_validate(const asicp_sgd_config* c) {
+  if (!(c->learning_rate > 0.0)) return "SgdConfig: learning_rate must be positive";
+  double d[49], l[7][7];
+  for (int i = 0; i < 7; ++i)
+    for (int j = 0; j < 7; ++j) d[7 * i + j] = c->A[7 * i + j] - c->A[7 * j + i];
+  const double na = a7_norm(c->A, 0), nt = a7_norm(c->A, 1);
+  if (!(a7_norm(d, 0) <= 1e-12 * (na < nt ? na : nt))) return "SgdConfig: A must be symmetric";
+  for (int i = 0; i < 7; ++i)
+    for (int j = 0; j < 7; ++j) l[i][j] = c->A[7 * i + j];
+  for (int j = 0; j < 7; ++j) {
+    double s = l[j][j];
+    for (int k = 0; k < j; ++k) s -= l[j][k] * l[j][k];
+    if (!(s > 0.0)) return "SgdConfig: A must be positive definite";
+    const double dd = sqrt(s);
+    l[j][j] = dd;
+    for (int i = j + 1; i < 7; ++i) {
+      double t = l[i][j];
+      for (int k = 0; k < j; ++k) t -= l[i][k] * l[j][k];
+      l[i][j] = t / dd;
+    }
+    for (int i = 0; i < j; ++i) l[i][j] = 0.0;
+  }
+  return NULL;
+}
+
+/* gauss_newton_rotation_step (optim.cpp:250-270), shim LDLT solve. */
+static void gn_step(const double* src, const int64_t* batch, int64_t m, const m3 dR[4], const double* g,
+                    double damping, double* dq) {
+  double jm[3][4] = {{0}}, mom[4][4] = {{0}}, cen[4][4], a[4][4], l[4][4], dv[4], y[4];
+  const double md = (double)m;
+  for (int64_t p = 0; p < m; ++p) {
+    const v3 s = vload(src, batch[p]);
+    v3 v[4];
+    for (int j = 0; j < 4; ++j) v[j] = mmul(&dR[j], s);
+    for (int j = 0; j < 4; ++j) {
+      jm[0][j] = jm[0][j] + v[j].x;
+      jm[1][j] = jm[1][j] + v[j].y;
+      jm[2][j] = jm[2][j] + v[j].z;
+    }
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) mom[i][j] = mom[i][j] + vdot(v[i], v[j]);
+  }
+  for (int r = 0; r < 3; ++r)
+    for (int j = 0; j < 4; ++j) jm[r][j] = jm[r][j] / md;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      cen[i][j] = mom[i][j] / md - ((jm[0][i] * jm[0][j] + jm[1][i] * jm[1][j]) + jm[2][i] * jm[2][j]);
+  const double trace = ((cen[0][0] + cen[1][1]) + cen[2][2]) + cen[3][3];
+  double gc[4];
+  for (int i = 0; i < 4; ++i) gc[i] = g[3 + i] - ((jm[0][i] * g[0] + jm[1][i] * g[1]) + jm[2][i] * g[2]);
+  if (!(trace > 1e-12)) {
+    for (int i = 0; i < 4; ++i) dq[i] = g[3 + i];
+    return;
+  }
+  const double sd = damping * trace / 4.0;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      a[i][j] = cen[i][j] + sd * (i == j ? 1.0 : 0.0);
+      l[i][j] = i == j ? 1.0 : 0.0;
+    }
+  for (int j = 0; j < 4; ++j) {
+    double s = a[j][j];
+    for (int k = 0; k < j; ++k) s -= l[j][k] * l[j][k] * dv[k];
+    dv[j] = s;
+    for (int i = j + 1; i < 4; ++i) {
+      double t = a[i][j];
+      for (int k = 0; k < j; ++k) t -= l[i][k] * l[j][k] * dv[k];
+      l[i][j] = t / dv[j];
+    }
+  }
+  for (int i = 0; i < 4; ++i) {
+    double s = gc[i];
+    for (int k = 0; k < i; ++k) s -= l[i][k] * y[k];
+    y[i] = s;
+  }
+  for (int i = 0; i < 4; ++i) y[i] /= dv[i];
+  for (int i = 3; i >= 0; --i) {
+    double s = y[i];
+    for (int k = i + 1; k < 4; ++k) s -= l[k][i] * dq[k];
+    dq[i] = s;
+  }
+}
+
+int port_register_sgd_icp(const double* src, int64_t ns, const double* ref, int64_t nr, const double* initial,
+                          const asicp_sgd_config* c, uint64_t seed, asicp_registration* out, char* err,
+                          size_t errlen) {
+  if (ns <= 0 || nr <= 0) {
+    set_err(err, errlen, "register_sgd_icp: empty cloud");
+    return ASICP_INVALID_ARGUMENT;
+  }
+  const int gn = c->preconditioner_mode == ASICP_PRECOND_GAUSS_NEWTON_ROTATION;
+  if (!gn) {
+    const char* msg = sgd_validate(c);
+    if (msg) {
+      set_err(err, errlen, msg);
+      return ASICP_INVALID_ARGUMENT;
+    }
+  }
+  mt64* rng = (mt64*)malloc(sizeof(mt64));
+  int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)ns);
+  mt_seed(rng, seed);
+  const int64_t m = c->minibatch_size < ns ? c->minibatch_size : ns;
+  double th[7];
+  memcpy(th, initial, sizeof th);
+  double prev = -1.0;
+  int rc = ASICP_OK;
+  out->iterations = 0;
+  out->final_loss = 0.0;
+  out->converged = 0;
+  for (int64_t k = 0; k < c->max_iterations; ++k) {
+    /* sample_minibatch_indices (spatial_index.cpp:113-125) */
+    if (m < 1) {
+      set_err(err, errlen, "sample_minibatch: m out of range");
+      rc = ASICP_INVALID_ARGUMENT;
+      break;
+    }
+    for (int64_t i = 0; i < ns; ++i) idx[i] = i;
+    for (int64_t i = 0; i < m; ++i) {
+      const int64_t j = i + (int64_t)uniform_index(rng, (uint64_t)(ns - i));
+      const int64_t v = idx[i];
+      idx[i] = idx[j];
+      idx[j] = v;
+    }
+    if (!(fabs(sqrt(qsq(th + 3)) - 1.0) <= 1e-6)) {
+      set_err(err, errlen, "rotation_matrix: quaternion is not unit-norm");
+      rc = ASICP_INVALID_ARGUMENT;
+      break;
+    }
+    const m3 R = rotation_matrix(th + 3);
+    m3 dR[4];
+    rotation_derivatives(th + 3, dR);
+    const v3 t = {th[0], th[1], th[2]};
+    double loss = 0.0, g[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t p = 0; p < m; ++p) {
+      const v3 s = vload(src, idx[p]);
+      const v3 q = vadd(mmul(&R, s), t);
+      const int64_t bi = nearest(ref, NULL, nr, q);
+      const v3 rp = vload(ref, bi);
+      const double dist = sqrt(vsq(vsub(rp, q)));
+      loss = loss + dist * dist;
+      const v3 res = vsub(q, rp);
+      g[0] = g[0] + res.x;
+      g[1] = g[1] + res.y;
+      g[2] = g[2] + res.z;
+      for (int j = 0; j < 4; ++j) g[3 + j] = g[3 + j] + vdot(res, mmul(&dR[j], s));
+    }
+    const double md = (double)m;
+    loss = loss / md;
+    for (int i = 0; i < 7; ++i) g[i] = g[i] / md;
+    double pre[7], dq[4];
+    for (int r = 0; r < 7; ++r) {
+      double s = c->A[7 * r] * g[0];
+      for (int k2 = 1; k2 < 7; ++k2) s = s + c->A[7 * r + k2] * g[k2];
+      pre[r] = s;
+    }
+    if (gn)
+      gn_step(src, idx, m, dR, g, c->gn_damping, dq);
+    else
+      for (int i = 0; i < 4; ++i) dq[i] = pre[3 + i];
+    for (int i = 0; i < 3; ++i) th[i] = th[i] - c->learning_rate * pre[i];
+    for (int i = 0; i < 4; ++i) th[3 + i] = th[3 + i] - c->learning_rate * dq[i];
+    normalize4(th + 3);
+    out->iterations = k + 1;
+    out->final_loss = loss;
+    if (prev > 0.0 && c->convergence_threshold >= 0.0 && fabs(loss - prev) / prev <= c->convergence_threshold &&
+        m == ns) {
+      out->converged = 1;
+      break;
+    }
+    prev = loss;
+  }
+  memcpy(out->theta, th, sizeof th);
+  free(idx);
+  free(rng);
+  return rc;
+}

@@ -196,3 +196,65 @@ def port_optimize_grasp(problem) -> GraspSolution:
     if rc != L.ASICP_OK:
         raise RuntimeError(err.value.decode())
     return bufs.solution(cp.k_stein)
+
+
+# ---------------------------------------------------------------------------
+# register_sgd_icp (optim.cpp:274-321): the reference and the C restatement.
+# ---------------------------------------------------------------------------
+def _reg_call(fn, source, reference, initial, cfg, seed):
+    from paper_2412_08346_b200.registration import _cloud, _pose, _result, sgd_config_struct
+
+    src, ref, init = _cloud(source), _cloud(reference), _pose(initial)
+    c = sgd_config_struct(cfg)
+    out = L.Registration()
+    err = C.create_string_buffer(512)
+    fn.argtypes = [L.c_double_p, C.c_int64, L.c_double_p, C.c_int64, L.c_double_p, C.POINTER(L.SgdCfg), C.c_uint64,
+                   C.POINTER(L.Registration), C.c_char_p, C.c_size_t]
+    rc = fn(src.ctypes.data_as(L.c_double_p), len(src), ref.ctypes.data_as(L.c_double_p), len(ref),
+            init.ctypes.data_as(L.c_double_p), C.byref(c), C.c_uint64(int(seed)), C.byref(out), err, 512)
+    if rc == L.ASICP_INVALID_ARGUMENT:
+        raise InvalidArgument(err.value.decode())
+    if rc != L.ASICP_OK:
+        raise RuntimeError(err.value.decode())
+    return _result(out)
+
+
+def register_sgd_icp(source, reference, initial, cfg, seed):
+    """Reference graspmatch::register_sgd_icp (oracle/_ref)."""
+    return _reg_call(load().ref_register_sgd_icp, source, reference, initial, cfg, seed)
+
+
+def port_register_sgd_icp(source, reference, initial, cfg, seed):
+    """The plain-C restatement (oracle/port/asicp_port.c)."""
+    global _PORT
+    if _PORT is None:
+        _PORT = C.CDLL(str(PORT_PATH))
+        _PORT.port_optimize_grasp.argtypes = [C.POINTER(L.Problem), C.POINTER(L.Solution), C.c_char_p, C.c_size_t]
+    return _reg_call(_PORT.port_register_sgd_icp, source, reference, initial, cfg, seed)
+
+
+def c2_trial(trial: int, n: int = 500):
+    """Acceptance C2 inputs from the reference's own generators."""
+    lib = load()
+    lib.ref_c2_trial.argtypes = [C.c_int, C.c_int, L.c_double_p, L.c_double_p, L.c_double_p]
+    src, ref, truth = np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(7)
+    lib.ref_c2_trial(trial, n, src.ctypes.data_as(L.c_double_p), ref.ctypes.data_as(L.c_double_p),
+                     truth.ctypes.data_as(L.c_double_p))
+    return src, ref, truth
+
+
+def blob_cloud(n: int, radius: float, seed: int) -> np.ndarray:
+    lib = load()
+    lib.ref_blob_cloud.argtypes = [C.c_int, C.c_double, C.c_uint64, L.c_double_p]
+    out = np.zeros((n, 3))
+    lib.ref_blob_cloud(n, radius, seed, out.ctypes.data_as(L.c_double_p))
+    return out
+
+
+def quaternion_angle(q1, q2) -> float:
+    lib = load()
+    lib.ref_quaternion_angle.restype = C.c_double
+    lib.ref_quaternion_angle.argtypes = [L.c_double_p, L.c_double_p]
+    a = np.ascontiguousarray(q1, dtype=np.float64)
+    b = np.ascontiguousarray(q2, dtype=np.float64)
+    return lib.ref_quaternion_angle(a.ctypes.data_as(L.c_double_p), b.ctypes.data_as(L.c_double_p))

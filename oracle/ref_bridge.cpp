@@ -10,6 +10,7 @@
 #include "graspmatch/geometry.hpp"
 #include "graspmatch/grasp.hpp"
 #include "graspmatch/io.hpp"
+#include "graspmatch/optim.hpp"
 #include "graspmatch/sdf.hpp"
 #include "graspmatch/spatial_index.hpp"
 #include "graspmatch/synthetic.hpp"
@@ -332,6 +333,75 @@ int ref_sample_minibatch_indices(uint64_t seed, int64_t skip, int64_t n, int64_t
     return ASICP_INVALID_ARGUMENT;
   }
   return ASICP_OK;
+}
+
+// graspmatch::register_sgd_icp (optim.cpp:274-321) on the C-ABI's structs.
+int ref_register_sgd_icp(const double* source, int64_t n_source, const double* reference, int64_t n_reference,
+                         const double* initial, const asicp_sgd_config* c, uint64_t seed, asicp_registration* out,
+                         char* err, size_t errlen) {
+  SgdConfig cfg;
+  cfg.learning_rate = c->learning_rate;
+  for (int i = 0; i < 7; ++i)
+    for (int j = 0; j < 7; ++j) cfg.A(i, j) = c->A[7 * i + j];
+  cfg.max_iterations = static_cast<size_t>(c->max_iterations);
+  cfg.convergence_threshold = c->convergence_threshold;
+  cfg.preconditioner_mode = c->preconditioner_mode == ASICP_PRECOND_GAUSS_NEWTON_ROTATION
+                                ? PreconditionerMode::kGaussNewtonRotation
+                                : PreconditionerMode::kFixed;
+  cfg.gn_damping = c->gn_damping;
+  cfg.minibatch_size = static_cast<size_t>(c->minibatch_size);
+  PoseParams init;
+  init.t = Vec3(initial[0], initial[1], initial[2]);
+  init.q = Vec4(initial[3], initial[4], initial[5], initial[6]);
+  try {
+    const RegistrationResult r =
+        register_sgd_icp(to_cloud(source, n_source), to_cloud(reference, n_reference), init, cfg, seed);
+    for (int i = 0; i < 3; ++i) out->theta[i] = r.theta.t[i];
+    for (int i = 0; i < 4; ++i) out->theta[3 + i] = r.theta.q[i];
+    out->iterations = static_cast<int64_t>(r.iterations);
+    out->final_loss = r.final_loss;
+    out->converged = r.converged ? 1 : 0;
+  } catch (const InvalidArgument& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_INVALID_ARGUMENT;
+  }
+  return ASICP_OK;
+}
+
+// test_acceptance.cpp:48-52 + 256-282: the C2 trial inputs, from the
+// reference's own generators.
+void ref_c2_trial(int trial, int n, double* source, double* reference, double* truth7) {
+  const PointCloud ref = synthetic::box_surface_cloud(n, Vec3(0.05, 0.03, 0.02), 42);
+  Rng rng(100 + trial);
+  Vec3 axis(rng.normal(), rng.normal(), rng.normal());
+  const double angle = rng.uniform(0.0, M_PI / 6.0);
+  axis.normalize();
+  const double sh = std::sin(angle / 2.0);
+  PoseParams truth;
+  truth.q = Vec4(std::cos(angle / 2.0), sh * axis.x(), sh * axis.y(), sh * axis.z());
+  Vec3 dir(rng.normal(), rng.normal(), rng.normal());
+  dir.normalize();
+  truth.t = dir * rng.uniform(0.0, 0.2);
+  const Mat3 r_true = rotation_matrix(truth.q);
+  for (size_t i = 0; i < ref.size(); ++i) {
+    const Vec3 s = r_true.transpose() * (ref[i] - truth.t);
+    for (int a = 0; a < 3; ++a) {
+      source[3 * i + a] = s[a];
+      reference[3 * i + a] = ref[i][a];
+    }
+  }
+  for (int i = 0; i < 3; ++i) truth7[i] = truth.t[i];
+  for (int i = 0; i < 4; ++i) truth7[3 + i] = truth.q[i];
+}
+
+void ref_blob_cloud(int n, double radius, uint64_t seed, double* out) {
+  const auto c = synthetic::blob_cloud(n, radius, seed);
+  for (size_t i = 0; i < c.size(); ++i)
+    for (int a = 0; a < 3; ++a) out[3 * i + a] = c[i][a];
+}
+
+double ref_quaternion_angle(const double* q1, const double* q2) {
+  return quaternion_angle(Vec4(q1[0], q1[1], q1[2], q1[3]), Vec4(q2[0], q2[1], q2[2], q2[3]));
 }
 
 int64_t ref_nearest(const double* cloud, int64_t n, const double* q, double* dist) {

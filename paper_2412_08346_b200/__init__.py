@@ -14,6 +14,7 @@ from .grasp import (  # noqa: F401
     InvalidArgument,
     ParticlePhase,
     PosePrior,
+    PreconditionerMode,
     Preshape,
     SdfGrid,
     SgdConfig,
@@ -25,4 +26,10 @@ from .grasp import (  # noqa: F401
     export_trace,
     minibatch_schedule,
     optimize_grasp,
+)
+from .registration import (  # noqa: F401
+    RegistrationBatch,
+    RegistrationResult,
+    register_sgd_icp,
+    register_sgd_icp_batch,
 )

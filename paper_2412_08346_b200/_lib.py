@@ -29,6 +29,8 @@ ASICP_OPT_USE_GRAPH = 2
 ASICP_OPT_PROFILE = 3
 ASICP_OPT_MAX_CHUNKS = 4
 ASICP_OPT_WINDOW_POOL = 5
+ASICP_PRECOND_FIXED = 0
+ASICP_PRECOND_GAUSS_NEWTON_ROTATION = 1
 
 
 class SdfGrid(C.Structure):
@@ -127,6 +129,29 @@ class Stats(C.Structure):
     ]
 
 
+class SgdCfg(C.Structure):
+    """asicp_sgd_config (graspmatch::SgdConfig, optim.hpp:29-43)."""
+    _fields_ = [
+        ("learning_rate", C.c_double),
+        ("A", C.c_double * 49),
+        ("max_iterations", C.c_int64),
+        ("convergence_threshold", C.c_double),
+        ("preconditioner_mode", C.c_int32),
+        ("gn_damping", C.c_double),
+        ("minibatch_size", C.c_int64),
+    ]
+
+
+class Registration(C.Structure):
+    """asicp_registration (graspmatch::RegistrationResult, optim.hpp:163-168)."""
+    _fields_ = [
+        ("theta", C.c_double * 7),
+        ("iterations", C.c_int64),
+        ("final_loss", C.c_double),
+        ("converged", C.c_int32),
+    ]
+
+
 # Every symbol include/asicp.h + include/asicp_fixtures.h declare.
 EXPORTS = (
     "asicp_abi_version", "asicp_create", "asicp_destroy", "asicp_set_option", "asicp_prepare",
@@ -134,7 +159,8 @@ EXPORTS = (
     "asicp_set_partition_nccl", "asicp_group_create", "asicp_group_destroy", "asicp_set_partition_group",
     "asicp_clear_partition", "asicp_get_stats", "asicp_minibatch_schedule",
     "asicp_annealing", "asicp_fx_desk", "asicp_fx_config", "asicp_fx_view", "asicp_fx_free",
-    "asicp_fx_cylinder_cloud", "asicp_fx_build_sdf",
+    "asicp_fx_cylinder_cloud", "asicp_fx_build_sdf", "asicp_register_sgd_icp", "asicp_register_sgd_icp_batch",
+    "asicp_register_prepare", "asicp_register_run", "asicp_fx_c2_trial", "asicp_fx_blob_cloud",
 )
 
 
@@ -177,6 +203,18 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.asicp_fx_build_sdf.restype = C.c_int64
     lib.asicp_fx_build_sdf.argtypes = [c_double_p, C.c_int64, C.c_double, C.c_double, C.c_double, c_i32_p,
                                        c_double_p, c_float_p]
+    lib.asicp_register_sgd_icp.argtypes = [C.c_void_p, c_double_p, C.c_int64, c_double_p, C.c_int64, c_double_p,
+                                           C.POINTER(SgdCfg), C.c_uint64, C.POINTER(Registration), C.c_char_p,
+                                           C.c_size_t]
+    lib.asicp_register_sgd_icp_batch.argtypes = [C.c_void_p, C.c_int64, c_double_p, c_i64_p, c_double_p, c_i64_p,
+                                                 c_double_p, C.POINTER(C.c_uint64), C.POINTER(SgdCfg),
+                                                 C.POINTER(Registration), C.c_char_p, C.c_size_t]
+    lib.asicp_register_prepare.argtypes = [C.c_void_p, C.c_int64, c_double_p, c_i64_p, c_double_p, c_i64_p,
+                                           c_double_p, C.POINTER(C.c_uint64), C.POINTER(SgdCfg), C.c_char_p,
+                                           C.c_size_t]
+    lib.asicp_register_run.argtypes = [C.c_void_p, C.POINTER(Registration), C.c_char_p, C.c_size_t]
+    lib.asicp_fx_c2_trial.argtypes = [C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]
+    lib.asicp_fx_blob_cloud.argtypes = [C.c_int, C.c_double, C.c_uint64, c_double_p]
     return lib
 
 

@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # built without FMA); the FP32 NN filter requests its FMAs explicitly.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3",
               "-diag-suppress", "177", f"-I{ROOT / 'include'}"]
-SOURCES = ["kernels.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "sdf_build.cu", "solver.cu", "fixtures.cu", "trace_io.cpp"]
+SOURCES = ["kernels.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "register.cu", "sdf_build.cu", "solver.cu", "fixtures.cu", "trace_io.cpp"]
 
 
 def _nvcc() -> str:

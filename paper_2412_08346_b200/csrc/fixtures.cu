@@ -63,6 +63,16 @@ class Rng {
   double spare_ = 0.0;
 };
 
+// `Vec3 v(rng.normal(), rng.normal(), rng.normal())` as the reference's g++
+// build evaluates it: constructor arguments right to left (z drawn first).
+// Checked against oracle/_ref in tests/test_fixtures_capi.py.
+P3 normal3(Rng& rng) {
+  const double z = rng.normal();
+  const double y = rng.normal();
+  const double x = rng.normal();
+  return P3{x, y, z};
+}
+
 P3 centroid(const Cloud& c) {
   P3 s{0.0, 0.0, 0.0};
   for (const P3& p : c) s = P3{s.x + p.x, s.y + p.y, s.z + p.z};
@@ -117,7 +127,7 @@ Cloud sphere_cloud(int n, double radius, uint64_t seed) {
   Rng rng(seed);
   Cloud cloud;
   for (int i = 0; i < n; ++i) {
-    const P3 v{rng.normal(), rng.normal(), rng.normal()};
+    const P3 v = normal3(rng);
     const double norm = std::sqrt(sqn(v));
     if (norm < 1e-12) {
       --i;
@@ -133,7 +143,7 @@ Cloud blob_cloud(int n, double radius, uint64_t seed) {
   Rng rng(seed);
   Cloud cloud;
   for (int i = 0; i < n; ++i) {
-    const P3 v{rng.normal(), rng.normal(), rng.normal()};
+    const P3 v = normal3(rng);
     const double norm = std::sqrt(sqn(v));
     if (norm < 1e-12) {
       --i;
@@ -779,6 +789,58 @@ double voxel_for_64(const Cloud& full) {
 }  // namespace
 
 extern "C" {
+
+// test_acceptance.cpp:256-282 (acceptance C2): trial `trial` of the SGD-ICP
+// recovery criterion.  reference = box_surface_cloud(n, (0.05, 0.03, 0.02), 42);
+// the truth pose draws axis, angle <= 30 deg, direction and distance <= 0.2 m
+// from Rng(100 + trial) (axis_angle_quaternion, test_acceptance.cpp:48-52);
+// source = R^T (p - t).  truth7 = (t, q).
+void asicp_fx_c2_trial(int trial, int n, double* source, double* reference, double* truth7) {
+  const Cloud ref = box_surface_cloud(n, P3{0.05, 0.03, 0.02}, 42);
+  Rng rng(100 + static_cast<uint64_t>(trial));
+  P3 axis = normal3(rng);
+  const double angle = rng.uniform(0.0, M_PI / 6.0);
+  auto normalize = [](P3& v) {
+    const double nv = std::sqrt(sqn(v));
+    if (nv > 0.0) v = P3{v.x / nv, v.y / nv, v.z / nv};
+  };
+  normalize(axis);
+  const double sh = std::sin(angle / 2.0);
+  const double q[4] = {std::cos(angle / 2.0), sh * axis.x, sh * axis.y, sh * axis.z};
+  P3 dir = normal3(rng);
+  normalize(dir);
+  const double dist = rng.uniform(0.0, 0.2);
+  const P3 t{dir.x * dist, dir.y * dist, dir.z * dist};
+  // rotation_matrix (geometry.cpp:8-21)
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  double r[9] = {w * w + x * x - y * y - z * z, 2.0 * (x * y - w * z), 2.0 * (x * z + w * y),
+                 2.0 * (x * y + w * z),         w * w - x * x + y * y - z * z, 2.0 * (y * z - w * x),
+                 2.0 * (x * z - w * y),         2.0 * (y * z + w * x),         w * w - x * x - y * y + z * z};
+  const double n2 = ((w * w + x * x) + y * y) + z * z;
+  for (double& v : r) v = v / n2;
+  for (size_t i = 0; i < ref.size(); ++i) {
+    const P3 d = sub(ref[i], t);
+    reference[3 * i] = ref[i].x;
+    reference[3 * i + 1] = ref[i].y;
+    reference[3 * i + 2] = ref[i].z;
+    for (int a = 0; a < 3; ++a)  // (R^T d)_a = sum_k R(k, a) d_k, left to right
+      source[3 * i + a] = (r[a] * d.x + r[3 + a] * d.y) + r[6 + a] * d.z;
+  }
+  truth7[0] = t.x;
+  truth7[1] = t.y;
+  truth7[2] = t.z;
+  for (int i = 0; i < 4; ++i) truth7[3 + i] = q[i];
+}
+
+// synthetic.cpp:69-83 blob_cloud (test_optim.cpp:540-584 registration inputs).
+void asicp_fx_blob_cloud(int n, double radius, uint64_t seed, double* out) {
+  const Cloud c = blob_cloud(n, radius, seed);
+  for (size_t i = 0; i < c.size(); ++i) {
+    out[3 * i] = c[i].x;
+    out[3 * i + 1] = c[i].y;
+    out[3 * i + 2] = c[i].z;
+  }
+}
 
 asicp_fixture* asicp_fx_desk(uint64_t seed, int64_t n_init, int64_t n_top) {
   Spec s;

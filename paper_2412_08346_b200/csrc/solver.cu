@@ -13,6 +13,7 @@
 #include "exchange.cuh"
 #include "kernels.cuh"
 #include "mt64.cuh"
+#include "register.cuh"
 
 #include <cuda_runtime.h>
 
@@ -152,6 +153,9 @@ struct asicp_ctx {
       trace_loss, trace_col,
       final_loss, final_free;
 
+  // SGD-ICP registration batches (register.cu), created on first use.
+  std::unique_ptr<asicp::RegBatch> reg;
+
   cudaGraphExec_t graph_exec = nullptr;
   bool graph_valid = false;
   std::vector<char> graph_sig;
@@ -209,6 +213,7 @@ struct asicp_ctx {
     free_staging();
     if (host_gath) cudaFreeHost(host_gath);
     xchg.reset();
+    reg.reset();
     Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend,    &xrecv,  &fsend, &frecv,
                          &gpop_off_d, &med_hist, &med_state, &kofs_d, &kmat};
     for (Buf* b : shard_bufs) b->release();
@@ -1167,6 +1172,59 @@ int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_sol
   return asicp_run(ctx, solution, err, errlen);
 }
 
+int asicp_register_prepare(asicp_ctx* ctx, int64_t n_problems, const double* sources, const int64_t* source_offsets,
+                           const double* references, const int64_t* reference_offsets, const double* initial,
+                           const uint64_t* seeds, const asicp_sgd_config* cfg, char* err, size_t errlen) {
+  if (!ctx || !cfg) return ASICP_INVALID_ARGUMENT;
+  std::string msg;
+  int rc = ASICP_OK;
+  try {
+    if (!ctx->reg) ctx->reg = std::make_unique<RegBatch>(ctx->device, ctx->stream);
+    rc = ctx->reg->prepare(n_problems, sources, source_offsets, references, reference_offsets, initial, seeds, *cfg,
+                           &msg);
+  } catch (const std::exception& e) {
+    msg = e.what();
+    rc = ASICP_DEVICE_ERROR;
+  }
+  if (rc != ASICP_OK) copy_err(msg, err, errlen);
+  return rc;
+}
+
+int asicp_register_run(asicp_ctx* ctx, asicp_registration* results, char* err, size_t errlen) {
+  if (!ctx) return ASICP_INVALID_ARGUMENT;
+  if (!ctx->reg) {
+    copy_err("asicp: no registration batch prepared", err, errlen);
+    return ASICP_INVALID_ARGUMENT;
+  }
+  std::string msg;
+  const int rc = ctx->reg->run(results, &msg);
+  if (rc != ASICP_OK) copy_err(msg, err, errlen);
+  if (rc == ASICP_OK) {
+    ctx->last_stats = asicp_stats{};
+    ctx->last_stats.solve_ms = ctx->reg->last_kernel_ms();
+    ctx->last_stats.kernel_launches = ctx->reg->launches();
+  }
+  return rc;
+}
+
+int asicp_register_sgd_icp_batch(asicp_ctx* ctx, int64_t n_problems, const double* sources,
+                                 const int64_t* source_offsets, const double* references,
+                                 const int64_t* reference_offsets, const double* initial, const uint64_t* seeds,
+                                 const asicp_sgd_config* cfg, asicp_registration* results, char* err,
+                                 size_t errlen) {
+  const int rc = asicp_register_prepare(ctx, n_problems, sources, source_offsets, references, reference_offsets,
+                                        initial, seeds, cfg, err, errlen);
+  if (rc != ASICP_OK) return rc;
+  return asicp_register_run(ctx, results, err, errlen);
+}
+
+int asicp_register_sgd_icp(asicp_ctx* ctx, const double* source, int64_t n_source, const double* reference,
+                           int64_t n_reference, const double* initial, const asicp_sgd_config* cfg, uint64_t seed,
+                           asicp_registration* result, char* err, size_t errlen) {
+  const int64_t so[2] = {0, n_source}, ro[2] = {0, n_reference};
+  return asicp_register_sgd_icp_batch(ctx, 1, source, so, reference, ro, initial, &seed, cfg, result, err, errlen);
+}
+
 int asicp_get_stats(asicp_ctx* ctx, asicp_stats* stats) {
   if (!ctx || !stats) return ASICP_INVALID_ARGUMENT;
   *stats = ctx->last_stats;
@@ -1180,6 +1238,7 @@ int64_t asicp_minibatch_schedule(int64_t k, int64_t k_max, int64_t n_ref) {
 double asicp_annealing(int64_t t, int64_t T, int64_t C, double p) { return annealing(t, T, C, p); }
 
 double asicp_dbg_ffma_tflops(int iters) { return run_ffma_peak(iters); }
+double asicp_dbg_dfma_tflops(int iters) { return run_dfma_peak(iters); }
 
 int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t calls, int32_t parallel, int32_t* out) {
   const bool par = parallel != 0;

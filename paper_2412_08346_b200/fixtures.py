@@ -94,3 +94,23 @@ def build_sdf(cloud: np.ndarray, voxel: float, padding: float = -1.0, band: floa
     lib.asicp_fx_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta,
                            vals.ctypes.data_as(L.c_float_p))
     return tuple(dims), np.array(meta[:3]), meta[3], meta[4], vals
+
+
+def c2_trial(trial: int, n: int = 500):
+    """Acceptance C2 trial inputs (test_acceptance.cpp:256-282): (source,
+    reference, truth pose) — the reference box cloud displaced by the trial's
+    seeded rigid transform."""
+    lib = L.load()
+    src = np.zeros((n, 3))
+    ref = np.zeros((n, 3))
+    truth = np.zeros(7)
+    lib.asicp_fx_c2_trial(trial, n, src.ctypes.data_as(L.c_double_p), ref.ctypes.data_as(L.c_double_p),
+                          truth.ctypes.data_as(L.c_double_p))
+    return src, ref, truth
+
+
+def blob_cloud(n: int, radius: float, seed: int) -> np.ndarray:
+    """synthetic::blob_cloud (synthetic.cpp:69-83)."""
+    out = np.zeros((n, 3))
+    L.load().asicp_fx_blob_cloud(n, radius, seed, out.ctypes.data_as(L.c_double_p))
+    return out

@@ -95,11 +95,23 @@ class AnnealingSchedule:
     exponent: float = 2.0
 
 
+class PreconditionerMode(enum.IntEnum):
+    """graspmatch::PreconditionerMode (optim.hpp:14-27)."""
+    kFixed = 0
+    kGaussNewtonRotation = 1
+
+
 @dataclass
 class SgdConfig:
+    """graspmatch::SgdConfig (optim.hpp:29-43).  optimize_grasp reads the
+    first three fields; register_sgd_icp reads all of them."""
     learning_rate: float = 1.0
     A: np.ndarray = field(default_factory=lambda: np.eye(7))
     convergence_threshold: float = 0.0002
+    max_iterations: int = 500
+    preconditioner_mode: PreconditionerMode = PreconditionerMode.kFixed
+    gn_damping: float = 1e-6
+    minibatch_size: int = 100
 
 
 @dataclass

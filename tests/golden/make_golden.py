@@ -3,7 +3,8 @@
 Run where /root/reference exists (oracle/_ref built by `make -C oracle`):
     python tests/golden/make_golden.py
 Every file is produced by the UNMODIFIED reference graspmatch::optimize_grasp
-(grasp.cpp:132-307) / sample_minibatch_indices (spatial_index.cpp:111-123)
+(grasp.cpp:132-307) / sample_minibatch_indices (spatial_index.cpp:111-123) /
+register_sgd_icp (optim.cpp:274-321)
 on the bit-identical fixtures of include/asicp_fixtures.h.
 """
 import sys
@@ -51,6 +52,23 @@ def main():
         arrays[f"idx_{i}"] = ref.sample_minibatch_indices(s, n, m, skip)
     np.savez_compressed(OUT / "minibatch.npz", cases=np.array(cases, dtype=np.int64), **arrays)
     print("wrote minibatch.npz")
+    # register_sgd_icp (optim.cpp:274-321): acceptance C2's 20 trials and the
+    # unit-test / variant cases of tests/reg_cases.py.
+    sys.path.insert(0, str(ROOT / "tests"))
+    import reg_cases
+
+    names, theta, iters, loss, conv = [], [], [], [], []
+    for name, src, rf, init, cfg, seed, _ in reg_cases.all_cases():
+        r = ref.register_sgd_icp(src, rf, init, cfg, seed)
+        names.append(name)
+        theta.append(r.theta)
+        iters.append(r.iterations)
+        loss.append(r.final_loss)
+        conv.append(int(r.converged))
+    np.savez_compressed(OUT / "registration.npz", names=np.array(names), theta=np.array(theta),
+                        iterations=np.array(iters, dtype=np.int64), final_loss=np.array(loss),
+                        converged=np.array(conv, dtype=np.int32))
+    print("wrote registration.npz")
 
 
 if __name__ == "__main__":
