@@ -545,6 +545,60 @@ __global__ void __launch_bounds__(kRegThreads, 4) register_kernel(RegArgs a, Reg
   }
 }
 
+// FP32 NN candidates of every problem's reference cloud, one CTA per problem:
+// centre c = the cloud's mean (any fixed point works — the certification
+// bound B is measured from the same c), b = r - c rounded to FP32,
+// (-2b, |b|^2) as the forward match builds them (solver.cu prepare), and
+// B = max |r - c| with slack.
+__global__ void __launch_bounds__(256) reg_cand_kernel(const double* ref, const long long* ref_off, float4* cand,
+                                                       double* geo) {
+  const int p = blockIdx.x, tid = threadIdx.x;
+  const long long r0 = ref_off[p];
+  const int nr = static_cast<int>(ref_off[p + 1] - r0);
+  const double* r = ref + 3 * r0;
+  __shared__ double red[3][256];
+  __shared__ double s_c[3];
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (int i = tid; i < nr; i += 256) {
+    sx += r[3 * i];
+    sy += r[3 * i + 1];
+    sz += r[3 * i + 2];
+  }
+  red[0][tid] = sx;
+  red[1][tid] = sy;
+  red[2][tid] = sz;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (tid < off)
+      for (int a = 0; a < 3; ++a) red[a][tid] += red[a][tid + off];
+    __syncthreads();
+  }
+  if (tid < 3) s_c[tid] = red[tid][0] / static_cast<double>(nr);
+  __syncthreads();
+  const double cx = s_c[0], cy = s_c[1], cz = s_c[2];
+  double bmax = 0.0;
+  for (int i = tid; i < nr; i += 256) {
+    const double bx = r[3 * i] - cx, by = r[3 * i + 1] - cy, bz = r[3 * i + 2] - cz;
+    const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
+    const double dx = fx, dy = fy, dz = fz;
+    cand[r0 + i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(dx * dx + dy * dy + dz * dz));
+    bmax = fmax(bmax, sqrt(bx * bx + by * by + bz * bz));
+  }
+  __syncthreads();
+  red[0][tid] = bmax;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (tid < off) red[0][tid] = fmax(red[0][tid], red[0][tid + off]);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    geo[4 * p] = cx;
+    geo[4 * p + 1] = cy;
+    geo[4 * p + 2] = cz;
+    geo[4 * p + 3] = red[0][0] * (1.0 + 1e-6) + 1e-12;
+  }
+}
+
 // Host restatements of SgdConfig::validate (optim.cpp:10-15) against the
 // shim's isApprox / LLT (oracle/shim/Eigen/Dense).
 double col_major_norm(const double* A, bool transposed) {
@@ -739,39 +793,6 @@ int RegBatch::prepare(int64_t n, const double* sources, const int64_t* src_off, 
   }
   REG_CUDA(D.src.ensure(std::max<int64_t>(tot_src, 1) * 24));
   REG_CUDA(D.ref.ensure(std::max<int64_t>(tot_ref, 1) * 24));
-  // FP32 NN candidates per reference point, as the forward match builds
-  // them (solver.cu prepare): b = r - centre rounded to FP32, (-2b, |b|^2).
-  std::vector<long long> co(ro.begin(), ro.end());
-  std::vector<float> cand(static_cast<size_t>(std::max<int64_t>(tot_ref, 1)) * 4, 0.0f);
-  std::vector<double> geo(4 * n);
-  for (int64_t i = 0; i < n; ++i) {
-    const double* r = references + 3 * ref_off[i];
-    const int64_t nr = ref_off[i + 1] - ref_off[i];
-    float* cf = cand.data() + 4 * co[i];
-    double c[3] = {0.0, 0.0, 0.0};
-    for (int64_t k = 0; k < nr; ++k)
-      for (int x = 0; x < 3; ++x) c[x] += r[3 * k + x];
-    for (int x = 0; x < 3; ++x) c[x] /= static_cast<double>(nr);
-    double bmax = 0.0;
-    for (int64_t k = 0; k < nr; ++k) {
-      const double bx = r[3 * k] - c[0], by = r[3 * k + 1] - c[1], bz = r[3 * k + 2] - c[2];
-      const float fx = static_cast<float>(bx), fy = static_cast<float>(by), fz = static_cast<float>(bz);
-      const double dx = fx, dy = fy, dz = fz;
-      cf[4 * k] = -2.0f * fx;
-      cf[4 * k + 1] = -2.0f * fy;
-      cf[4 * k + 2] = -2.0f * fz;
-      cf[4 * k + 3] = static_cast<float>(dx * dx + dy * dy + dz * dz);
-      bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
-    }
-    for (int x = 0; x < 3; ++x) geo[4 * i + x] = c[x];
-    geo[4 * i + 3] = bmax * (1.0 + 1e-6) + 1e-12;
-  }
-  REG_CUDA(D.cand.ensure(cand.size() * sizeof(float)));
-  REG_CUDA(D.cand_off.ensure(co.size() * 8));
-  REG_CUDA(D.geo.ensure(geo.size() * 8));
-  REG_CUDA(cudaMemcpyAsync(D.cand.p, cand.data(), cand.size() * sizeof(float), cudaMemcpyHostToDevice, st_));
-  REG_CUDA(cudaMemcpyAsync(D.cand_off.p, co.data(), co.size() * 8, cudaMemcpyHostToDevice, st_));
-  REG_CUDA(cudaMemcpyAsync(D.geo.p, geo.data(), geo.size() * 8, cudaMemcpyHostToDevice, st_));
   REG_CUDA(D.src_off.ensure((n + 1) * 8));
   REG_CUDA(D.ref_off.ensure((n + 1) * 8));
   REG_CUDA(D.init.ensure(n * 56));
@@ -787,6 +808,13 @@ int RegBatch::prepare(int64_t n, const double* sources, const int64_t* src_off, 
   REG_CUDA(cudaMemcpyAsync(D.ref.p, references + 3 * ref_off[0], tot_ref * 24, cudaMemcpyHostToDevice, st_));
   REG_CUDA(cudaMemcpyAsync(D.src_off.p, so.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st_));
   REG_CUDA(cudaMemcpyAsync(D.ref_off.p, ro.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st_));
+  REG_CUDA(D.cand.ensure(static_cast<size_t>(std::max<int64_t>(tot_ref, 1)) * sizeof(float4)));
+  REG_CUDA(D.geo.ensure(static_cast<size_t>(n) * 4 * 8));
+  reg_cand_kernel<<<static_cast<unsigned>(n), 256, 0, st_>>>(static_cast<const double*>(D.ref.p),
+                                                             static_cast<const long long*>(D.ref_off.p),
+                                                             static_cast<float4*>(D.cand.p),
+                                                             static_cast<double*>(D.geo.p));
+  REG_CUDA(cudaGetLastError());
   REG_CUDA(cudaMemcpyAsync(D.init.p, initial, n * 56, cudaMemcpyHostToDevice, st_));
   REG_CUDA(cudaMemcpyAsync(D.seeds.p, seeds, n * 8, cudaMemcpyHostToDevice, st_));
   if (D.h_cap < n) {
@@ -822,7 +850,7 @@ int RegBatch::run(asicp_registration* out, std::string* err) {
   a.ref = static_cast<const double*>(D.ref.p);
   a.ref_off = static_cast<const long long*>(D.ref_off.p);
   a.cand = static_cast<const float4*>(D.cand.p);
-  a.cand_off = static_cast<const long long*>(D.cand_off.p);
+  a.cand_off = static_cast<const long long*>(D.ref_off.p);
   a.geo = static_cast<const double*>(D.geo.p);
   a.init = static_cast<const double*>(D.init.p);
   a.seeds = static_cast<const unsigned long long*>(D.seeds.p);
