@@ -15,6 +15,7 @@
 // optimize_grasp tests on the GPU path.
 #include "asicp.h"
 #include "graspmatch/grasp.hpp"
+#include "graspmatch/optim.hpp"
 
 #include <mutex>
 #include <stdexcept>
@@ -197,6 +198,40 @@ GraspSolution optimize_grasp(const GraspProblem& problem) {
     sol.trace.push_back(rec);
   }
   return sol;
+}
+
+// Drop-in definition of graspmatch::register_sgd_icp (optim.hpp:170-176) in
+// place of optim.cpp:274-321: same signature, same InvalidArgument messages,
+// bit-identical RegistrationResult (csrc/register.cu).
+RegistrationResult register_sgd_icp(const PointCloud& source, const PointCloud& reference, const PoseParams& initial,
+                                    const SgdConfig& cfg, std::uint64_t seed) {
+  asicp_sgd_config c{};
+  c.learning_rate = cfg.learning_rate;
+  for (int i = 0; i < 7; ++i)
+    for (int j = 0; j < 7; ++j) c.A[7 * i + j] = cfg.A(i, j);
+  c.max_iterations = static_cast<int64_t>(cfg.max_iterations);
+  c.convergence_threshold = cfg.convergence_threshold;
+  c.preconditioner_mode = cfg.preconditioner_mode == PreconditionerMode::kGaussNewtonRotation
+                              ? ASICP_PRECOND_GAUSS_NEWTON_ROTATION
+                              : ASICP_PRECOND_FIXED;
+  c.gn_damping = cfg.gn_damping;
+  c.minibatch_size = static_cast<int64_t>(cfg.minibatch_size);
+  const std::vector<double> src = flatten(source), ref = flatten(reference);
+  const double init[7] = {initial.t[0], initial.t[1], initial.t[2], initial.q[0],
+                          initial.q[1], initial.q[2], initial.q[3]};
+  asicp_registration r{};
+  char err[512] = {0};
+  const int rc = asicp_register_sgd_icp(thread_context(), src.data(), static_cast<int64_t>(source.size()), ref.data(),
+                                        static_cast<int64_t>(reference.size()), init, &c, seed, &r, err, sizeof(err));
+  if (rc == ASICP_INVALID_ARGUMENT) throw InvalidArgument(err);
+  if (rc != ASICP_OK) throw std::runtime_error(std::string("asicp_register_sgd_icp: ") + err);
+  RegistrationResult out;
+  out.theta.t = Vec3(r.theta[0], r.theta[1], r.theta[2]);
+  out.theta.q = Vec4(r.theta[3], r.theta[4], r.theta[5], r.theta[6]);
+  out.iterations = static_cast<std::size_t>(r.iterations);
+  out.final_loss = r.final_loss;
+  out.converged = r.converged != 0;
+  return out;
 }
 
 }  // namespace graspmatch
