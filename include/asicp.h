@@ -288,6 +288,27 @@ int asicp_register_prepare(asicp_ctx* ctx, int64_t n_problems, const double* sou
                            const uint64_t* seeds, const asicp_sgd_config* cfg, char* err, size_t errlen);
 int asicp_register_run(asicp_ctx* ctx, asicp_registration* results, char* err, size_t errlen);
 
+/* graspmatch::ClosedFormStepResult (optim.hpp:82-85). */
+typedef struct asicp_icp_step {
+  double theta[7];
+  int32_t degenerate;
+} asicp_icp_step;
+
+/* graspmatch::icp_closed_form_step(source, reference, theta, index)
+ * (optim.hpp:87-91, optim.cpp:51-90): match every transformed source point,
+ * then the closed-form Kabsch/SVD step; bit-identical (the reference's
+ * JacobiSVD is the oracle/shim one).  The NnIndex argument of the reference
+ * is replaced by the reference cloud.  Errors: "icp_closed_form_step: empty
+ * cloud", "rotation_matrix: quaternion is not unit-norm". */
+int asicp_icp_closed_form_step(asicp_ctx* ctx, const double* source, int64_t n_source, const double* reference,
+                               int64_t n_reference, const double* theta /* 7 */, asicp_icp_step* result, char* err,
+                               size_t errlen);
+/* n independent steps in one launch (one CTA each). */
+int asicp_icp_closed_form_step_batch(asicp_ctx* ctx, int64_t n_problems, const double* sources,
+                                     const int64_t* source_offsets, const double* references,
+                                     const int64_t* reference_offsets, const double* thetas,
+                                     asicp_icp_step* results, char* err, size_t errlen);
+
 /* prepare + run: the drop-in for graspmatch::optimize_grasp. */
 int asicp_optimize_grasp(asicp_ctx* ctx, const asicp_problem* problem, asicp_solution* solution,
                          char* err, size_t errlen);

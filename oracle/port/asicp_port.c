@@ -689,3 +689,179 @@ int port_register_sgd_icp(const double* src, int64_t ns, const double* ref, int6
   free(rng);
   return rc;
 }
+
+/* ------------------------------------------------------------------------
+ * graspmatch::icp_closed_form_step (optim.cpp:51-90) with the Eigen shim's
+ * JacobiSVD (oracle/shim/Eigen/Dense) and quaternion_from_matrix (:29-46).
+ * ------------------------------------------------------------------------ */
+typedef struct { double a[3][3]; } mat3;
+
+static mat3 mm3(const mat3* x, const mat3* y) {
+  mat3 o;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o.a[i][j] = (x->a[i][0] * y->a[0][j] + x->a[i][1] * y->a[1][j]) + x->a[i][2] * y->a[2][j];
+  return o;
+}
+static mat3 tr3(const mat3* x) {
+  mat3 o;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o.a[i][j] = x->a[j][i];
+  return o;
+}
+static double det3(const mat3* m) {
+  const double(*c)[3] = m->a;
+  return (c[0][0] * (c[1][1] * c[2][2] - c[1][2] * c[2][1]) - c[1][0] * (c[0][1] * c[2][2] - c[0][2] * c[2][1])) +
+         c[2][0] * (c[0][1] * c[1][2] - c[0][2] * c[1][1]);
+}
+static double max1(double s) { return 1.0 < s ? s : 1.0; } /* std::max(1.0, s) */
+
+static void svd3(const mat3* in, double sing[3], mat3* U, mat3* V) {
+  mat3 u = *in, v = {{{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}};
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    int rotated = 0;
+    for (int p = 0; p < 3; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        double alpha = 0, beta = 0, gamma = 0;
+        for (int k = 0; k < 3; ++k) {
+          alpha += u.a[k][p] * u.a[k][p];
+          beta += u.a[k][q] * u.a[k][q];
+          gamma += u.a[k][p] * u.a[k][q];
+        }
+        if (fabs(gamma) <= 1e-300 || fabs(gamma) <= 1e-17 * sqrt(alpha * beta)) continue;
+        rotated = 1;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        for (int k = 0; k < 3; ++k) {
+          const double up = u.a[k][p], uq = u.a[k][q];
+          u.a[k][p] = c * up - s * uq;
+          u.a[k][q] = s * up + c * uq;
+          const double vp = v.a[k][p], vq = v.a[k][q];
+          v.a[k][p] = c * vp - s * vq;
+          v.a[k][q] = s * vp + c * vq;
+        }
+      }
+    if (!rotated) break;
+  }
+  double sv[3];
+  for (int j = 0; j < 3; ++j) {
+    double s2 = 0.0;
+    for (int k = 0; k < 3; ++k) s2 += u.a[k][j] * u.a[k][j];
+    sv[j] = sqrt(s2);
+  }
+  int order[3] = {0, 1, 2}; /* std::sort descending: libstdc++ insertion sort for 3 elements */
+  for (int i = 1; i < 3; ++i) {
+    const int val = order[i];
+    int j = i;
+    while (j > 0 && sv[val] > sv[order[j - 1]]) {
+      order[j] = order[j - 1];
+      --j;
+    }
+    order[j] = val;
+  }
+  const double tiny = 1e-300;
+  for (int i = 0; i < 3; ++i) {
+    const int j = order[i];
+    sing[i] = sv[j];
+    for (int k = 0; k < 3; ++k) {
+      V->a[k][i] = v.a[k][j];
+      U->a[k][i] = sv[j] > tiny ? u.a[k][j] / sv[j] : 0.0;
+    }
+  }
+  for (int i = 0; i < 3; ++i) {
+    if (sing[i] > tiny * max1(sing[0]) && sing[i] > 0.0) continue;
+    for (int trial = 0; trial < 3; ++trial) {
+      double cand[3] = {trial == 0 ? 1.0 : 0.0, trial == 1 ? 1.0 : 0.0, trial == 2 ? 1.0 : 0.0};
+      for (int k = 0; k < 3; ++k) {
+        if (k == i) continue;
+        if (k > i && !(sing[k] > 0.0)) continue;
+        const double proj = (U->a[0][k] * cand[0] + U->a[1][k] * cand[1]) + U->a[2][k] * cand[2];
+        for (int r = 0; r < 3; ++r) cand[r] = cand[r] - U->a[r][k] * proj;
+      }
+      const double n = sqrt((cand[0] * cand[0] + cand[1] * cand[1]) + cand[2] * cand[2]);
+      if (n > 1e-6) {
+        for (int r = 0; r < 3; ++r) U->a[r][i] = cand[r] / n;
+        break;
+      }
+    }
+  }
+}
+
+static void quat_from_matrix(const mat3* m, double* q) {
+  const double(*r)[3] = m->a;
+  const double tr = (r[0][0] + r[1][1]) + r[2][2];
+  if (tr > 0.0) {
+    const double s = sqrt(tr + 1.0) * 2.0;
+    q[0] = 0.25 * s; q[1] = (r[2][1] - r[1][2]) / s; q[2] = (r[0][2] - r[2][0]) / s; q[3] = (r[1][0] - r[0][1]) / s;
+  } else if (r[0][0] > r[1][1] && r[0][0] > r[2][2]) {
+    const double s = sqrt(((1.0 + r[0][0]) - r[1][1]) - r[2][2]) * 2.0;
+    q[0] = (r[2][1] - r[1][2]) / s; q[1] = 0.25 * s; q[2] = (r[0][1] + r[1][0]) / s; q[3] = (r[0][2] + r[2][0]) / s;
+  } else if (r[1][1] > r[2][2]) {
+    const double s = sqrt(((1.0 + r[1][1]) - r[0][0]) - r[2][2]) * 2.0;
+    q[0] = (r[0][2] - r[2][0]) / s; q[1] = (r[0][1] + r[1][0]) / s; q[2] = 0.25 * s; q[3] = (r[1][2] + r[2][1]) / s;
+  } else {
+    const double s = sqrt(((1.0 + r[2][2]) - r[0][0]) - r[1][1]) * 2.0;
+    q[0] = (r[1][0] - r[0][1]) / s; q[1] = (r[0][2] + r[2][0]) / s; q[2] = (r[1][2] + r[2][1]) / s; q[3] = 0.25 * s;
+  }
+  normalize4(q);
+}
+
+int port_icp_closed_form_step(const double* src, int64_t ns, const double* ref, int64_t nr, const double* theta,
+                              asicp_icp_step* out, char* err, size_t errlen) {
+  if (ns <= 0 || nr <= 0) {
+    set_err(err, errlen, "icp_closed_form_step: empty cloud");
+    return ASICP_INVALID_ARGUMENT;
+  }
+  if (!(fabs(sqrt(qsq(theta + 3)) - 1.0) <= 1e-6)) {
+    set_err(err, errlen, "rotation_matrix: quaternion is not unit-norm");
+    return ASICP_INVALID_ARGUMENT;
+  }
+  const m3 R = rotation_matrix(theta + 3);
+  const v3 t = {theta[0], theta[1], theta[2]};
+  int64_t* match = (int64_t*)malloc(sizeof(int64_t) * (size_t)ns);
+  double rm[3] = {0, 0, 0}, sm[3] = {0, 0, 0};
+  for (int64_t i = 0; i < ns; ++i) {
+    match[i] = nearest(ref, NULL, nr, vadd(mmul(&R, vload(src, i)), t));
+    const v3 m = vload(ref, match[i]);
+    rm[0] = rm[0] + m.x;
+    rm[1] = rm[1] + m.y;
+    rm[2] = rm[2] + m.z;
+  }
+  for (int64_t i = 0; i < ns; ++i)
+    for (int a = 0; a < 3; ++a) sm[a] = sm[a] + src[3 * i + a];
+  for (int a = 0; a < 3; ++a) {
+    sm[a] = sm[a] / (double)ns;
+    rm[a] = rm[a] / (double)ns;
+  }
+  mat3 cov = {{{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}};
+  for (int64_t i = 0; i < ns; ++i)
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) cov.a[r][c] = cov.a[r][c] + (src[3 * i + r] - sm[r]) * (ref[3 * match[i] + c] - rm[c]);
+  free(match);
+  double sing[3];
+  mat3 U, V;
+  svd3(&cov, sing, &U, &V);
+  if (ns < 3 || sing[1] <= 1e-12 * max1(sing[0])) {
+    const v3 smv = {sm[0], sm[1], sm[2]};
+    const v3 moved = vadd(mmul(&R, smv), t);
+    out->theta[0] = theta[0] + (rm[0] - moved.x);
+    out->theta[1] = theta[1] + (rm[1] - moved.y);
+    out->theta[2] = theta[2] + (rm[2] - moved.z);
+    for (int i = 3; i < 7; ++i) out->theta[i] = theta[i];
+    out->degenerate = 1;
+    return ASICP_OK;
+  }
+  const mat3 Ut = tr3(&U);
+  mat3 D = {{{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}};
+  const mat3 VUt = mm3(&V, &Ut);
+  D.a[2][2] = det3(&VUt) < 0.0 ? -1.0 : 1.0;
+  const mat3 VD = mm3(&V, &D);
+  const mat3 r = mm3(&VD, &Ut);
+  double q[4];
+  quat_from_matrix(&r, q);
+  for (int i = 0; i < 3; ++i)
+    out->theta[i] = rm[i] - ((r.a[i][0] * sm[0] + r.a[i][1] * sm[1]) + r.a[i][2] * sm[2]);
+  for (int i = 0; i < 4; ++i) out->theta[3 + i] = q[i];
+  out->degenerate = 0;
+  return ASICP_OK;
+}

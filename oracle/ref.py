@@ -258,3 +258,34 @@ def quaternion_angle(q1, q2) -> float:
     a = np.ascontiguousarray(q1, dtype=np.float64)
     b = np.ascontiguousarray(q2, dtype=np.float64)
     return lib.ref_quaternion_angle(a.ctypes.data_as(L.c_double_p), b.ctypes.data_as(L.c_double_p))
+
+
+def _icp_call(fn, source, reference, theta):
+    from paper_2412_08346_b200.registration import ClosedFormStepResult, _cloud, _pose
+
+    src, ref, th = _cloud(source), _cloud(reference), _pose(theta)
+    out = L.IcpStep()
+    err = C.create_string_buffer(512)
+    fn.argtypes = [L.c_double_p, C.c_int64, L.c_double_p, C.c_int64, L.c_double_p, C.POINTER(L.IcpStep), C.c_char_p,
+                   C.c_size_t]
+    rc = fn(src.ctypes.data_as(L.c_double_p), len(src), ref.ctypes.data_as(L.c_double_p), len(ref),
+            th.ctypes.data_as(L.c_double_p), C.byref(out), err, 512)
+    if rc == L.ASICP_INVALID_ARGUMENT:
+        raise InvalidArgument(err.value.decode())
+    if rc != L.ASICP_OK:
+        raise RuntimeError(err.value.decode())
+    return ClosedFormStepResult(np.array(out.theta[:]), bool(out.degenerate))
+
+
+def icp_closed_form_step(source, reference, theta):
+    """Reference graspmatch::icp_closed_form_step (oracle/_ref)."""
+    return _icp_call(load().ref_icp_closed_form_step, source, reference, theta)
+
+
+def port_icp_closed_form_step(source, reference, theta):
+    """The plain-C restatement (oracle/port/asicp_port.c)."""
+    global _PORT
+    if _PORT is None:
+        _PORT = C.CDLL(str(PORT_PATH))
+        _PORT.port_optimize_grasp.argtypes = [C.POINTER(L.Problem), C.POINTER(L.Solution), C.c_char_p, C.c_size_t]
+    return _icp_call(_PORT.port_icp_closed_form_step, source, reference, theta)

@@ -368,6 +368,30 @@ int ref_register_sgd_icp(const double* source, int64_t n_source, const double* r
   return ASICP_OK;
 }
 
+// graspmatch::icp_closed_form_step (optim.cpp:51-90).
+int ref_icp_closed_form_step(const double* source, int64_t n_source, const double* reference, int64_t n_reference,
+                             const double* theta, asicp_icp_step* out, char* err, size_t errlen) {
+  try {
+    const PointCloud ref = to_cloud(reference, n_reference);
+    PoseParams th;
+    th.t = Vec3(theta[0], theta[1], theta[2]);
+    th.q = Vec4(theta[3], theta[4], theta[5], theta[6]);
+    if (ref.empty()) {  // build_index would throw its own message first; the reference test passes an index
+      copy_err("icp_closed_form_step: empty cloud", err, errlen);
+      return ASICP_INVALID_ARGUMENT;
+    }
+    const NnIndex index = build_index(ref);
+    const ClosedFormStepResult r = icp_closed_form_step(to_cloud(source, n_source), ref, th, index);
+    for (int i = 0; i < 3; ++i) out->theta[i] = r.theta.t[i];
+    for (int i = 0; i < 4; ++i) out->theta[3 + i] = r.theta.q[i];
+    out->degenerate = r.degenerate ? 1 : 0;
+  } catch (const InvalidArgument& e) {
+    copy_err(e.what(), err, errlen);
+    return ASICP_INVALID_ARGUMENT;
+  }
+  return ASICP_OK;
+}
+
 // test_acceptance.cpp:48-52 + 256-282: the C2 trial inputs, from the
 // reference's own generators.
 void ref_c2_trial(int trial, int n, double* source, double* reference, double* truth7) {

@@ -28,8 +28,11 @@ from .grasp import (  # noqa: F401
     optimize_grasp,
 )
 from .registration import (  # noqa: F401
+    ClosedFormStepResult,
     RegistrationBatch,
     RegistrationResult,
     register_sgd_icp,
     register_sgd_icp_batch,
+    icp_closed_form_step,
+    icp_closed_form_step_batch,
 )

@@ -152,6 +152,11 @@ class Registration(C.Structure):
     ]
 
 
+class IcpStep(C.Structure):
+    """asicp_icp_step (graspmatch::ClosedFormStepResult, optim.hpp:82-85)."""
+    _fields_ = [("theta", C.c_double * 7), ("degenerate", C.c_int32)]
+
+
 # Every symbol include/asicp.h + include/asicp_fixtures.h declare.
 EXPORTS = (
     "asicp_abi_version", "asicp_create", "asicp_destroy", "asicp_set_option", "asicp_prepare",
@@ -161,6 +166,7 @@ EXPORTS = (
     "asicp_annealing", "asicp_fx_desk", "asicp_fx_config", "asicp_fx_view", "asicp_fx_free",
     "asicp_fx_cylinder_cloud", "asicp_fx_build_sdf", "asicp_register_sgd_icp", "asicp_register_sgd_icp_batch",
     "asicp_register_prepare", "asicp_register_run", "asicp_fx_c2_trial", "asicp_fx_blob_cloud",
+    "asicp_icp_closed_form_step", "asicp_icp_closed_form_step_batch",
 )
 
 
@@ -213,6 +219,10 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                            c_double_p, C.POINTER(C.c_uint64), C.POINTER(SgdCfg), C.c_char_p,
                                            C.c_size_t]
     lib.asicp_register_run.argtypes = [C.c_void_p, C.POINTER(Registration), C.c_char_p, C.c_size_t]
+    lib.asicp_icp_closed_form_step.argtypes = [C.c_void_p, c_double_p, C.c_int64, c_double_p, C.c_int64, c_double_p,
+                                               C.POINTER(IcpStep), C.c_char_p, C.c_size_t]
+    lib.asicp_icp_closed_form_step_batch.argtypes = [C.c_void_p, C.c_int64, c_double_p, c_i64_p, c_double_p, c_i64_p,
+                                                     c_double_p, C.POINTER(IcpStep), C.c_char_p, C.c_size_t]
     lib.asicp_fx_c2_trial.argtypes = [C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]
     lib.asicp_fx_blob_cloud.argtypes = [C.c_int, C.c_double, C.c_uint64, c_double_p]
     return lib

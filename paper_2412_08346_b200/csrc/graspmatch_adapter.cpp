@@ -234,4 +234,26 @@ RegistrationResult register_sgd_icp(const PointCloud& source, const PointCloud& 
   return out;
 }
 
+// Drop-in definition of graspmatch::icp_closed_form_step (optim.hpp:87-91)
+// in place of optim.cpp:51-90.  The NnIndex argument is not needed: the GPU
+// matches against the reference cloud itself (same answers, the kd-tree's
+// tie rule).
+ClosedFormStepResult icp_closed_form_step(const PointCloud& source, const PointCloud& reference,
+                                          const PoseParams& theta, const NnIndex& /*index*/) {
+  const std::vector<double> src = flatten(source), ref = flatten(reference);
+  const double th[7] = {theta.t[0], theta.t[1], theta.t[2], theta.q[0], theta.q[1], theta.q[2], theta.q[3]};
+  asicp_icp_step r{};
+  char err[512] = {0};
+  const int rc = asicp_icp_closed_form_step(thread_context(), src.data(), static_cast<int64_t>(source.size()),
+                                            ref.data(), static_cast<int64_t>(reference.size()), th, &r, err,
+                                            sizeof(err));
+  if (rc == ASICP_INVALID_ARGUMENT) throw InvalidArgument(err);
+  if (rc != ASICP_OK) throw std::runtime_error(std::string("asicp_icp_closed_form_step: ") + err);
+  ClosedFormStepResult out;
+  out.theta.t = Vec3(r.theta[0], r.theta[1], r.theta[2]);
+  out.theta.q = Vec4(r.theta[3], r.theta[4], r.theta[5], r.theta[6]);
+  out.degenerate = r.degenerate != 0;
+  return out;
+}
+
 }  // namespace graspmatch

@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "dmath.cuh"
+#include "kabsch.cuh"
 #include "mt64.cuh"
 
 #include <cuda_runtime.h>
@@ -599,6 +600,84 @@ __global__ void __launch_bounds__(256) reg_cand_kernel(const double* ref, const 
   }
 }
 
+// graspmatch::icp_closed_form_step (optim.cpp:51-90), one CTA per problem:
+// every source point transformed by theta and matched in the reference (the
+// certified FP32 filter + FP64 check of the registration kernel), the means
+// and the covariance as the reference's sequential sums (one thread each, in
+// source order), then the SVD / Kabsch / quaternion tail on thread 0.
+struct IcpArgs {
+  const double* src;
+  const long long* src_off;
+  const double* ref;
+  const long long* ref_off;
+  const float4* cand;
+  const double* geo;
+  const double* theta;  // n x 7 input poses
+  int* match;           // per source point: matched reference index
+  double* out;          // n x 7
+  int* degenerate;
+};
+
+__global__ void __launch_bounds__(256) icp_step_kernel(IcpArgs a) {
+  const int p = blockIdx.x, tid = threadIdx.x;
+  const long long s0 = a.src_off[p], r0 = a.ref_off[p];
+  const int n_src = static_cast<int>(a.src_off[p + 1] - s0), n_ref = static_cast<int>(a.ref_off[p + 1] - r0);
+  const double* src = a.src + 3 * s0;
+  const double* refg = a.ref + 3 * r0;
+  const float4* candg = a.cand + r0;
+  int* match = a.match + s0;
+  const double* th = a.theta + 7 * static_cast<long long>(p);
+  const double cx = a.geo[4 * p], cy = a.geo[4 * p + 1], cz = a.geo[4 * p + 2], Bp = a.geo[4 * p + 3];
+  __shared__ double s_mean[6], s_cov[9];
+  const M3 R = rotation_matrix(pose_q(th));  // apply_transform (geometry.cpp:68-74); unit norm checked on the host
+  const V3 t = pose_t(th);
+  for (int i = tid; i < n_src; i += blockDim.x) {
+    const V3 q = transform(R, t, load3(src, i));
+    const double ax = q.x - cx, ay = q.y - cy, az = q.z - cz;
+    const double A = sqrt(ax * ax + ay * ay + az * az);
+    double best = INFINITY;
+    int bi = -1;
+    if (!(A < 1e15 && Bp < 1e15)) {
+      for (int k = 0; k < n_ref; ++k) {
+        const double d2 = sqnorm(sub(load3(refg, k), q));
+        if (d2 < best) {
+          best = d2;
+          bi = k;
+        }
+      }
+    } else {
+      nn_window(candg, refg, 0, n_ref, q, __double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az),
+                nn_margin(A, Bp), best, bi);
+    }
+    match[i] = bi < 0 ? 0 : bi;
+  }
+  __syncthreads();
+  const double nd = static_cast<double>(n_src);
+  if (tid < 6) {  // ref_mean += match; src_mean += s (optim.cpp:57-62)
+    double acc = 0.0;
+    if (tid < 3)
+      for (int i = 0; i < n_src; ++i) acc = acc + refg[3 * match[i] + tid];
+    else
+      for (int i = 0; i < n_src; ++i) acc = acc + src[3 * i + tid - 3];
+    s_mean[tid] = acc / nd;
+  }
+  __syncthreads();
+  if (tid < 9) {  // cov += (s - src_mean)(match - ref_mean)^T (optim.cpp:64-66)
+    const int r = tid / 3, c = tid % 3;
+    const double sm = s_mean[3 + r], rm = s_mean[c];
+    double acc = 0.0;
+    for (int i = 0; i < n_src; ++i) acc = acc + (src[3 * i + r] - sm) * (refg[3 * match[i] + c] - rm);
+    s_cov[tid] = acc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    Mat3 cov;
+    for (int i = 0; i < 9; ++i) cov.a[i / 3][i % 3] = s_cov[i];
+    a.degenerate[p] = kabsch_finish(th, V3{s_mean[3], s_mean[4], s_mean[5]}, V3{s_mean[0], s_mean[1], s_mean[2]}, cov,
+                                    n_src, a.out + 7 * static_cast<long long>(p));
+  }
+}
+
 // Host restatements of SgdConfig::validate (optim.cpp:10-15) against the
 // shim's isApprox / LLT (oracle/shim/Eigen/Dense).
 double col_major_norm(const double* A, bool transposed) {
@@ -716,6 +795,8 @@ RegBatch::~RegBatch() { release(); }
 void RegBatch::release() {
   delete d_;
   d_ = nullptr;
+  delete icp_;
+  icp_ = nullptr;
 }
 
 #define REG_CUDA(expr)                                                                    \
@@ -832,6 +913,77 @@ int RegBatch::prepare(int64_t n, const double* sources, const int64_t* src_off, 
                                 static_cast<int>(D.smem)));
   // The upload reads caller memory: finish it before returning.
   REG_CUDA(cudaStreamSynchronize(st_));
+  return ASICP_OK;
+}
+
+int RegBatch::icp_step(int64_t n, const double* sources, const int64_t* src_off, const double* references,
+                       const int64_t* ref_off, const double* thetas, asicp_icp_step* out, std::string* err) {
+  auto invalid = [&](const char* msg) {
+    *err = msg;
+    return ASICP_INVALID_ARGUMENT;
+  };
+  if (n < 0 || n > (1ll << 31) - 1) return invalid("asicp: bad problem count");
+  if (n > 0 && (!src_off || !ref_off || !thetas)) return invalid("asicp: null batch array");
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t ns = src_off[i + 1] - src_off[i], nr = ref_off[i + 1] - ref_off[i];
+    if (ns < 0 || nr < 0) return invalid("asicp: decreasing cloud offsets");
+    if (ns == 0 || nr == 0) return invalid("icp_closed_form_step: empty cloud");
+    if (ns >= (1ll << 31) || nr >= (1ll << 31)) return invalid("asicp: cloud too large");
+    const double* q = thetas + 7 * i + 3;
+    const double n2 = ((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3];
+    if (!(std::abs(std::sqrt(n2) - 1.0) <= 1e-6)) return invalid("rotation_matrix: quaternion is not unit-norm");
+  }
+  if (n == 0) return ASICP_OK;
+  REG_CUDA(cudaSetDevice(device_));
+  if (!icp_) icp_ = new Dev();
+  Dev& D = *icp_;
+  const int64_t tot_src = src_off[n] - src_off[0], tot_ref = ref_off[n] - ref_off[0];
+  std::vector<long long> so(n + 1), ro(n + 1);
+  for (int64_t i = 0; i <= n; ++i) {
+    so[i] = src_off[i] - src_off[0];
+    ro[i] = ref_off[i] - ref_off[0];
+  }
+  REG_CUDA(D.src.ensure(tot_src * 24));
+  REG_CUDA(D.ref.ensure(tot_ref * 24));
+  REG_CUDA(D.src_off.ensure((n + 1) * 8));
+  REG_CUDA(D.ref_off.ensure((n + 1) * 8));
+  REG_CUDA(D.cand.ensure(tot_ref * sizeof(float4)));
+  REG_CUDA(D.geo.ensure(n * 32));
+  REG_CUDA(D.init.ensure(n * 56));
+  REG_CUDA(D.theta.ensure(n * 56));
+  REG_CUDA(D.fy.ensure(tot_src * 4));
+  REG_CUDA(D.status.ensure(n * 4));
+  REG_CUDA(cudaMemcpyAsync(D.src.p, sources + 3 * src_off[0], tot_src * 24, cudaMemcpyHostToDevice, st_));
+  REG_CUDA(cudaMemcpyAsync(D.ref.p, references + 3 * ref_off[0], tot_ref * 24, cudaMemcpyHostToDevice, st_));
+  REG_CUDA(cudaMemcpyAsync(D.src_off.p, so.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st_));
+  REG_CUDA(cudaMemcpyAsync(D.ref_off.p, ro.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st_));
+  REG_CUDA(cudaMemcpyAsync(D.init.p, thetas, n * 56, cudaMemcpyHostToDevice, st_));
+  reg_cand_kernel<<<static_cast<unsigned>(n), 256, 0, st_>>>(static_cast<const double*>(D.ref.p),
+                                                             static_cast<const long long*>(D.ref_off.p),
+                                                             static_cast<float4*>(D.cand.p),
+                                                             static_cast<double*>(D.geo.p));
+  IcpArgs a;
+  a.src = static_cast<const double*>(D.src.p);
+  a.src_off = static_cast<const long long*>(D.src_off.p);
+  a.ref = static_cast<const double*>(D.ref.p);
+  a.ref_off = static_cast<const long long*>(D.ref_off.p);
+  a.cand = static_cast<const float4*>(D.cand.p);
+  a.geo = static_cast<const double*>(D.geo.p);
+  a.theta = static_cast<const double*>(D.init.p);
+  a.match = static_cast<int*>(D.fy.p);
+  a.out = static_cast<double*>(D.theta.p);
+  a.degenerate = static_cast<int*>(D.status.p);
+  icp_step_kernel<<<static_cast<unsigned>(n), 256, 0, st_>>>(a);
+  REG_CUDA(cudaGetLastError());
+  std::vector<double> th(7 * n);
+  std::vector<int> dg(n);
+  REG_CUDA(cudaMemcpyAsync(th.data(), D.theta.p, n * 56, cudaMemcpyDeviceToHost, st_));
+  REG_CUDA(cudaMemcpyAsync(dg.data(), D.status.p, n * 4, cudaMemcpyDeviceToHost, st_));
+  REG_CUDA(cudaStreamSynchronize(st_));
+  for (int64_t i = 0; i < n; ++i) {
+    std::memcpy(out[i].theta, &th[7 * i], 56);
+    out[i].degenerate = dg[i];
+  }
   return ASICP_OK;
 }
 

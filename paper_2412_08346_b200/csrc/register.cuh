@@ -26,6 +26,9 @@ class RegBatch {
   // Solve the prepared batch (synchronous).  A pose that leaves the unit
   // sphere mid-run fails the call like the reference's require.
   int run(asicp_registration* out, std::string* err);
+  // graspmatch::icp_closed_form_step for n independent problems (synchronous).
+  int icp_step(int64_t n, const double* sources, const int64_t* src_off, const double* references,
+               const int64_t* ref_off, const double* thetas, asicp_icp_step* out, std::string* err);
   // Device time of the last run's kernel (ms).
   float last_kernel_ms() const { return kernel_ms_; }
   int launches() const { return 1; }
@@ -36,6 +39,7 @@ class RegBatch {
   int device_;
   cudaStream_t st_;
   Dev* d_ = nullptr;
+  Dev* icp_ = nullptr;
   float kernel_ms_ = 0.0f;
 };
 

@@ -1225,6 +1225,32 @@ int asicp_register_sgd_icp(asicp_ctx* ctx, const double* source, int64_t n_sourc
   return asicp_register_sgd_icp_batch(ctx, 1, source, so, reference, ro, initial, &seed, cfg, result, err, errlen);
 }
 
+int asicp_icp_closed_form_step_batch(asicp_ctx* ctx, int64_t n_problems, const double* sources,
+                                     const int64_t* source_offsets, const double* references,
+                                     const int64_t* reference_offsets, const double* thetas,
+                                     asicp_icp_step* results, char* err, size_t errlen) {
+  if (!ctx) return ASICP_INVALID_ARGUMENT;
+  std::string msg;
+  int rc = ASICP_OK;
+  try {
+    if (!ctx->reg) ctx->reg = std::make_unique<RegBatch>(ctx->device, ctx->stream);
+    rc = ctx->reg->icp_step(n_problems, sources, source_offsets, references, reference_offsets, thetas, results,
+                            &msg);
+  } catch (const std::exception& e) {
+    msg = e.what();
+    rc = ASICP_DEVICE_ERROR;
+  }
+  if (rc != ASICP_OK) copy_err(msg, err, errlen);
+  return rc;
+}
+
+int asicp_icp_closed_form_step(asicp_ctx* ctx, const double* source, int64_t n_source, const double* reference,
+                               int64_t n_reference, const double* theta, asicp_icp_step* result, char* err,
+                               size_t errlen) {
+  const int64_t so[2] = {0, n_source}, ro[2] = {0, n_reference};
+  return asicp_icp_closed_form_step_batch(ctx, 1, source, so, reference, ro, theta, result, err, errlen);
+}
+
 int asicp_get_stats(asicp_ctx* ctx, asicp_stats* stats) {
   if (!ctx || !stats) return ASICP_INVALID_ARGUMENT;
   *stats = ctx->last_stats;

@@ -18,7 +18,7 @@ from . import _lib as L
 from .grasp import PreconditionerMode, SgdConfig, Solver, _check
 
 __all__ = ["RegistrationResult", "register_sgd_icp", "register_sgd_icp_batch", "RegistrationBatch",
-           "sgd_config_struct"]
+           "sgd_config_struct", "ClosedFormStepResult", "icp_closed_form_step", "icp_closed_form_step_batch"]
 
 
 @dataclass
@@ -140,6 +140,48 @@ def register_sgd_icp_batch(sources: Sequence, references: Sequence, initials, cf
             s.ctx, n, _dp(S), so.ctypes.data_as(L.c_i64_p), _dp(R), ro.ctypes.data_as(L.c_i64_p), _dp(init),
             sd.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(c), out, err, 512), err)
         return [_result(out[i]) for i in range(n)]
+    finally:
+        if own:
+            s.close()
+
+
+@dataclass
+class ClosedFormStepResult:
+    """graspmatch::ClosedFormStepResult (optim.hpp:82-85); theta = (t, q)."""
+    theta: np.ndarray
+    degenerate: bool
+
+
+def icp_closed_form_step_batch(sources: Sequence, references: Sequence, thetas, solver: Solver | None = None
+                               ) -> List[ClosedFormStepResult]:
+    """graspmatch::icp_closed_form_step (optim.cpp:51-90) for every (source,
+    reference, theta) at once, one CTA each.  The reference's NnIndex argument
+    is its reference cloud here."""
+    own = solver is None
+    s = Solver() if own else solver
+    try:
+        n, S, so, R, ro, th, _ = _pack(sources, references, thetas, np.zeros(len(sources), dtype=np.uint64))
+        out = (L.IcpStep * max(n, 1))()
+        err = C.create_string_buffer(512)
+        _check(s.lib.asicp_icp_closed_form_step_batch(s.ctx, n, _dp(S), so.ctypes.data_as(L.c_i64_p), _dp(R),
+                                                      ro.ctypes.data_as(L.c_i64_p), _dp(th), out, err, 512), err)
+        return [ClosedFormStepResult(np.array(out[i].theta[:]), bool(out[i].degenerate)) for i in range(n)]
+    finally:
+        if own:
+            s.close()
+
+
+def icp_closed_form_step(source, reference, theta, solver: Solver | None = None) -> ClosedFormStepResult:
+    """graspmatch::icp_closed_form_step (optim.cpp:51-90) on the GPU."""
+    own = solver is None
+    s = Solver() if own else solver
+    try:
+        src, ref, th = _cloud(source), _cloud(reference), _pose(theta)
+        out = L.IcpStep()
+        err = C.create_string_buffer(512)
+        _check(s.lib.asicp_icp_closed_form_step(s.ctx, _dp(src), len(src), _dp(ref), len(ref), _dp(th), C.byref(out),
+                                                err, 512), err)
+        return ClosedFormStepResult(np.array(out.theta[:]), bool(out.degenerate))
     finally:
         if own:
             s.close()

@@ -69,6 +69,16 @@ def main():
                         iterations=np.array(iters, dtype=np.int64), final_loss=np.array(loss),
                         converged=np.array(conv, dtype=np.int32))
     print("wrote registration.npz")
+    # icp_closed_form_step (optim.cpp:51-90).
+    names, theta, degen = [], [], []
+    for name, src, rf, th in reg_cases.icp_cases():
+        r = ref.icp_closed_form_step(src, rf, th)
+        names.append(name)
+        theta.append(r.theta)
+        degen.append(int(r.degenerate))
+    np.savez_compressed(OUT / "icp_step.npz", names=np.array(names), theta=np.array(theta),
+                        degenerate=np.array(degen, dtype=np.int32))
+    print("wrote icp_step.npz")
 
 
 if __name__ == "__main__":

@@ -84,3 +84,40 @@ def unit_cases():
 
 def all_cases():
     return c2_cases() + unit_cases()
+
+
+def icp_cases():
+    """icp_closed_form_step inputs: test_optim.cpp:69-124 and variants that
+    reach every branch of the SVD / Kabsch / quaternion tail."""
+    cases = []
+    blob = fixtures.blob_cloud(100, 0.05, 41)
+    cases.append(("aligned", blob, blob.copy(), IDENTITY))
+    src = fixtures.blob_cloud(200, 0.05, 42)
+    cases.append(("translation", src, src + np.array([0.01, 0.0, 0.0]), IDENTITY))
+    cases.append(("single_point", np.array([[0.0, 0.0, 0.0]]), np.array([[0.05, 0.0, 0.0]]), IDENTITY))
+    cases.append(("two_points", src[:2], src[:2] + 0.01, IDENTITY))
+    rng = np.random.default_rng(43)
+    s120, r150 = fixtures.blob_cloud(120, 0.05, 44), fixtures.blob_cloud(150, 0.06, 45)
+    for k in range(6):
+        q = _normalized(np.concatenate([[1.0], rng.normal(scale=0.3, size=3)]))
+        cases.append((f"random_pose_{k}", s120, r150, np.concatenate([rng.normal(scale=0.03, size=3), q])))
+    for k in range(3):  # large rotations: the other Shepperd branches
+        q = _normalized(rng.normal(size=4))
+        s2, r2, _ = fixtures.c2_trial(k)
+        cases.append((f"c2_big_rotation_{k}", s2, r2, np.concatenate([[0.0, 0.0, 0.0], q])))
+    # Exact 150-degree rotations about x, y, z started at the truth: the
+    # Kabsch rotation has a negative trace (the three non-trace branches).
+    for ax in range(3):
+        half = np.deg2rad(150.0) / 2.0
+        q = np.zeros(4)
+        q[0] = np.cos(half)
+        q[1 + ax] = np.sin(half)
+        q = _normalized(q)
+        truth = np.concatenate([[0.01, -0.02, 0.005], q])
+        cases.append((f"rot150_axis{ax}", s120, _apply(truth, s120), truth))
+    g = np.stack(np.meshgrid(np.linspace(-0.05, 0.05, 7), np.linspace(-0.03, 0.03, 5)), -1).reshape(-1, 2)
+    plane = np.concatenate([g, np.zeros((len(g), 1))], axis=1)
+    cases.append(("planar", plane, plane + np.array([0.001, -0.002, 0.003]), IDENTITY))
+    line = np.outer(np.linspace(-0.05, 0.05, 9), [1.0, 0.5, 0.25])
+    cases.append(("collinear", line, line + 0.01, IDENTITY))
+    return cases

@@ -5,8 +5,8 @@ doctest suite (103 cases) and acceptance binary (criteria C1-C9) linked against
 paper_2412_08346_b200/csrc/graspmatch_adapter.cpp — i.e. every
 graspmatch::optimize_grasp call in them (test_grasp.cpp:348-458, acceptance C7
 desk grasp over 10 seeds and C9 worker-count determinism) and every
-graspmatch::register_sgd_icp call (test_optim.cpp:540-584, acceptance C2's 20
-recovery trials) runs on the B200 through the C-ABI.  Built here by `make -C oracle dropin`; the binaries travel
+graspmatch::register_sgd_icp / icp_closed_form_step call (test_optim.cpp:69-124,
+540-584, acceptance C2's 20 recovery trials) runs on the B200 through the C-ABI.  Built here by `make -C oracle dropin`; the binaries travel
 to the GPU box with the repo.
 """
 import subprocess

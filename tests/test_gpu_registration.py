@@ -131,3 +131,53 @@ def test_errors_match_reference(solver, case):
 
 def test_empty_batch(solver):
     assert register_sgd_icp_batch([], [], np.zeros((0, 7)), SgdConfig(), [], solver=solver) == []
+
+
+# ---------------------------------------------------------------------------
+# icp_closed_form_step (optim.cpp:51-90)
+# ---------------------------------------------------------------------------
+from paper_2412_08346_b200 import icp_closed_form_step, icp_closed_form_step_batch  # noqa: E402
+
+ICP_GOLDEN = Path(__file__).resolve().parent / "golden" / "icp_step.npz"
+
+
+@pytest.fixture(scope="module")
+def icp_golden():
+    g = np.load(ICP_GOLDEN)
+    return {str(n): (g["theta"][i], bool(g["degenerate"][i])) for i, n in enumerate(g["names"])}
+
+
+def test_icp_step_batch_matches_reference(solver, icp_golden):
+    cases = reg_cases.icp_cases()
+    res = icp_closed_form_step_batch([c[1] for c in cases], [c[2] for c in cases], [c[3] for c in cases],
+                                     solver=solver)
+    for c, r in zip(cases, res):
+        assert np.array_equal(r.theta, icp_golden[c[0]][0]), c[0]
+        assert r.degenerate == icp_golden[c[0]][1], c[0]
+
+
+def test_icp_step_chain_matches_port(solver):
+    """Ten chained steps (test_optim.cpp:79-95) and a large-cloud case
+    (reference beyond any shared-memory stage)."""
+    src = fixtures.blob_cloud(200, 0.05, 42)
+    rf = src + np.array([0.01, 0.0, 0.0])
+    a = b = reg_cases.IDENTITY
+    for _ in range(10):
+        a = icp_closed_form_step(src, rf, a, solver=solver).theta
+        b = ref.port_icp_closed_form_step(src, rf, b).theta if ref.port_available() else a
+        assert np.array_equal(a, b)
+    big_s, big_r = fixtures.blob_cloud(6000, 0.08, 7), fixtures.blob_cloud(9000, 0.08, 8)
+    got = icp_closed_form_step(big_s, big_r, reg_cases.IDENTITY, solver=solver)
+    if ref.port_available():
+        want = ref.port_icp_closed_form_step(big_s, big_r, reg_cases.IDENTITY)
+        assert np.array_equal(got.theta, want.theta) and got.degenerate == want.degenerate
+
+
+def test_icp_step_errors(solver):
+    src = np.zeros((5, 3))
+    bad = reg_cases.IDENTITY.copy()
+    bad[3] = 1.2
+    with pytest.raises(InvalidArgument, match="icp_closed_form_step: empty cloud"):
+        icp_closed_form_step(np.zeros((0, 3)), src, reg_cases.IDENTITY, solver=solver)
+    with pytest.raises(InvalidArgument, match="quaternion is not unit-norm"):
+        icp_closed_form_step(src, src + 1.0, bad, solver=solver)
