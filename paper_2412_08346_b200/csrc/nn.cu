@@ -174,11 +174,11 @@ __device__ __forceinline__ int nn_decide(const NnGeom& g, const int* pos, int n,
 
 // Ambiguous-window member lists: a block of kWinCap (position, d32) entries
 // per ambiguous query, allocated from a pool; amb_n > kWinCap marks overflow.
-__device__ __forceinline__ int win_alloc(DevState& S) {
+__device__ __forceinline__ int win_alloc(const DevState& S) {
   const int b = atomicAdd(S.amb_count, 1);
   return b < S.amb_cap ? b : -1;
 }
-__device__ __forceinline__ void win_push(DevState& S, int blk, int pos, float d) {
+__device__ __forceinline__ void win_push(const DevState& S, int blk, int pos, float d) {
   const int n = S.amb_n[blk];
   if (n < kWinCap) S.amb_pool[static_cast<int64_t>(blk) * kWinCap + n] = make_int2(pos, __float_as_int(d));
   S.amb_n[blk] = n + 1;
@@ -210,7 +210,7 @@ __device__ __forceinline__ bool win_collect(const DevState& S, int p1, float thr
 // stats[5 + kind]: rescans per match kind; stats[8 + reason]: 0 validation
 // mode, 1 ambiguous window, 3 ambiguous across splits; stats[16 + k]: rescans
 // in iteration k.
-__device__ __forceinline__ void push_refine(DevState& S, int kind, int j, int qlocal, int reason, int iter) {
+__device__ __forceinline__ void push_refine(const DevState& S, int kind, int j, int qlocal, int reason, int iter) {
   const int slot = atomicAdd(S.refine_count, 1);
   if (slot < S.refine_cap) S.refine_list[slot] = make_int4(kind, j, qlocal, 0);
   atomicAdd(S.stats + 1, 1ull);
@@ -275,6 +275,118 @@ __device__ __forceinline__ float half2f(f32x2 v, int k) {
   return (k & 1) ? hi : lo;
 }
 
+// Running window of one query (position / ambiguous-list state).
+struct RunState {
+  float b;
+  int p;
+};
+
+// Sub-chunk epilogue of one query, out of line: the kernel keeps one copy of
+// this code instead of Q unrolled ones.  At small candidate counts (early
+// minibatch iterations) the instruction fetch of the unrolled copies, not the
+// arithmetic, set the launch time.  Members of the sub-chunk's window and the
+// position of its minimum are merged into the running window (an explicit
+// member list only once it holds two).
+__device__ __noinline__ RunState subchunk_window(const DevState& S, const float4* tiles, int base, float qx,
+                                                 float qy, float qz, float b1, float b2, float b3, int s12, float mg,
+                                                 RunState run) {
+  RunState out = run;
+  {
+        const float thr = __fadd_ru(b1, mg);
+        bool ovf = b3 <= thr;
+        int pmin = -1, np = 0;
+        int mpos[kWinCap];
+        float md[kWinCap];
+        const int nscan = b2 <= thr ? 2 : 1;
+                for (int r = 0; r < nscan; ++r) {
+          const int sid = r == 0 ? (s12 & 0xffff) : (s12 >> 16);
+          const float4* sp = tiles + sid * kSub;
+          for (int c = 0; c < kSub; c += 2) {
+            // One interleaved pair (two LDS.128): candidates c and c + 1.
+            const float4 A = sp[c], B = sp[c + 1];
+            const float dd[2] = {d32(qx, qy, qz, make_float4(A.x, A.z, B.x, B.z)),
+                                 d32(qx, qy, qz, make_float4(A.y, A.w, B.y, B.w))};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float d = dd[h];
+              if (d <= thr) {
+                const int p = base + sid * kSub + c + h;
+                if (np < kWinCap) {
+                  mpos[np] = p;
+                  md[np] = d;
+                }
+                ++np;
+                if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
+              }
+            }
+          }
+        }
+        ovf = ovf || np > kWinCap;
+        const float run_b = run.b;
+        const int run_p = run.p;
+        if (b1 < run_b) {
+          // New best: old members stay in the window only if the old best is
+          // still within the new margin.
+          const bool keep_old = run_b <= thr;
+          if (!keep_old && np == 1 && !ovf) {
+            out.p = pmin;
+          } else {
+            // The running window is certified (run_p a position), listed (a
+            // block of the pool) or listless (the pool ran out: kNoBlock).  A
+            // listless window that stays inside the new margin keeps the query
+            // listless; otherwise a fresh block takes the new members.
+            const bool was_amb = (run_p & kAmbiguous) != 0;
+            const bool old_listed = was_amb && (run_p & ~kAmbiguous) != kNoBlock;
+            int blk = -1;
+            if (old_listed)
+              blk = run_p & ~kAmbiguous;
+            else if (!(was_amb && keep_old))
+              blk = win_alloc(S);
+            if (blk >= 0) {
+              if (!old_listed) {
+                S.amb_n[blk] = 0;
+                if (keep_old) win_push(S, blk, run_p, run_b);  // certified old best (was_amb is false here)
+              } else if (!keep_old) {
+                S.amb_n[blk] = 0;
+              }
+              for (int e = 0; e < min(np, kWinCap); ++e) win_push(S, blk, mpos[e], md[e]);
+              if (ovf) S.amb_n[blk] = kWinCap + 1;
+            }
+            out.p = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
+          }
+          out.b = b1;
+        } else if (b1 <= __fadd_ru(run_b, mg)) {
+          const float run_thr = __fadd_ru(run_b, mg);
+          int blk = (run_p & kAmbiguous) ? (run_p & ~kAmbiguous) : win_alloc(S);
+          if (blk >= 0 && blk != kNoBlock) {
+            if (!(run_p & kAmbiguous)) {
+              S.amb_n[blk] = 0;
+              win_push(S, blk, run_p, run_b);
+            }
+            for (int e = 0; e < min(np, kWinCap); ++e)
+              if (md[e] <= run_thr) win_push(S, blk, mpos[e], md[e]);
+            if (ovf) S.amb_n[blk] = kWinCap + 1;
+          }
+          out.p = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
+        }
+      }
+  return out;
+}
+
+// Emit of an ambiguous query (out of line, see subchunk_window): decide the
+// window members in FP64 with the reference formula, or queue a full rescan.
+__device__ __noinline__ void emit_ambiguous(const DevProblem& P, const DevState& S, const NnPlan& plan, int kind,
+                                            int owner, int qlocal, int p1, float thr) {
+  int pos[kWinCap];
+  int n = 0;
+  if (win_collect(S, p1, thr, pos, &n, kWinCap)) {
+    const NnGeom g = nn_geom(P, S, plan, kind, owner, qlocal);
+    *nn_result_slot(P, S, kind, owner, qlocal) = nn_decide(g, pos, n, kind == 0 && !plan.pooled, S.stats);
+  } else {
+    push_refine(S, kind, owner, qlocal, 1, plan.iter);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // The filter kernel (persistent over one work list).
 // ---------------------------------------------------------------------------
@@ -286,7 +398,8 @@ template <int Q>
 #define ASICP_NN_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
-    nn_filter_kernel(DevProblem P, DevState S, NnPlan plan, int list) {
+    nn_filter_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevState S,
+                     const __grid_constant__ NnPlan plan, int list) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float4* tiles = reinterpret_cast<float4*>(smem_raw);
   __shared__ __align__(8) uint64_t full_bar[kNnStages];
@@ -419,84 +532,10 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
       // running window (an explicit member list only once it holds two).
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
-        const float thr = __fadd_ru(b1[k], MG(k));
-        bool ovf = b3[k] <= thr;
-        int pmin = -1, np = 0;
-        int mpos[kWinCap];
-        float md[kWinCap];
-        const int nscan = b2[k] <= thr ? 2 : 1;
-        const int base = w.c_base + sc0;
-        for (int r = 0; r < nscan; ++r) {
-          const int sid = r == 0 ? (s12[k] & 0xffff) : (s12[k] >> 16);
-          const float4* sp = tiles + sid * kSub;
-          for (int c = 0; c < kSub; c += 2) {
-            // One interleaved pair (two LDS.128): candidates c and c + 1.
-            const float4 A = sp[c], B = sp[c + 1];
-            const float dd[2] = {d32(qx[k], qy[k], qz[k], make_float4(A.x, A.z, B.x, B.z)),
-                                 d32(qx[k], qy[k], qz[k], make_float4(A.y, A.w, B.y, B.w))};
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const float d = dd[h];
-              if (d <= thr) {
-                const int p = base + sid * kSub + c + h;
-                if (np < kWinCap) {
-                  mpos[np] = p;
-                  md[np] = d;
-                }
-                ++np;
-                if (d == b1[k] && (pmin < 0 || p < pmin)) pmin = p;
-              }
-            }
-          }
-        }
-        ovf = ovf || np > kWinCap;
-        const float run_b = B1(k);
-        const int run_p = P1(k);
-        if (b1[k] < run_b) {
-          // New best: old members stay in the window only if the old best is
-          // still within the new margin.
-          const bool keep_old = run_b <= thr;
-          if (!keep_old && np == 1 && !ovf) {
-            P1(k) = pmin;
-          } else {
-            // The running window is certified (run_p a position), listed (a
-            // block of the pool) or listless (the pool ran out: kNoBlock).  A
-            // listless window that stays inside the new margin keeps the query
-            // listless; otherwise a fresh block takes the new members.
-            const bool was_amb = (run_p & kAmbiguous) != 0;
-            const bool old_listed = was_amb && (run_p & ~kAmbiguous) != kNoBlock;
-            int blk = -1;
-            if (old_listed)
-              blk = run_p & ~kAmbiguous;
-            else if (!(was_amb && keep_old))
-              blk = win_alloc(S);
-            if (blk >= 0) {
-              if (!old_listed) {
-                S.amb_n[blk] = 0;
-                if (keep_old) win_push(S, blk, run_p, run_b);  // certified old best (was_amb is false here)
-              } else if (!keep_old) {
-                S.amb_n[blk] = 0;
-              }
-              for (int e = 0; e < min(np, kWinCap); ++e) win_push(S, blk, mpos[e], md[e]);
-              if (ovf) S.amb_n[blk] = kWinCap + 1;
-            }
-            P1(k) = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
-          }
-          B1(k) = b1[k];
-        } else if (b1[k] <= __fadd_ru(run_b, MG(k))) {
-          const float run_thr = __fadd_ru(run_b, MG(k));
-          int blk = (run_p & kAmbiguous) ? (run_p & ~kAmbiguous) : win_alloc(S);
-          if (blk >= 0 && blk != kNoBlock) {
-            if (!(run_p & kAmbiguous)) {
-              S.amb_n[blk] = 0;
-              win_push(S, blk, run_p, run_b);
-            }
-            for (int e = 0; e < min(np, kWinCap); ++e)
-              if (md[e] <= run_thr) win_push(S, blk, mpos[e], md[e]);
-            if (ovf) S.amb_n[blk] = kWinCap + 1;
-          }
-          P1(k) = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
-        }
+        const RunState r = subchunk_window(S, tiles, w.c_base + sc0, qx[k], qy[k], qz[k], b1[k], b2[k], b3[k], s12[k],
+                                           MG(k), RunState{B1(k), P1(k)});
+        B1(k) = r.b;
+        P1(k) = r.p;
       }
       __syncthreads();  // all rescans done before the next sub-chunk overwrites the tiles
     }
@@ -513,17 +552,7 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
         } else if (!(p1 & kAmbiguous)) {
           *nn_result_slot(P, S, w.kind, w.owner, qlocal) = p1;  // certified
         } else {
-          // Ambiguous: decide the window members in FP64 (reference formula).
-          const float thr = __fadd_ru(B1(k), MG(k));
-          int pos[kWinCap];
-          int n = 0;
-          if (win_collect(S, p1, thr, pos, &n, kWinCap)) {
-            const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
-            *nn_result_slot(P, S, w.kind, w.owner, qlocal) =
-                nn_decide(g, pos, n, w.kind == 0 && !plan.pooled, S.stats);
-          } else {
-            push_refine(S, w.kind, w.owner, qlocal, 1, plan.iter);
-          }
+          emit_ambiguous(P, S, plan, w.kind, w.owner, qlocal, p1, __fadd_ru(B1(k), MG(k)));
         }
       } else {
         NnPartial pr;
