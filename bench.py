@@ -375,6 +375,8 @@ def run_registration(args):
     ms_max = all_max(float(np.mean([a.elapsed_time(b) for a, b in ev])))
     value = world * n / (ms_max * 1e-3)
 
+    for _ in range(args.warmup):  # untimed end-to-end warm-ups (host allocator first touch)
+        register_sgd_icp_batch(srcs, refs, inits, cfg, seeds, solver=solver)
     e2e_ms = []
     for k in range(max(1, args.steps)):
         barrier()
@@ -383,7 +385,8 @@ def run_registration(args):
         t0 = time.perf_counter()
         e2e_res = register_sgd_icp_batch(srcs, refs, inits, cfg, seeds, solver=solver)
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-    e2e_max = all_max(float(np.mean(e2e_ms)))
+    e2e_max = all_max(float(np.median(e2e_ms)))  # median: see the grasp workloads below
+    e2e_mean = all_max(float(np.mean(e2e_ms)))
     same_e2e = all(np.array_equal(a.theta, b.theta) for a, b in zip(result, e2e_res))
 
     lib = L.load()
@@ -402,7 +405,9 @@ def run_registration(args):
             "registration_iterations_per_s": world * iters / (ms_max * 1e-3),
             "e2e": {"value": world * n / (e2e_max * 1e-3), "unit": REG_UNIT,
                     "h2d_bytes_per_step": batch.input_bytes, "d2h_bytes_per_step": batch.output_bytes,
-                    "latency_ms": e2e_max, "steps_ms": e2e_ms, "bit_identical_to_resident": same_e2e},
+                    "latency_ms": e2e_max, "stat": "median of the K steps (max over ranks)",
+                    "mean_latency_ms": e2e_mean, "mean_value": world * n / (e2e_mean * 1e-3),
+                    "steps_ms": e2e_ms, "bit_identical_to_resident": same_e2e},
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "roofline": {"bound": "fp64", "kernel": "register_kernel", "achieved": achieved, "peak": peak,
@@ -576,6 +581,12 @@ def main():
     launches = launches_of()
 
     # ---- end-to-end through the public API with host buffers ----
+    # W untimed end-to-end warm-ups first: the first few host-side prepares
+    # run into fresh-page faults of the host allocator (tools/prepare_timing.py).
+    for _ in range(args.warmup):
+        barrier()
+        solve_e2e()
+    e2e_split.clear()
     e2e_ms, e2e_dev_ms = [], []
     for k in range(max(1, args.steps)):
         barrier()
@@ -586,7 +597,11 @@ def main():
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
         if not batch:
             e2e_dev_ms.append(solver.stats().solve_ms)
-    e2e_max = all_max(float(np.mean(e2e_ms)))
+    # Median over the K end-to-end steps: the host side of a step (validate +
+    # pageable H2D) sees sporadic multi-ms stalls on these boxes that are not
+    # the library's (tools/prepare_timing.py); the mean is reported beside it.
+    e2e_max = all_max(float(np.median(e2e_ms)))
+    e2e_mean = all_max(float(np.mean(e2e_ms)))
     e2e_value = pits_total / (e2e_max * 1e-3)
 
     # ---- roofline of the dominant kernel (NN filter), profiled run on one problem ----
@@ -622,7 +637,9 @@ def main():
             "solve_latency_ms": ms_max,
             "paper_latency_ms": PAPER_LATENCY_S * 1e3,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "latency_ms": e2e_max, "steps_ms": e2e_ms, "device_solve_ms": e2e_dev_ms,
+                    "latency_ms": e2e_max, "stat": "median of the K steps (max over ranks)",
+                    "mean_latency_ms": e2e_mean, "mean_value": pits_total / (e2e_mean * 1e-3),
+                    "steps_ms": e2e_ms, "device_solve_ms": e2e_dev_ms,
                     "prepare_run_ms": e2e_split},
             "gpu_launches": int(launches) * args.steps,
             "clocks": clk.summary(),

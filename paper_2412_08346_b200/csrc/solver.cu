@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -302,7 +303,17 @@ void validate(const asicp_problem& p) {
 }
 
 void prepare(asicp_ctx* c, const asicp_problem& p) {
+  // ASICP_PREPARE_TIMING=1: host-side section times to stderr (diagnostics).
+  static const bool timing = std::getenv("ASICP_PREPARE_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "prepare %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   validate(p);
+  mark("validate");
   CUDA_OK(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   const int n_pre = static_cast<int>(p.n_preshapes);
@@ -405,8 +416,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     d.coarse_offset = coarse_total;
     coarse_total += static_cast<int64_t>(d.cdims[0]) * d.cdims[1] * d.cdims[2];
   }
+  mark("host-build");
   upload(c->grids, grids.data(), grids.size(), st);
   upload(c->sdf_values, values.data(), values.size(), st);
+  mark("sdf-upload");
   c->sdf_coarse.ensure(static_cast<size_t>(std::max<int64_t>(coarse_total, 1)) * sizeof(float));
   launch_grid_bounds(c->grids.as<Grid>(), static_cast<int>(p.n_sdf_grids), c->sdf_values.as<float>(),
                      c->sdf_coarse.as<float>(), st);
@@ -545,7 +558,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   // Parallel Fisher-Yates scratch (5 int arrays per particle) when it takes at
   // most a quarter of the free HBM; the serial kernel covers the rest.
   size_t free_b = 0, total_b = 0;
+  mark("particles");
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  mark("memgetinfo");
   const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
   // (The parallel kernel takes draws of m <= 20480 per call; larger m and an
   // absent scratch fall back to the serial kernel.)
@@ -700,7 +715,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.trace_col = c->trace_col.as<int>();
   S.final_loss = c->final_loss.as<double>();
   S.final_free = c->final_free.as<int>();
+  mark("buffers");
   CUDA_OK(cudaStreamSynchronize(st));
+  mark("sync");
   // The captured graph bakes DevProblem/DevState and the k schedule into its
   // kernel parameters: keep it only if all of them are unchanged.
   std::vector<char> sig(sizeof(DevProblem) + sizeof(DevState));
