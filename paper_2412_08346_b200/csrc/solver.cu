@@ -139,6 +139,8 @@ struct asicp_ctx {
   int med_big_grid = 0, max_gpop = 0;
   double* host_gath = nullptr;
   size_t host_gath_bytes = 0;
+  char* pin = nullptr;  // pinned upload staging (upload())
+  size_t pin_cap = 0, pin_off = 0;
 
   DevProblem P{};
   DevState S{};
@@ -213,6 +215,7 @@ struct asicp_ctx {
     if (in_flight && stream) cudaStreamSynchronize(stream);
     free_staging();
     if (host_gath) cudaFreeHost(host_gath);
+    if (pin) cudaFreeHost(pin);
     xchg.reset();
     reg.reset();
     Buf* shard_bufs[] = {&theta_all, &drift_all, &xsend,    &xrecv,  &fsend, &frecv,
@@ -242,10 +245,34 @@ struct asicp_ctx {
 
 namespace {
 
+// Host -> device through the ctx's pinned staging buffer: a memcpy into
+// pinned memory, then a true async DMA.  Pageable copies made the driver pin
+// pages on the fly, and asicp_prepare's time varied from 1 to 80 ms on the
+// bench boxes (tools/prepare_timing.py).  Staged copies stay in flight until
+// the stream synchronizes at the end of asicp_prepare; a full buffer
+// synchronizes and restarts.
 template <typename T>
-void upload(Buf& b, const T* src, size_t n, cudaStream_t st) {
+void upload(asicp_ctx* c, Buf& b, const T* src, size_t n, cudaStream_t st) {
+  const size_t bytes = n * sizeof(T);
   b.ensure(std::max<size_t>(n, 1) * sizeof(T));
-  if (n) CUDA_OK(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, st));
+  if (!n) return;
+  const size_t need = (bytes + 255) / 256 * 256;
+  if (c->pin_off + need > c->pin_cap) {
+    CUDA_OK(cudaStreamSynchronize(st));
+    c->pin_off = 0;
+    if (need > c->pin_cap) {
+      if (c->pin) cudaFreeHost(c->pin);
+      c->pin = nullptr;
+      c->pin_cap = 0;
+      const size_t cap = std::max<size_t>(need, size_t(16) << 20);
+      CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&c->pin), cap));
+      c->pin_cap = cap;
+    }
+  }
+  char* dst = c->pin + c->pin_off;
+  std::memcpy(dst, src, bytes);
+  CUDA_OK(cudaMemcpyAsync(b.p, dst, bytes, cudaMemcpyHostToDevice, st));
+  c->pin_off += need;
 }
 
 // GraspProblem::validate (grasp.cpp:20-31) + Preshape::validate (:13-18),
@@ -314,6 +341,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   };
   validate(p);
   mark("validate");
+  c->pin_off = 0;
   CUDA_OK(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
   const int n_pre = static_cast<int>(p.n_preshapes);
@@ -354,9 +382,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
   }
   for (int64_t i = p.n_object; i < c->n_obj_pad; ++i) put(i, 0.0f, 0.0f, 0.0f, INFINITY);
-  upload(c->obj64, obj.data(), obj.size(), st);
-  upload(c->obj_cand, cand.data(), cand.size(), st);
-  upload(c->scene64, p.scene_cloud, 3 * p.n_scene, st);
+  upload(c, c->obj64, obj.data(), obj.size(), st);
+  upload(c, c->obj_cand, cand.data(), cand.size(), st);
+  upload(c, c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
     std::vector<float4> s32(p.n_scene);
     for (int64_t i = 0; i < p.n_scene; ++i) {
@@ -368,7 +396,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
                         std::fabs(static_cast<double>(z));
       s32[i] = make_float4(x, y, z, std::nextafter(static_cast<float>(l1), INFINITY));
     }
-    upload(c->scene32, s32.data(), s32.size(), st);
+    upload(c, c->scene32, s32.data(), s32.size(), st);
   }
 
   // Preshapes.
@@ -386,10 +414,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     c->max_ns = std::max(c->max_ns, static_cast<int>(s.n_surface));
   }
   pre_off[n_pre] = static_cast<int>(surf.size() / 3);
-  upload(c->surf64, surf.data(), surf.size(), st);
-  upload(c->pre_surf_off, pre_off.data(), pre_off.size(), st);
-  upload(c->pre_tcp, tcp.data(), tcp.size(), st);
-  upload(c->pre_sdf, pre_sdf.data(), pre_sdf.size(), st);
+  upload(c, c->surf64, surf.data(), surf.size(), st);
+  upload(c, c->pre_surf_off, pre_off.data(), pre_off.size(), st);
+  upload(c, c->pre_tcp, tcp.data(), tcp.size(), st);
+  upload(c, c->pre_sdf, pre_sdf.data(), pre_sdf.size(), st);
 
   // SDF grids.
   std::vector<Grid> grids(p.n_sdf_grids);
@@ -417,8 +445,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     coarse_total += static_cast<int64_t>(d.cdims[0]) * d.cdims[1] * d.cdims[2];
   }
   mark("host-build");
-  upload(c->grids, grids.data(), grids.size(), st);
-  upload(c->sdf_values, values.data(), values.size(), st);
+  upload(c, c->grids, grids.data(), grids.size(), st);
+  upload(c, c->sdf_values, values.data(), values.size(), st);
   mark("sdf-upload");
   c->sdf_coarse.ensure(static_cast<size_t>(std::max<int64_t>(coarse_total, 1)) * sizeof(float));
   launch_grid_bounds(c->grids.as<Grid>(), static_cast<int>(p.n_sdf_grids), c->sdf_values.as<float>(),
@@ -472,10 +500,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->rows_per_rank = static_cast<int>((Jg + world - 1) / world);
   c->total_surf = so;
   c->part_pre = part_pre_glob;
-  upload(c->part_pre_d, part_pre.data(), part_pre.size(), st);
-  upload(c->part_pop, part_pop.data(), part_pop.size(), st);
-  upload(c->pop_off, pop_off.data(), pop_off.size(), st);
-  upload(c->gpop_off_d, gpop_off.data(), gpop_off.size(), st);
+  upload(c, c->part_pre_d, part_pre.data(), part_pre.size(), st);
+  upload(c, c->part_pop, part_pop.data(), part_pop.size(), st);
+  upload(c, c->pop_off, pop_off.data(), pop_off.size(), st);
+  upload(c, c->gpop_off_d, gpop_off.data(), gpop_off.size(), st);
   // Split SVGD (kernel matrix, then ordered sums) while the K x K_local
   // matrices stay under 8 M pairs (128 MB); the fused kernel otherwise.
   std::vector<long long> kofs(n_pre, 0);
@@ -488,8 +516,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   }
   const bool svgd_split = c->k_stein > 0 && ktot > 0 && ktot <= (8ll << 20);
   if (svgd_split) c->kmat.ensure(static_cast<size_t>(ktot) * sizeof(double2));
-  upload(c->kofs_d, kofs.data(), kofs.size(), st);
-  upload(c->pop_logk1, logk1.data(), logk1.size(), st);
+  upload(c, c->kofs_d, kofs.data(), kofs.size(), st);
+  upload(c, c->pop_logk1, logk1.data(), logk1.size(), st);
   // Median select: populations below kMedBigK in one CTA (median.cu), larger
   // ones grid-wide over 128 x 128 tiles of the pair triangle (kernels.cu).
   long long big_tiles = 0;
@@ -503,9 +531,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->med_big_grid = static_cast<int>(std::min<long long>(big_tiles, 8ll * c->num_sms));
   c->med_hist.ensure(static_cast<size_t>(n_pre) * 4096 * 4);
   c->med_state.ensure(static_cast<size_t>(n_pre) * sizeof(MedState));
-  upload(c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
+  upload(c, c->part_surf_off, part_surf_off.data(), part_surf_off.size(), st);
   c->init_theta.assign(p.init_poses + 7 * static_cast<int64_t>(lo), p.init_poses + 7 * static_cast<int64_t>(hi));
-  upload(c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
+  upload(c, c->init_theta_d, c->init_theta.data(), c->init_theta.size(), st);
 
   // Schedules (host-exact: llround / fmod / pow of the reference).
   c->ms.resize(c->k_max);
