@@ -275,6 +275,12 @@ __device__ __forceinline__ float half2f(f32x2 v, int k) {
   return (k & 1) ? hi : lo;
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+
 // Running window of one query (position / ambiguous-list state).
 struct RunState {
   float b;
@@ -298,27 +304,38 @@ __device__ __noinline__ RunState subchunk_window(const DevState& S, const float4
         int mpos[kWinCap];
         float md[kWinCap];
         const int nscan = b2 <= thr ? 2 : 1;
-                for (int r = 0; r < nscan; ++r) {
+        // Window members of the best one or two subtiles: a member bitmask
+        // from one pass of shared-memory loads (the tiles are shared; this
+        // out-of-line function sees a generic pointer, hence ld.shared by
+        // address), then the members in increasing position.
+        const uint32_t tiles_s = static_cast<uint32_t>(__cvta_generic_to_shared(tiles));
+        for (int r = 0; r < nscan; ++r) {
           const int sid = r == 0 ? (s12 & 0xffff) : (s12 >> 16);
-          const float4* sp = tiles + sid * kSub;
+          const uint32_t sp = tiles_s + static_cast<uint32_t>(sid * kSub) * 16u;
+          unsigned mask = 0;
+#pragma unroll 8
           for (int c = 0; c < kSub; c += 2) {
-            // One interleaved pair (two LDS.128): candidates c and c + 1.
-            const float4 A = sp[c], B = sp[c + 1];
-            const float dd[2] = {d32(qx, qy, qz, make_float4(A.x, A.z, B.x, B.z)),
-                                 d32(qx, qy, qz, make_float4(A.y, A.w, B.y, B.w))};
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const float d = dd[h];
-              if (d <= thr) {
-                const int p = base + sid * kSub + c + h;
-                if (np < kWinCap) {
-                  mpos[np] = p;
-                  md[np] = d;
-                }
-                ++np;
-                if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
-              }
+            // One interleaved pair (two 16-byte loads): candidates c and c + 1.
+            const float4 A = lds128(sp + c * 16u), B = lds128(sp + (c + 1) * 16u);
+            const float d0 = d32(qx, qy, qz, make_float4(A.x, A.z, B.x, B.z));
+            const float d1 = d32(qx, qy, qz, make_float4(A.y, A.w, B.y, B.w));
+            mask |= (d0 <= thr ? 1u : 0u) << c;
+            mask |= (d1 <= thr ? 1u : 0u) << (c + 1);
+          }
+          while (mask) {
+            const int c = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const uint32_t cp = static_cast<uint32_t>(c & ~1);
+            const float4 A = lds128(sp + cp * 16u), B = lds128(sp + (cp + 1) * 16u);
+            const float d = (c & 1) ? d32(qx, qy, qz, make_float4(A.y, A.w, B.y, B.w))
+                                    : d32(qx, qy, qz, make_float4(A.x, A.z, B.x, B.z));
+            const int p = base + sid * kSub + c;
+            if (np < kWinCap) {
+              mpos[np] = p;
+              md[np] = d;
             }
+            ++np;
+            if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
           }
         }
         ovf = ovf || np > kWinCap;
