@@ -756,14 +756,18 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
     for (int r = 0; r < nscan; ++r) {
       const int sid = r == 0 ? s1 : s2;
       const float4* sp = cand + sid * kSub;
-      for (int c = 0; c < kSub; ++c) {
+      // Member bitmask in one pass, then the members in increasing position.
+      unsigned mask = 0;
+#pragma unroll 8
+      for (int c = 0; c < kSub; ++c) mask |= (d32(q.x, q.y, q.z, sp[c]) <= thr ? 1u : 0u) << c;
+      while (mask) {
+        const int c = __ffs(mask) - 1;
+        mask &= mask - 1;
         const float d = d32(q.x, q.y, q.z, sp[c]);
-        if (d <= thr) {
-          const int p = sid * kSub + c;
-          if (np < kWinCap) pos[np] = p;
-          ++np;
-          if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
-        }
+        const int p = sid * kSub + c;
+        if (np < kWinCap) pos[np] = p;
+        ++np;
+        if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
       }
     }
     ovf = ovf || np > kWinCap;
