@@ -1,3 +1,4 @@
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/lat_bench tools/lat_bench.cu
 // Dependent-chain latency of a few instruction classes on this GPU (cycles),
 // one thread: DADD, DMUL, DFMA, FFMA, LDS.64 + DADD, DP sqrt, DP division.
 #include <cstdio>
