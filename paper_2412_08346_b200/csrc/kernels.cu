@@ -371,16 +371,31 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
 // branch.  Per-pair terms are computed in parallel; the 8 running sums are
 // accumulated in pair order by 8 threads, exactly like the reference loops.
 // ---------------------------------------------------------------------------
-constexpr int kCostThreads = 256;
-constexpr int kCostChunk = 1024;             // pairs per chunk: a whole KG3 surface in one pass
+constexpr int kCostThreads = 256;           // two particles per CTA, 128 threads each
+constexpr int kCostHalf = 128;
+constexpr int kCostChunk = 512;              // pairs per chunk and particle
 constexpr int kCostRow = kCostChunk + 1;     // +1 double: the 8 summing threads hit distinct banks
-constexpr int kCostSmem = 8 * kCostRow * 8;  // bytes
+constexpr int kCostSmem = 2 * 8 * kCostRow * 8;  // bytes (both halves)
 
+// Each half of the CTA (128 threads, its own named barrier) owns one particle:
+// 384 CTAs of 2 x 32 KB of terms fit one wave at 3 CTAs/SM, where one
+// particle per CTA took two.
 __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevState S, int final_pass) {
-  const int j = blockIdx.x;
+  const int half = threadIdx.x >= kCostHalf ? 1 : 0;
+  const int tid = threadIdx.x - half * kCostHalf;
+  const int j = 2 * blockIdx.x + half;
+  if (j >= P.J) return;
   if (!final_pass && !S.active[j]) return;
-  extern __shared__ double cost_terms[];  // [8][kCostRow]
-  __shared__ double acc[8];
+  extern __shared__ double cost_smem[];
+  double* cost_terms = cost_smem + half * 8 * kCostRow;  // [8][kCostRow]
+  __shared__ double acc2[2][8];
+  double* acc = acc2[half];
+  auto half_sync = [half]() {
+    if (half)
+      asm volatile("bar.sync 2, %0;" ::"n"(kCostHalf) : "memory");
+    else
+      asm volatile("bar.sync 1, %0;" ::"n"(kCostHalf) : "memory");
+  };
   const int pre = P.part_pre[j];
   const double* th = th_of(S.theta, j);
   const Q4 q = pose_q(th);
@@ -396,21 +411,21 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   const V3 tcp = V3{P.pre_tcp[3 * pre], P.pre_tcp[3 * pre + 1], P.pre_tcp[3 * pre + 2]};
   const V3 com = V3{P.com[0], P.com[1], P.com[2]};
   const V3 com_residual = sub(add(mul(r, tcp), t), com);
-  if (threadIdx.x < 8) {
+  if (tid < 8) {
     double init = 0.0;
     if (!reverse) {
-      if (threadIdx.x < 3)
-        init = threadIdx.x == 0 ? com_residual.x : (threadIdx.x == 1 ? com_residual.y : com_residual.z);
-      else if (threadIdx.x < 7)
-        init = dot(com_residual, mul(dR[threadIdx.x - 3], tcp));
+      if (tid < 3)
+        init = tid == 0 ? com_residual.x : (tid == 1 ? com_residual.y : com_residual.z);
+      else if (tid < 7)
+        init = dot(com_residual, mul(dR[tid - 3], tcp));
     }
-    acc[threadIdx.x] = init;  // slot 7: contact-loss sum starts at 0.0
+    acc[tid] = init;  // slot 7: contact-loss sum starts at 0.0
   }
   const int64_t row = static_cast<int64_t>(j) * P.n_scene;
   const int* pmap = final_pass ? nullptr : S.pool_map;
   for (int c0 = 0; c0 < npairs; c0 += kCostChunk) {
     const int n = min(kCostChunk, npairs - c0);
-    for (int e = threadIdx.x; e < n; e += kCostThreads) {
+    for (int e = tid; e < n; e += kCostHalf) {
       const int i = c0 + e;
       V3 src, tr, ref;
       if (reverse) {
@@ -432,18 +447,18 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
       for (int jj = 0; jj < 4; ++jj) cost_terms[(3 + jj) * kCostRow + e] = dot(res, mul(dR[jj], src));
       cost_terms[7 * kCostRow + e] = sqnorm(res);
     }
-    __syncthreads();
-    if (threadIdx.x < 8) {
+    half_sync();
+    if (tid < 8) {
       // The reference's running sums, in pair order (the critical path).
-      const double* tr = cost_terms + threadIdx.x * kCostRow;
-      double a = acc[threadIdx.x];
+      const double* tr = cost_terms + tid * kCostRow;
+      double a = acc[tid];
 #pragma unroll 8
       for (int e = 0; e < n; ++e) a = a + tr[e];
-      acc[threadIdx.x] = a;
+      acc[tid] = a;
     }
-    __syncthreads();
+    half_sync();
   }
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     const double m = static_cast<double>(npairs);
     const double contact = acc[7] / m;
     const double loss = reverse ? contact : contact + sqnorm(com_residual);  // total_loss(contact, com_loss)
@@ -1061,7 +1076,7 @@ void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) 
   }
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
-  cost_kernel<<<P.J, kCostThreads, kCostSmem, st>>>(P, S, final_pass);
+  cost_kernel<<<(P.J + 1) / 2, kCostThreads, kCostSmem, st>>>(P, S, final_pass);
 }
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {
   trace_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, k);
