@@ -181,3 +181,16 @@ def test_icp_step_errors(solver):
         icp_closed_form_step(np.zeros((0, 3)), src, reg_cases.IDENTITY, solver=solver)
     with pytest.raises(InvalidArgument, match="quaternion is not unit-norm"):
         icp_closed_form_step(src, src + 1.0, bad, solver=solver)
+
+
+def test_large_minibatch_global_buffers(solver):
+    """Minibatches beyond the shared-memory batch buffers (m > 2048) and the
+    gathered-point stage (m > 256): the double buffer and the draws live in
+    global memory."""
+    port = _port()
+    src = fixtures.blob_cloud(5000, 0.06, 21)
+    rf = fixtures.blob_cloud(3000, 0.06, 22)
+    cfg = SgdConfig(preconditioner_mode=PreconditionerMode.kGaussNewtonRotation, minibatch_size=3000,
+                    max_iterations=6)
+    got = register_sgd_icp(src, rf, reg_cases.IDENTITY, cfg, 77, solver=solver)
+    same(got, port(src, rf, reg_cases.IDENTITY, cfg, 77))
