@@ -130,7 +130,7 @@ class ClockSampler:
 def problem_bytes(view) -> int:
     """Host->device bytes asicp_prepare uploads for this problem."""
     v = view.struct
-    b = 24 * (v.n_object + v.n_scene) + 16 * v.n_object  # FP64 clouds + FP32 candidates
+    b = 24 * (v.n_object + v.n_scene) + 32 * v.n_object  # FP64 clouds + FP32 candidates (two layouts)
     for i in range(v.n_preshapes):
         b += 24 * v.preshapes[i].n_surface + 24 + 4 + 4
     for i in range(v.n_sdf_grids):

@@ -48,6 +48,22 @@ __device__ __forceinline__ void pc_put(float4* base, int64_t c, float4 v) {
   f[6] = v.w;
 }
 
+// Minibatch pool gather: pool32 = candidates pool[0..m) in sample order,
+// pair-interleaved (pc_index) and +inf padded to the subtile.  A thread writes
+// one candidate pair: two 16-byte loads from the plain copy, two 16-byte
+// stores (the per-float pc_get / pc_put took four of each per candidate).
+__device__ __forceinline__ void gather_pool(const float4* cand4, const int* pool, int m, float4* pool32, int tid,
+                                            int nt) {
+  const int mp = round_up(m, kSub);
+  const float4 pad = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+  for (int i2 = 2 * tid; i2 < mp; i2 += 2 * nt) {
+    const float4 a = i2 < m ? cand4[pool[i2]] : pad;
+    const float4 b = i2 + 1 < m ? cand4[pool[i2 + 1]] : pad;
+    pool32[i2] = make_float4(a.x, b.x, a.y, b.y);
+    pool32[i2 + 1] = make_float4(a.z, b.z, a.w, b.w);
+  }
+}
+
 // True contact-surface size of particle j (surface rows are padded to kSub).
 __device__ __forceinline__ int surf_count(const DevProblem& P, int j) {
   const int pre = P.part_pre[j];

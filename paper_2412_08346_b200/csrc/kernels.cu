@@ -359,9 +359,7 @@ __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S
   if (threadIdx.x == 0) S.rng_mti[j] = s_mti;
   __syncthreads();
   float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;  // pair-interleaved (pc_*)
-  for (int i = threadIdx.x; i < m; i += blockDim.x) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
-  for (int i = m + threadIdx.x; i < round_up(m, kSub); i += blockDim.x)
-    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
+  gather_pool(P.obj_cand4, pool, m, pool32, threadIdx.x, blockDim.x);
 }
 
 // ---------------------------------------------------------------------------

@@ -22,6 +22,7 @@ struct DevProblem {
   int n_pop;        // Stein populations (= preshapes)
   const double* obj64;      // R, n_obj x 3
   const float4* obj_cand;   // R as FP32 NN candidates (-2b, |b|^2), b = r - center
+  const float4* obj_cand4;  // the same candidates one float4 per point (minibatch pool gathers)
   const double* scene64;    // C, n_scene x 3
   const float4* scene32;    // C rounded to FP32 (x, y, z, |p|_1 rounded up), for the collision pre-test
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)

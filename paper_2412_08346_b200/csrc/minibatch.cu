@@ -170,9 +170,7 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P,
   // Gather the FP32 candidates in sample order (+inf padded to the subtile),
   // pair-interleaved like the object cloud (common.cuh pc_*).
   float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
-  for (int i = tid; i < m; i += kMbThreads) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
-  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads)
-    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
+  gather_pool(P.obj_cand4, pool, m, pool32, tid, kMbThreads);
 }
 
 // Same algorithm with the stable sort replaced by a counting sort in shared
@@ -362,9 +360,7 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
   for (int i = tid; i < mt::kN; i += kMbThreads) gst[i] = st[i];
   if (tid == 0) S.rng_mti[j] = s_mti;
   float4* pool32 = S.pool32 + static_cast<int64_t>(j) * P.n_obj_pad;
-  for (int i = tid; i < m; i += kMbThreads) pc_put(pool32, i, pc_get(P.obj_cand, pool[i]));
-  for (int i = m + tid; i < round_up(m, kSub); i += kMbThreads)
-    pc_put(pool32, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
+  gather_pool(P.obj_cand4, pool, m, pool32, tid, kMbThreads);
 }
 
 template <int ITEMS>

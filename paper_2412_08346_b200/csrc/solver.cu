@@ -146,7 +146,7 @@ struct asicp_ctx {
   DevState S{};
 
   // Device buffers.
-  Buf obj64, obj_cand, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
+  Buf obj64, obj_cand, obj_cand4, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, scene32, sdf_coarse;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
       Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
@@ -228,7 +228,7 @@ struct asicp_ctx {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    Buf* all[] = {&obj64, &obj_cand, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
+    Buf* all[] = {&obj64, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
@@ -382,8 +382,14 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
   }
   for (int64_t i = p.n_object; i < c->n_obj_pad; ++i) put(i, 0.0f, 0.0f, 0.0f, INFINITY);
+  std::vector<float4> cand4(c->n_obj_pad);
+  for (int64_t i = 0; i < c->n_obj_pad; ++i) {
+    const float* f = cf + pc_index(i);
+    cand4[i] = make_float4(f[0], f[2], f[4], f[6]);
+  }
   upload(c, c->obj64, obj.data(), obj.size(), st);
   upload(c, c->obj_cand, cand.data(), cand.size(), st);
+  upload(c, c->obj_cand4, cand4.data(), cand4.size(), st);
   upload(c, c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
     std::vector<float4> s32(p.n_scene);
@@ -649,6 +655,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.n_pop = n_pre;
   P.obj64 = c->obj64.as<double>();
   P.obj_cand = c->obj_cand.as<float4>();
+  P.obj_cand4 = c->obj_cand4.as<float4>();
   P.scene64 = c->scene64.as<double>();
   P.scene32 = c->scene32.as<float4>();
   P.surf64 = c->surf64.as<double>();
@@ -1340,6 +1347,7 @@ int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t cal
     S.fy_par = par ? fyp.as<int>() : nullptr;
     S.fy_stride = 5 * static_cast<int64_t>(P.n_obj_pad);
     P.obj_cand = cand.as<float4>();
+    P.obj_cand4 = cand.as<float4>();  // all-zero candidates: either layout
     S.active = active.as<int>();
     S.n_col = ncol.as<int>();
     S.rng_state = st.as<uint64_t>();
