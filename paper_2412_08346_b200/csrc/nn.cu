@@ -56,11 +56,78 @@ __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_ou
   *nch_out = ceil_div(plan.m, chunk);
 }
 
-__global__ void nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
+// Item counts of particle j: forward query blocks, or reverse warp items when
+// the particle collides (the final ranking matches every particle forward).
+__device__ __forceinline__ void plan_counts(const DevProblem& P, const DevState& S, const NnPlan& plan, int j,
+                                            int* fwd, int* rev) {
+  *fwd = *rev = 0;
+  if (plan.kind == 2 || S.active[j]) {
+    if (plan.kind != 2 && S.n_col[j] > 0)
+      *rev = ceil_div(S.n_col[j], kRevWQ);
+    else
+      *fwd = ceil_div(surf_count(P, j), kFwdQB);
+  }
+}
+
+// Planning and item fill in one launch: every CTA recomputes the exclusive
+// scans of the per-particle counts (a few hundred to a few thousand
+// particles — cheaper than a second launch and a one-CTA kernel), then fills
+// the items of its own 128 particles; CTA 0 publishes the totals and resets
+// the round's counters.
+constexpr int kFillThreads = 128;
+__global__ void __launch_bounds__(kFillThreads) nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
+  __shared__ int sf[kFillThreads], sr[kFillThreads];
+  const int tid = threadIdx.x;
+  const int per = ceil_div(P.J, kFillThreads);
+  {
+    const int j0 = min(P.J, tid * per), j1 = min(P.J, j0 + per);
+    int cf = 0, cr = 0;
+    for (int jj = j0; jj < j1; ++jj) {
+      int f, r;
+      plan_counts(P, S, plan, jj, &f, &r);
+      cf += f;
+      cr += r;
+    }
+    sf[tid] = cf;
+    sr[tid] = cr;
+  }
+  __syncthreads();
+  for (int off = 1; off < kFillThreads; off <<= 1) {  // inclusive scans of the range sums
+    const int vf = tid >= off ? sf[tid - off] : 0, vr = tid >= off ? sr[tid - off] : 0;
+    __syncthreads();
+    sf[tid] += vf;
+    sr[tid] += vr;
+    __syncthreads();
+  }
+  const int T = sf[kFillThreads - 1];
+  if (blockIdx.x == 0 && tid == 0) {
+    S.item_off[0][P.J] = T;
+    S.item_off[1][P.J] = sr[kFillThreads - 1];
+    S.item_count[0][P.J] = S.item_count[1][P.J] = 0;
+    S.item_counter[0] = S.item_counter[1] = 0;
+    *S.refine_count = 0;
+    *S.amb_count = 0;
+  }
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
+  {
+    // Offsets of j: the scan up to its range, plus the counts before j in it.
+    const int r = j / per;
+    int of = r ? sf[r - 1] : 0, orr = r ? sr[r - 1] : 0;
+    for (int jj = r * per; jj < j; ++jj) {
+      int f, rv;
+      plan_counts(P, S, plan, jj, &f, &rv);
+      of += f;
+      orr += rv;
+    }
+    int f, rv;
+    plan_counts(P, S, plan, j, &f, &rv);
+    S.item_count[0][j] = f;
+    S.item_count[1][j] = rv;
+    S.item_off[0][j] = of;
+    S.item_off[1][j] = orr;
+  }
   int nch, chunk;
-  const int T = S.item_off[0][P.J];
   fwd_split(T, plan, &nch, &chunk);
   if (j == 0) {
     S.nn_dyn[0] = nch;
@@ -837,8 +904,7 @@ __global__ void __launch_bounds__(kPlanThreads) nn_plan_kernel(DevProblem P, Dev
 }
 
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
-  nn_plan_kernel<<<1, kPlanThreads, 0, st>>>(P, S, plan);
-  nn_fill_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, plan);
+  nn_fill_kernel<<<(P.J + kFillThreads - 1) / kFillThreads, kFillThreads, 0, st>>>(P, S, plan);
 }
 
 int nn_smem_bytes() { return kNnSmem; }

@@ -804,7 +804,7 @@ void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture)
     c->nn_events.push_back(e);
   }
   const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.first, e.second);
-  c->launches += 4 + n + (minibatch_m > 0);
+  c->launches += 1 + n + (minibatch_m > 0);  // fill (plan fused) + filter(s), merge, refine + minibatch
 }
 
 // The whole optimize_grasp as a kernel sequence on c->stream.
