@@ -5,6 +5,10 @@
  *   graspmatch::GraspSolution graspmatch::optimize_grasp(const GraspProblem&)
  *   (/root/reference/proj/include/graspmatch/grasp.hpp:141, defined at
  *    /root/reference/proj/src/grasp.cpp:132-307).
+ * It also replaces the registration entry points of SURVEY.md §8(f) rank 4,
+ *   graspmatch::register_sgd_icp (optim.hpp:170-176, optim.cpp:274-321) and
+ *   graspmatch::icp_closed_form_step (optim.hpp:87-91, optim.cpp:51-90),
+ * declared further below.
  * The reference has no FFI layer of its own; its C++ entry point is replaced
  * at link time by the adapter in paper_2412_08346_b200/csrc/graspmatch_adapter.cpp,
  * which marshals GraspProblem into the POD structs below.
