@@ -1096,9 +1096,12 @@ void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int
   pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
 }
 int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
-                        cudaStream_t st) {
-  int n = 3;
-  launch_median_small(P, S, st);
+                        cudaStream_t st, bool small_median) {
+  int n = 2;
+  if (small_median) {
+    launch_median_small(P, S, st);
+    ++n;
+  }
   if (big_grid > 0) {
     med_init_kernel<<<P.n_pop, 256, 0, st>>>(P, S);
     const int shifts[6] = {52, 40, 28, 16, 4, 0}, bits[6] = {12, 12, 12, 12, 12, 4};

@@ -166,8 +166,10 @@ void launch_median_small(const DevProblem& P, DevState& S, cudaStream_t st);  //
 // with big_grid CTAs per population (returns the launch count).
 // S.kmat != null selects the split SVGD (kmat + accumulate kernels);
 // max_pop / max_gpop: largest local / global population.
+// small_median = false: the caller already launched launch_median_small
+// (e.g. on a forked stream, overlapping the iteration's matching).
 int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
-                        cudaStream_t st);
+                        cudaStream_t st, bool small_median = true);
 // Particle-sharding exchange helpers: pack local rows [theta(7), drift(7)]
 // into `send` (stride 14 doubles), and scatter a gathered world x rows_per_rank
 // block back into global order (rank r's rows start at floor(r * J_glob / world)).

@@ -163,6 +163,8 @@ struct asicp_ctx {
   bool graph_valid = false;
   std::vector<char> graph_sig;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t side = nullptr;  // forked work inside an iteration (median bandwidth)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> nn_events;
   asicp_stats last_stats{};
   double nn_pairs_planned = 0.0;
@@ -228,6 +230,9 @@ struct asicp_ctx {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     Buf* all[] = {&obj64, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &theta,
@@ -840,6 +845,18 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
     const bool stein = k < c->k_stein;
     const int64_t m = c->ms[k];
     const bool pooled = m < c->n_obj;
+    // The small-population median bandwidth reads only the poses at the start
+    // of the iteration: fork it onto the side stream so its few CTAs overlap
+    // the collision test / matching / cost (unsharded runs; sharded ones need
+    // the pose all-gather first).  Joined before the Stein update.
+    const bool fork_median = stein && !c->xchg && !dbg_sync;
+    if (fork_median) {
+      CUDA_OK(cudaEventRecord(c->ev_fork, st));
+      CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+      launch_median_small(P, S, c->side);
+      CUDA_OK(cudaEventRecord(c->ev_join, c->side));
+      ++c->launches;
+    }
     launch_pose_prep(P, S, 0, st);
     stage("pose_prep");
     launch_collide(P, S, 0, 0, st);
@@ -876,7 +893,9 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
                             c->xchg->world, c->rows_per_rank, st);
         c->launches += 2;
       }
-      c->launches += 1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->max_gpop, c->med_big_grid, st);
+      if (fork_median) CUDA_OK(cudaStreamWaitEvent(st, c->ev_join, 0));
+      c->launches +=
+          1 + launch_stein_update(P, S, c->eta_stein, c->max_pop, c->max_gpop, c->med_big_grid, st, !fork_median);
       stage("stein");
     } else {
       launch_sgd(P, S, st);
@@ -1095,6 +1114,9 @@ asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen) {
     set_all_kernel_attrs();
     CUDA_OK(cudaEventCreate(&c->ev0));
     CUDA_OK(cudaEventCreate(&c->ev1));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     c->nn_grid = c->num_sms * std::max(1, nn_blocks_per_sm());
   });
   if (rc != ASICP_OK) {
