@@ -1095,6 +1095,11 @@ void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int
                        cudaStream_t st) {
   pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
 }
+void launch_svgd_kmat(const DevProblem& P, DevState& S, int max_pop, int max_gpop, cudaStream_t st) {
+  svgd_kmat_kernel<<<dim3((max_pop + kSvgdJ - 1) / kSvgdJ, (max_gpop + kSvgdJ - 1) / kSvgdJ, P.n_pop), 256, 0, st>>>(
+      P, S);
+}
+
 int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
                         cudaStream_t st, bool small_median) {
   int n = 2;
@@ -1113,9 +1118,13 @@ int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_po
   }
   dim3 grid((max_pop + kSvgdJ - 1) / kSvgdJ, P.n_pop);
   if (S.kmat) {
-    svgd_kmat_kernel<<<dim3(grid.x, (max_gpop + kSvgdJ - 1) / kSvgdJ, P.n_pop), 256, 0, st>>>(P, S);
+    // Split SVGD: the kernel matrix needs only the poses and h; with the small
+    // median forked (small_median false) the caller launched it on the fork too.
+    if (small_median || big_grid > 0) {
+      launch_svgd_kmat(P, S, max_pop, max_gpop, st);
+      ++n;
+    }
     svgd_acc_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
-    ++n;
   } else {
     svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
   }

@@ -166,7 +166,9 @@ void launch_median_small(const DevProblem& P, DevState& S, cudaStream_t st);  //
 // with big_grid CTAs per population (returns the launch count).
 // S.kmat != null selects the split SVGD (kmat + accumulate kernels);
 // max_pop / max_gpop: largest local / global population.
-// small_median = false: the caller already launched launch_median_small
+void launch_svgd_kmat(const DevProblem& P, DevState& S, int max_pop, int max_gpop, cudaStream_t st);
+// small_median = false: the caller already launched launch_median_small (and,
+// for the split SVGD without a grid-wide median, launch_svgd_kmat)
 // (e.g. on a forked stream, overlapping the iteration's matching).
 int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_pop, int max_gpop, int big_grid,
                         cudaStream_t st, bool small_median = true);

@@ -854,8 +854,12 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
       CUDA_OK(cudaEventRecord(c->ev_fork, st));
       CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
       launch_median_small(P, S, c->side);
-      CUDA_OK(cudaEventRecord(c->ev_join, c->side));
       ++c->launches;
+      if (S.kmat && c->med_big_grid == 0) {  // the split SVGD's kernel matrix: poses and h only
+        launch_svgd_kmat(P, S, c->max_pop, c->max_gpop, c->side);
+        ++c->launches;
+      }
+      CUDA_OK(cudaEventRecord(c->ev_join, c->side));
     }
     launch_pose_prep(P, S, 0, st);
     stage("pose_prep");
