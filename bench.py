@@ -1,34 +1,39 @@
 #!/usr/bin/env python
 """B200 AS-ICP bench: particle-iterations/s and per-grasp solve latency.
 
-Default workload (BASELINE.json configs[1]): 3 KG3
-preshapes x 256 particles (J = 768) against a 10k-point synthetic cylinder,
-64^3 gripper SDFs, k_max = 100 (38 annealed Stein + 62 SGD iterations).  One
-step = one complete optimize_grasp solve: J * k_max = 76,800
-particle-iterations.
+Default workload (BASELINE.json configs[3], SURVEY.md §8(d) cfg4 — the largest
+single-GPU configuration and the north star's multi-object batch): 11
+synthetic objects (cylinders / boxes / spheres / blobs, 10k points each, each
+on its own table scene) x 3 KG3 preshapes x 1024 particles, k_max = 40 (15
+annealed Stein + 25 SGD iterations).  One step = all 11 objects solved and
+selected: 33,792 particles x 40 = 1,351,680 particle-iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload cfg2|cfg3|cfg4|cfg5|reg] [--n-object N] [--reg-batch B]
 
-cfg2 / cfg3 at N > 1 run under torchrun, one rank per GPU; each rank solves its
-own object instance (object sharding: no data-path collective), so the scaling
-is weak and `value` is the total particle-iterations of all ranks over the
-max-over-ranks device time.
+--gpus N > 1 without torchrun in the environment re-launches this script under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL);
+under torchrun, WORLD_SIZE must equal N.
 
-cfg4 (BASELINE.json configs[3]) is the 11-object batch x 3 KG3 preshapes x
-1024 particles (40 iterations): its 33 (object, preshape) units are spread over
-the ranks by longest-processing-time (shard.py), each rank keeps its units
-device-resident and overlaps them on one GPU (batch.py), and the per-object
-answers are gathered and selected after the solves.  Total work is fixed, so
-the scaling is strong.
+cfg4 is sharded by shard.plan: whole (object, preshape) units go to the ranks
+while they fit the mean load, the leftover units are particle-sharded over all
+ranks (NCCL all-gather of the population per Stein iteration, captured in the
+solve's CUDA graph), so every rank carries the same particle count; each rank
+keeps its pieces device-resident and overlaps them on one GPU (batch.py); the
+per-object answers are gathered and selected after the solves.  Total work is
+fixed, so the scaling is strong.
 
-reg is a batch of register_sgd_icp problems (acceptance
-C2's inputs, one CTA each); metric registrations/s.
+cfg2 / cfg3 at N > 1: each rank solves its own object instance (object
+sharding, no data-path collective): weak scaling.  cfg5 (configs[4]) is one
+population of 16384 particles against an n-point cylinder (--n-object, default
+10k), particle-sharded over the ranks (strong scaling).  reg (SURVEY.md §8(f)
+rank 4) is a batch of register_sgd_icp problems; metric registrations/s.
 
-cfg5 (BASELINE.json configs[4]) is one population of 16384 particles against
-an n-point cylinder (--n-object, default 10k): at N > 1 the particles are
-sharded over the ranks, which all-gather the population's poses and drifts
-over NCCL each Stein iteration (strong scaling).
+The reference arm (--impl reference) times the unmodified reference
+optimize_grasp (oracle/_ref) on the host cores, one bounded sample of the
+workload per step (cfg4: one (object, preshape) unit — a whole 1024-particle
+Stein population — cycling over the 33 units), with inputs built by the
+oracle-side fixture library, so that arm maps no product library.
 """
 from __future__ import annotations
 
@@ -69,10 +74,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS) + ["reg"])
+    ap.add_argument("--workload", default="cfg4", choices=sorted(WORKLOADS) + ["reg"])
     ap.add_argument("--reg-batch", type=int, default=1184, help="reg: problems per GPU (default 8 per SM)")
     ap.add_argument("--n-object", type=int, default=0, help="cfg5 object cloud size (default 10000)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic capture of the NN kernel")
+    ap.add_argument("--cpu-1worker", action="store_true",
+                    help="also time the reference with workers = 1 on the cpu_baseline sample")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="start the ranks (gloo), report them and exit: checks the --gpus launch without a GPU")
     return ap.parse_args()
 
 
@@ -81,6 +91,45 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def relaunch_under_torchrun(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-run this script as N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1; returns its exit code.
+    Under torchrun (or N = 1) returns None and the caller proceeds."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus and not (args.gpus == 1 and world > 1 and "--gpus" not in sys.argv):
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+def dry_run(args) -> int:
+    """Rank plumbing only (gloo, no GPU): every rank reports in, rank 0
+    prints one JSON line."""
+    rank, world, _ = dist_env()
+    ranks = [rank]
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        ranks = [None] * world
+        dist.all_gather_object(ranks, rank)
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_arg": args.gpus, "ranks": ranks}), flush=True)
+    return 0
 
 
 class ClockSampler:
@@ -157,16 +206,48 @@ def cpu_reference(fixture, threads: int):
     return dt, sol
 
 
-def sample_fixture(workload: str, n_object: int = 0, seed: int = 0):
-    """The bounded CPU-reference sample: one full solve of one object (cfg5:
-    the same object with 2048 of the 16384 particles — a smaller population
-    makes the reference's O(K^2) Stein step cheaper per particle, so the
-    sampled rate flatters the CPU)."""
-    from paper_2412_08346_b200 import fixtures
+def sample_fixture(workload: str, n_object: int = 0, seed: int = 0, reference: bool = False):
+    """The workload's fixture for object `seed` (cfg5: 2048 of the 16384
+    particles — a smaller population makes the reference's O(K^2) Stein step
+    cheaper per particle, so the sampled rate flatters the CPU).  reference:
+    built by the oracle-side fixture library (the reference arm maps no
+    product library)."""
+    if reference:
+        from oracle import ref
 
+        make = ref.fixture_config
+    else:
+        from paper_2412_08346_b200 import fixtures
+
+        make = fixtures.config
     if workload == "cfg5":
-        return fixtures.config(5, seed=seed, particles_per_preshape=CFG5_CPU_SAMPLE_PARTICLES, n_object=n_object)
-    return fixtures.config(WORKLOADS[workload][0], seed=seed)
+        return make(5, seed=seed, particles_per_preshape=CFG5_CPU_SAMPLE_PARTICLES, n_object=n_object)
+    return make(WORKLOADS[workload][0], seed=seed)
+
+
+def reference_samples(workload: str, n_object: int, count: int):
+    """Per-step samples of the reference arm.  cfg4: the (object, preshape)
+    units in order (one whole 1024-particle Stein population each, solved
+    exactly as the sharded GPU path solves it, shard.subproblem); others: the
+    whole object-0 solve."""
+    if workload != "cfg4":
+        fx = sample_fixture(workload, n_object, reference=True)
+        return [fx] * count, f"full {workload} solve of object 0 ({fx.J * fx.k_max} particle-iterations) per step"
+    from paper_2412_08346_b200 import shard
+    from paper_2412_08346_b200.grasp import CProblem
+
+    n_units = 3 * N_BATCH_OBJECTS
+    objs = {}
+    out = []
+    for k in range(count):
+        u = k % n_units
+        o = u // 3
+        if o not in objs:
+            objs[o] = sample_fixture(workload, seed=o, reference=True).problem()
+        unit = shard.units_of([objs[o]])[u % 3]
+        out.append(CProblem(shard.subproblem(objs[o], unit)))
+    return out, ("one cfg4 (object, preshape) unit per step (1024 particles x 40 iterations = 40960 "
+                 "particle-iterations, a whole Stein population), cycling over the 33 units")
 
 
 def run_reference_arm(args):
@@ -179,23 +260,23 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (make -C oracle)"}))
         return 0
     threads = os.cpu_count() or 1
-    fx = sample_fixture(args.workload, args.n_object)
-    pits = fx.J * fx.k_max
-    for _ in range(args.warmup):
+    samples, what = reference_samples(args.workload, args.n_object, args.warmup + args.steps)
+    for fx in samples[:args.warmup]:
         cpu_reference(fx, threads)
-    times = []
-    for _ in range(args.steps):
+    times, pits = [], []
+    for fx in samples[args.warmup:]:
         dt, _ = cpu_reference(fx, threads)
         times.append(dt)
+        pits.append(fx.J * fx.k_max)
     ms = 1e3 * float(np.mean(times))
-    value = pits / (ms * 1e-3)
-    sample = (f"full {args.workload} solve of object 0 ({pits} particle-iterations) per step, "
-              f"graspmatch::optimize_grasp workers={threads}")
+    value = float(np.sum(pits)) / float(np.sum(times))
+    sample = f"{what}, graspmatch::optimize_grasp workers={threads}"
+    cfg_fx = sample_fixture(args.workload, args.n_object, reference=True)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if args.workload in ("cfg4", "cfg5") else "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args.workload, fx, world),
+        "data": "synthetic", "config": config_dict(args.workload, cfg_fx, world),
         "solve_latency_ms": ms,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -216,8 +297,11 @@ def config_dict(workload, fx, world):
                                  if world > 1 else "1 GPU",
                   "step": "one full optimize_grasp solve of the 16384-particle population"})
     elif workload == "cfg4":
-        d.update({"objects": N_BATCH_OBJECTS, "units": 3 * N_BATCH_OBJECTS,
-                  "parallelism": f"(object, preshape) units, LPT over {world} GPU(s), overlapped streams per GPU",
+        d.update({"objects": N_BATCH_OBJECTS, "units": 3 * N_BATCH_OBJECTS, "particles": 3 * N_BATCH_OBJECTS * 1024,
+                  "particles_per_object": fx.J,
+                  "parallelism": (f"shard.plan over {world} GPU(s): whole (object, preshape) units up to the mean "
+                                  "load, leftover units particle-sharded over all GPUs (NCCL allgather per Stein "
+                                  "iteration); pieces overlapped on streams per GPU"),
                   "step": "all 11 objects solved (33 units) + per-object selection"})
     else:
         d.update({"parallelism": f"object-shard x{world}" if world > 1 else "1 GPU",
@@ -441,8 +525,111 @@ def run_registration(args):
     return 0
 
 
+def cpu_baseline(args, result, batch: bool) -> dict:
+    """The reference (oracle/_ref) on this box's host cores, on a bounded
+    sample of the workload, with the bit-identity of the sample's answer.
+    cfg4: object 0 solved whole (3 preshapes x 1024 particles) vs the GPU's
+    object-0 answer (its units' summaries combined)."""
+    try:
+        from oracle import ref
+
+        if not ref.available():
+            return {"error": "oracle/_ref not built"}
+        threads = os.cpu_count() or 1
+        sfx = sample_fixture(args.workload, args.n_object, reference=True)
+        spits = sfx.J * sfx.k_max
+        dt, rs = cpu_reference(sfx, threads)
+        if args.workload == "cfg5":
+            same = None  # the sample is a smaller population than the bench's
+        elif batch:
+            r0 = result[0]
+            same = bool(rs.final_loss == r0["final_loss"] and np.array_equal(rs.theta, r0["theta"])
+                        and np.array_equal(rs.particle_theta, r0["particle_theta"])
+                        and np.array_equal(rs.particle_loss, r0["particle_loss"]))
+        else:
+            same = bool(np.array_equal(rs.particle_theta, result.particle_theta)
+                        and rs.final_loss == result.final_loss)
+        out = {
+            "value": spits / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"one full {args.workload} solve of object 0 ({sfx.J} particles, {spits} particle-iterations), "
+                      f"oracle/_ref graspmatch::optimize_grasp workers={threads}"
+                      + (" (extrapolated per particle-iteration to the 11-object batch)" if batch else ""),
+            "latency_ms": dt * 1e3,
+            "bit_identical": same,
+        }
+        if args.cpu_1worker:
+            dt1, _ = cpu_reference(sfx, 1)
+            out["workers_1"] = {"value": spits / dt1, "latency_ms": dt1 * 1e3, "cores": 1}
+        return out
+    except Exception as e:  # the baseline is reported, never required
+        return {"error": repr(e)}
+
+
+def traffic_child(workload: str, n_object: int) -> None:
+    """Run under ncu by measure_traffic: one profiled (eager) solve of the
+    workload's NN roofline problem (cfg4: unit 0)."""
+    from paper_2412_08346_b200 import Solver, fixtures, shard
+    from paper_2412_08346_b200.grasp import CProblem
+
+    if workload == "cfg4":
+        p = fixtures.config(4, seed=0).problem()
+        prob = CProblem(shard.subproblem(p, shard.units_of([p])[0]))
+    elif workload == "cfg5":
+        prob = fixtures.config(5, seed=0, n_object=n_object)
+    else:
+        prob = fixtures.config(WORKLOADS[workload][0], seed=0)
+    s = Solver(device=0, profile=True)
+    s.prepare(prob)
+    s.run()
+    s.close()
+
+
+def measure_traffic(args, timeout_s: int = 300) -> dict | None:
+    """roofline.traffic: DRAM bytes (read + write) per launch of the NN filter
+    kernel, from one ncu capture (two DRAM counters only) of one profiled solve
+    of the same problem the roofline times.  ncu's timings are not used."""
+    import csv
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return {"error": "ncu not found"}
+    with tempfile.TemporaryDirectory() as td:
+        log = Path(td) / "traffic.csv"
+        code = f"import sys; sys.path.insert(0, {str(ROOT)!r}); import bench; bench.traffic_child({args.workload!r}, {args.n_object})"
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--print-units", "base",
+               "-k", "regex:nn_filter_kernel", "--csv", "--log-file", str(log), sys.executable, "-c", code]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s, cwd=str(ROOT))
+        except subprocess.TimeoutExpired:
+            return {"error": f"ncu timed out after {timeout_s} s"}
+        if r.returncode != 0 or not log.exists():
+            return {"error": f"ncu rc={r.returncode}: {(r.stderr or r.stdout)[-300:]}"}
+        per = {}
+        with open(log) as f:
+            rows = [ln for ln in f if ln.startswith('"')]
+        for row in csv.DictReader(rows):
+            name = row.get("Metric Name", "")
+            if name.startswith("dram__bytes_"):
+                v = float(str(row.get("Metric Value", "0")).replace(",", ""))
+                per[row["ID"]] = per.get(row["ID"], 0.0) + v
+        if not per:
+            return {"error": "no nn_filter_kernel launches captured"}
+        vals = list(per.values())
+        return {"bytes_per_launch": float(np.mean(vals)), "launches": len(vals), "max_bytes": float(max(vals)),
+                "total_bytes": float(sum(vals)),
+                "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum over every nn_filter_kernel "
+                          "launch of one profiled solve (cfg4: unit 0), measured inside this bench run"}
+
+
 def main():
     args = parse()
+    rc = relaunch_under_torchrun(args)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return dry_run(args)
     if args.workload == "reg":
         return run_registration(args)
     if args.impl == "reference":
@@ -459,7 +646,7 @@ def main():
     from paper_2412_08346_b200 import Solver, fixtures, shard
     from paper_2412_08346_b200 import _lib as L
     from paper_2412_08346_b200.batch import BatchSolver
-    from paper_2412_08346_b200.grasp import CProblem
+    from paper_2412_08346_b200.grasp import CProblem, nccl_unique_id
     import ctypes as C
 
     main_stream = torch.cuda.current_stream()
@@ -483,18 +670,33 @@ def main():
         dist.all_gather_object(out, obj)
         return out
 
+    def all_sum(x: int) -> int:
+        return int(sum(all_gather(x)))
+
+    def broadcast(obj):
+        box = [obj]
+        dist.broadcast_object_list(box, src=0)
+        return box[0]
+
     batch = args.workload == "cfg4"
     e2e_split = []  # (prepare ms, run ms) per e2e step (single-problem workloads)
     if batch:
         problems = [fixtures.config(4, seed=o).problem() for o in range(N_BATCH_OBJECTS)]
         units = shard.units_of(problems)
-        owner = shard.assign(units, world)
-        mine = [i for i in range(len(units)) if owner[i] == rank]
-        subs = [CProblem(shard.subproblem(problems[units[i].obj], units[i])) for i in mine]
+        pieces = shard.plan(units, world)[rank]
+        subs = [CProblem(shard.subproblem(problems[units[pc.unit].obj], units[pc.unit])) for pc in pieces]
         k_max = problems[0].k_max
         pits_total = sum(u.count for u in units) * k_max
         streams = [torch.cuda.Stream() for _ in subs]
-        runner = BatchSolver(subs, device=local, streams=[s.cuda_stream for s in streams])
+
+        def join(i, solver):
+            # A unit shared by all ranks: one NCCL communicator per unit (ids
+            # made by rank 0 and broadcast in the same unit order everywhere).
+            pc = pieces[i]
+            if pc.world > 1:
+                solver.set_partition_nccl(pc.rank, pc.world, broadcast(nccl_unique_id() if rank == 0 else None))
+
+        runner = BatchSolver(subs, device=local, streams=[s.cuda_stream for s in streams], setup=join)
         fx = fixtures.config(4, seed=0)  # config description / CPU sample (object 0)
 
         def solve_resident():
@@ -502,9 +704,7 @@ def main():
 
         def finish():
             sols = runner.wait()
-            parts = all_gather([(i, np.asarray(s.particle_theta), np.asarray(s.particle_loss),
-                                 np.asarray(s.particle_collision_free), np.asarray(s.particle_converged))
-                                for i, s in zip(mine, sols)])
+            parts = all_gather([shard.summary(pc.unit, s) for pc, s in zip(pieces, sols) if pc.rank == 0])
             return shard.combine(problems, parts)
 
         def solve_e2e():
@@ -525,11 +725,6 @@ def main():
             fx = fixtures.config(5, seed=0, n_object=args.n_object)
             pits_total = fx.J * fx.k_max
             if world > 1:
-                def broadcast(obj):
-                    box = [obj]
-                    dist.broadcast_object_list(box, src=0)
-                    return box[0]
-
                 shard.join_particle_partition(solver, rank, world, broadcast)
         else:
             fx = fixtures.config(cfg, seed=rank)  # object instance per rank (object sharding)
@@ -616,13 +811,12 @@ def main():
     lib = L.load()
     lib.asicp_dbg_ffma_tflops.restype = C.c_double
     peak = float(lib.asicp_dbg_ffma_tflops(20000))
+    active_evals = sum(int(x) for x in ([s.raw_stats()[13] for s in runner.solvers] if batch
+                                         else [solver.raw_stats()[13]]))
+    active_total = all_sum(active_evals)  # particle evaluations that were not SGD-frozen
     traffic = None
-    tfile = ROOT / "profiles" / "nn_traffic.json"
-    if tfile.exists() and args.workload == "cfg2":
-        try:
-            traffic = json.loads(tfile.read_text()).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic = measure_traffic(args)
 
     if rank == 0:
         best = result[0] if batch else result
@@ -647,42 +841,22 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if (achieved and peak > 0) else None,
                          "peak_source": "FFMA microbenchmark on this GPU (asicp_dbg_ffma_tflops)",
-                         "traffic": traffic, "nn_ms_per_launch": nn_ms_per_launch,
+                         "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                         "traffic_detail": traffic, "nn_ms_per_launch": nn_ms_per_launch,
                          "nn_launches": int(st.nn_launches), "nn_share_of_step": st.nn_ms / st.solve_ms,
                          "algorithmic": "8 FLOP x (query, candidate) pairs; pairs counted by the kernel"},
             "status": status, "final_loss": final_loss,
+            "active_particle_iterations_per_step": active_total,
+            "stage_ms_profiled_unit": {"nn_filter": st.nn_ms, "collide": st.collide_ms,
+                                       "minibatch": st.minibatch_ms, "cost": st.cost_ms, "stein": st.svgd_ms,
+                                       "solve": st.solve_ms},
         }
         if batch:
             line["objects_found"] = int(sum(int(r["status"]) == 0 for r in result))
         else:
             line["nn"] = result.diagnostics
         if world == 1 and not args.no_cpu_baseline:
-            try:
-                from oracle import ref
-
-                if ref.available():
-                    threads = os.cpu_count() or 1
-                    sfx = sample_fixture(args.workload, args.n_object)
-                    spits = sfx.J * sfx.k_max
-                    dt, rs = cpu_reference(sfx, threads)
-                    if args.workload == "cfg5":
-                        same = None  # the sample is a smaller population than the bench's
-                    elif batch:
-                        same = bool(rs.final_loss == result[0]["final_loss"]
-                                    and np.array_equal(rs.theta, result[0]["theta"]))
-                    else:
-                        same = bool(np.array_equal(rs.particle_theta, result.particle_theta)
-                                    and rs.final_loss == result.final_loss)
-                    line["cpu_baseline"] = {
-                        "value": spits / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                        "sample": f"one full {args.workload} solve of object 0 ({sfx.J} particles, {spits} "
-                                  f"particle-iterations), "
-                                  f"oracle/_ref graspmatch::optimize_grasp workers={threads}",
-                        "latency_ms": dt * 1e3,
-                        "bit_identical": same,
-                    }
-            except Exception as e:  # the baseline is reported, never required
-                line["cpu_baseline"] = {"error": repr(e)}
+            line["cpu_baseline"] = cpu_baseline(args, result, batch)
         print(json.dumps(line), flush=True)
     if batch:
         runner.close()

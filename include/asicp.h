@@ -146,16 +146,18 @@ typedef struct asicp_solution {
   double nn_pairs;             /* (query, candidate) pairs evaluated by the NN kernels */
 } asicp_solution;
 
-/* Per-kernel device timing collected when ASICP_OPT_PROFILE is set. */
+/* Per-stage device timing collected when ASICP_OPT_PROFILE is set (the solve
+ * then runs eagerly on the ctx stream, every stage bracketed by CUDA events);
+ * only solve_ms and kernel_launches are filled otherwise. */
 typedef struct asicp_stats {
   double solve_ms;             /* device time of the last asicp_run (events on the ctx stream) */
-  double nn_ms;                /* summed device time of NN filter launches */
+  double nn_ms;                /* summed device time of forward/final NN filter launches */
   int64_t nn_launches;
   double nn_pairs;             /* candidate pairs processed by those launches */
-  double collide_ms;
-  double minibatch_ms;
-  double cost_ms;
-  double svgd_ms;
+  double collide_ms;           /* collision test (colliding_points) launches */
+  double minibatch_ms;         /* minibatch sampling + pool gather launches */
+  double cost_ms;              /* cost / gradient launches of the iterations */
+  double svgd_ms;              /* Stein step (drift, exchange, median, kernel matrix, update) */
   int64_t kernel_launches;     /* kernels enqueued by the last asicp_run */
 } asicp_stats;
 

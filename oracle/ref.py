@@ -156,6 +156,49 @@ def build_sdf(cloud, voxel, padding=-1.0, band=0.003):
 
 
 # ---------------------------------------------------------------------------
+# Oracle-side build of the synthetic-input generators (csrc/fixtures.cu compiled
+# by oracle/Makefile into _build/libasicp_fixtures_oracle.so): the reference arm
+# of bench.py builds its inputs with it, so that arm maps oracle libraries only.
+# Same source, same C-ABI as the product-side libasicp_fixtures.so.
+# ---------------------------------------------------------------------------
+FIXTURES_PATH = HERE / "_build" / "libasicp_fixtures_oracle.so"
+_FX = None
+
+
+def fixtures_lib() -> C.CDLL:
+    global _FX
+    if _FX is None:
+        if not FIXTURES_PATH.exists():
+            raise RuntimeError(f"{FIXTURES_PATH} missing: run `make -C oracle port`")
+        _FX = L.declare_fixtures(C.CDLL(str(FIXTURES_PATH)))
+    return _FX
+
+
+class OracleFixture(RefFixture):
+    """A fixture owned by the oracle-side generator library."""
+
+    def __init__(self, handle):
+        if not handle:
+            raise ValueError("unknown fixture")
+        self.lib = fixtures_lib()
+        self.handle = handle
+        self._view = self.lib.asicp_fx_view(handle)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self.lib.asicp_fx_free(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def fixture_config(cfg: int, seed: int = 0, particles_per_preshape: int = 0, n_object: int = 0) -> OracleFixture:
+    """asicp_fx_config (include/asicp_fixtures.h) from the oracle-side library."""
+    return OracleFixture(fixtures_lib().asicp_fx_config(cfg, seed, particles_per_preshape, n_object))
+
+
+# ---------------------------------------------------------------------------
 # The plain-C restatement (oracle/port/asicp_port.c) — available wherever the
 # repo is built, even without /root/reference.
 # ---------------------------------------------------------------------------

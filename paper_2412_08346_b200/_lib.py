@@ -2,7 +2,9 @@
 
 The product path is the CUDA library libasicp.so built in-tree by
 paper_2412_08346_b200/build.py.  There is no CPU fallback: if the library is
-missing, loading fails loudly.
+missing, loading fails loudly.  The synthetic-input generators of
+include/asicp_fixtures.h (tests and bench inputs, not the product) are a
+separate host-only library, libasicp_fixtures.so.
 """
 from __future__ import annotations
 
@@ -11,6 +13,7 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libasicp.so"
+FIXTURES_PATH = PKG / "libasicp_fixtures.so"
 
 c_double_p = C.POINTER(C.c_double)
 c_float_p = C.POINTER(C.c_float)
@@ -157,16 +160,20 @@ class IcpStep(C.Structure):
     _fields_ = [("theta", C.c_double * 7), ("degenerate", C.c_int32)]
 
 
-# Every symbol include/asicp.h + include/asicp_fixtures.h declare.
+# Every symbol include/asicp.h declares (libasicp.so) ...
 EXPORTS = (
     "asicp_abi_version", "asicp_create", "asicp_destroy", "asicp_set_option", "asicp_prepare",
-    "asicp_run", "asicp_run_async", "asicp_wait", "asicp_optimize_grasp", "asicp_build_sdf", "asicp_export_trace", "asicp_nccl_unique_id",
-    "asicp_set_partition_nccl", "asicp_group_create", "asicp_group_destroy", "asicp_set_partition_group",
-    "asicp_clear_partition", "asicp_get_stats", "asicp_minibatch_schedule",
-    "asicp_annealing", "asicp_fx_desk", "asicp_fx_config", "asicp_fx_view", "asicp_fx_free",
-    "asicp_fx_cylinder_cloud", "asicp_fx_build_sdf", "asicp_register_sgd_icp", "asicp_register_sgd_icp_batch",
-    "asicp_register_prepare", "asicp_register_run", "asicp_fx_c2_trial", "asicp_fx_blob_cloud",
+    "asicp_run", "asicp_run_async", "asicp_wait", "asicp_optimize_grasp", "asicp_build_sdf", "asicp_export_trace",
+    "asicp_nccl_unique_id", "asicp_set_partition_nccl", "asicp_group_create", "asicp_group_destroy",
+    "asicp_set_partition_group", "asicp_clear_partition", "asicp_get_stats", "asicp_minibatch_schedule",
+    "asicp_annealing", "asicp_register_sgd_icp", "asicp_register_sgd_icp_batch",
+    "asicp_register_prepare", "asicp_register_run",
     "asicp_icp_closed_form_step", "asicp_icp_closed_form_step_batch",
+)
+# ... and every symbol include/asicp_fixtures.h declares (libasicp_fixtures.so).
+FIXTURE_EXPORTS = (
+    "asicp_fx_desk", "asicp_fx_config", "asicp_fx_view", "asicp_fx_free", "asicp_fx_cylinder_cloud",
+    "asicp_fx_build_sdf", "asicp_fx_c2_trial", "asicp_fx_blob_cloud",
 )
 
 
@@ -198,17 +205,6 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     lib.asicp_minibatch_schedule.argtypes = [C.c_int64, C.c_int64, C.c_int64]
     lib.asicp_annealing.restype = C.c_double
     lib.asicp_annealing.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double]
-    lib.asicp_fx_desk.restype = C.c_void_p
-    lib.asicp_fx_desk.argtypes = [C.c_uint64, C.c_int64, C.c_int64]
-    lib.asicp_fx_config.restype = C.c_void_p
-    lib.asicp_fx_config.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64]
-    lib.asicp_fx_view.restype = C.POINTER(Problem)
-    lib.asicp_fx_view.argtypes = [C.c_void_p]
-    lib.asicp_fx_free.argtypes = [C.c_void_p]
-    lib.asicp_fx_cylinder_cloud.argtypes = [C.c_double, C.c_double, C.c_int, C.c_uint64, c_double_p]
-    lib.asicp_fx_build_sdf.restype = C.c_int64
-    lib.asicp_fx_build_sdf.argtypes = [c_double_p, C.c_int64, C.c_double, C.c_double, C.c_double, c_i32_p,
-                                       c_double_p, c_float_p]
     lib.asicp_register_sgd_icp.argtypes = [C.c_void_p, c_double_p, C.c_int64, c_double_p, C.c_int64, c_double_p,
                                            C.POINTER(SgdCfg), C.c_uint64, C.POINTER(Registration), C.c_char_p,
                                            C.c_size_t]
@@ -223,12 +219,37 @@ def _declare(lib: C.CDLL) -> C.CDLL:
                                                C.POINTER(IcpStep), C.c_char_p, C.c_size_t]
     lib.asicp_icp_closed_form_step_batch.argtypes = [C.c_void_p, C.c_int64, c_double_p, c_i64_p, c_double_p, c_i64_p,
                                                      c_double_p, C.POINTER(IcpStep), C.c_char_p, C.c_size_t]
+    # include/asicp_debug.h (diagnostics)
+    lib.asicp_dbg_raw_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+    lib.asicp_dbg_iter_stats.restype = C.c_int64
+    lib.asicp_dbg_iter_stats.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
+    lib.asicp_dbg_ffma_tflops.restype = C.c_double
+    lib.asicp_dbg_ffma_tflops.argtypes = [C.c_int]
+    lib.asicp_dbg_dfma_tflops.restype = C.c_double
+    lib.asicp_dbg_dfma_tflops.argtypes = [C.c_int]
+    return lib
+
+
+def declare_fixtures(lib: C.CDLL) -> C.CDLL:
+    """Signatures of include/asicp_fixtures.h (any library exporting them)."""
+    lib.asicp_fx_desk.restype = C.c_void_p
+    lib.asicp_fx_desk.argtypes = [C.c_uint64, C.c_int64, C.c_int64]
+    lib.asicp_fx_config.restype = C.c_void_p
+    lib.asicp_fx_config.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int64]
+    lib.asicp_fx_view.restype = C.POINTER(Problem)
+    lib.asicp_fx_view.argtypes = [C.c_void_p]
+    lib.asicp_fx_free.argtypes = [C.c_void_p]
+    lib.asicp_fx_cylinder_cloud.argtypes = [C.c_double, C.c_double, C.c_int, C.c_uint64, c_double_p]
+    lib.asicp_fx_build_sdf.restype = C.c_int64
+    lib.asicp_fx_build_sdf.argtypes = [c_double_p, C.c_int64, C.c_double, C.c_double, C.c_double, c_i32_p,
+                                       c_double_p, c_float_p]
     lib.asicp_fx_c2_trial.argtypes = [C.c_int, C.c_int, c_double_p, c_double_p, c_double_p]
     lib.asicp_fx_blob_cloud.argtypes = [C.c_int, C.c_double, C.c_uint64, c_double_p]
     return lib
 
 
 _LIB: C.CDLL | None = None
+_FX: C.CDLL | None = None
 
 
 def load() -> C.CDLL:
@@ -239,3 +260,13 @@ def load() -> C.CDLL:
             raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2412_08346_b200.build`")
         _LIB = _declare(C.CDLL(str(LIB_PATH)))
     return _LIB
+
+
+def load_fixtures() -> C.CDLL:
+    """Load libasicp_fixtures.so (the synthetic-input generators)."""
+    global _FX
+    if _FX is None:
+        if not FIXTURES_PATH.exists():
+            raise RuntimeError(f"{FIXTURES_PATH} is missing: build it with `python -m paper_2412_08346_b200.build`")
+        _FX = declare_fixtures(C.CDLL(str(FIXTURES_PATH)))
+    return _FX

@@ -12,19 +12,24 @@ grasp.cpp:283-306); nothing here changes what a solve computes.
 """
 from __future__ import annotations
 
-from typing import List, Sequence
+from typing import Callable, List, Sequence
 
 from .grasp import GraspProblem, GraspSolution, Solver
 
 
 class BatchSolver:
+    """`setup(i, solver)`, when given, runs before entry i is prepared (e.g. to
+    join a particle partition, shard.plan's shared units)."""
+
     def __init__(self, problems: Sequence[GraspProblem], device: int = 0, streams: Sequence[int] | None = None,
-                 **solver_kw):
+                 setup: Callable[[int, Solver], None] | None = None, **solver_kw):
         if streams is not None and len(streams) != len(problems):
             raise ValueError("one stream per problem")
         self.solvers: List[Solver] = []
         for i, p in enumerate(problems):
             s = Solver(device=device, stream=streams[i] if streams is not None else None, **solver_kw)
+            if setup is not None:
+                setup(i, s)
             s.prepare(p)
             self.solvers.append(s)
 

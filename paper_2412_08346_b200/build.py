@@ -1,10 +1,14 @@
 """In-tree build of the CUDA extension (libasicp.so) for sm_100a.
 
 `python -m paper_2412_08346_b200.build` (or __graft_entry__.build()) compiles
-every .cu under csrc/ with nvcc for `-gencode arch=compute_100a,code=sm_100a`
-and links them into paper_2412_08346_b200/libasicp.so, which the ctypes
-binding (paper_2412_08346_b200/_lib.py) loads.  The shared library travels to
-the GPU box with the repo snapshot; no JIT cache is involved.
+the product sources under csrc/ with nvcc for `-gencode
+arch=compute_100a,code=sm_100a` and links them into
+paper_2412_08346_b200/libasicp.so, which the ctypes binding
+(paper_2412_08346_b200/_lib.py) loads.  The synthetic-input generators
+(csrc/fixtures.cu, host-only C++) go into their own library,
+libasicp_fixtures.so: they feed tests and bench.py, never the solve.  Both
+libraries travel to the GPU box with the repo snapshot; no JIT cache is
+involved.
 """
 from __future__ import annotations
 
@@ -19,13 +23,16 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libasicp.so"
+FX_LIB = PKG / "libasicp_fixtures.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: the FP64 path must not contract a*b+c (the reference oracle is
 # built without FMA); the FP32 NN filter requests its FMAs explicitly.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3",
               "-diag-suppress", "177", f"-I{ROOT / 'include'}"]
-SOURCES = ["kernels.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "register.cu", "sdf_build.cu", "solver.cu", "fixtures.cu", "trace_io.cpp"]
+SOURCES = ["kernels.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "register.cu", "sdf_build.cu", "solver.cu",
+           "trace_io.cpp"]
+FX_SOURCE = "fixtures.cu"
 
 
 def _nvcc() -> str:
@@ -58,6 +65,13 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    fx_src = CSRC / FX_SOURCE
+    if force or _stale(FX_LIB, [fx_src] + headers):
+        cmd = [shutil.which("g++") or "g++", "-x", "c++", "-std=c++17", "-O2", "-fPIC", "-shared",
+               f"-I{ROOT / 'include'}", "-o", str(FX_LIB), str(fx_src)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

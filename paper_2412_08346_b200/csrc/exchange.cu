@@ -4,20 +4,31 @@
 #include <dlfcn.h>
 #include <nccl.h>  // types only; the library is resolved at run time
 
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
 
 void asicp_group::barrier() {
   std::unique_lock<std::mutex> lock(mu);
+  if (aborted) throw std::runtime_error("asicp exchange: another rank of the group failed");
   const unsigned long long g = generation;
   if (++arrived == world) {
     arrived = 0;
     ++generation;
     cv.notify_all();
   } else {
-    cv.wait(lock, [&] { return generation != g; });
+    cv.wait(lock, [&] { return generation != g || aborted; });
+    if (aborted) throw std::runtime_error("asicp exchange: another rank of the group failed");
   }
+}
+
+// A rank that fails between the two barriers of an allgather releases the
+// others (they throw instead of waiting forever); the group is then unusable.
+void asicp_group::abort() {
+  std::lock_guard<std::mutex> lock(mu);
+  aborted = true;
+  cv.notify_all();
 }
 
 namespace asicp {
@@ -77,10 +88,18 @@ class NcclExchange final : public Exchange {
   ~NcclExchange() override {
     if (comm_) NcclApi::get().comm_destroy(comm_);
   }
-  // Kept out of graph capture: a rank's graph would embed the communicator
-  // and every replay must then be collective; the sharded solve is launched
-  // eagerly instead (its kernels are large enough that launch cost is noise).
-  bool capturable() const override { return false; }
+  // NCCL collectives may be captured into a CUDA graph: every rank captures
+  // the same solve (same problem, same partition) and replays it once per
+  // solve, so each replay's all-gathers stay collective.  A re-prepare that
+  // changes the shape re-captures on every rank alike.  ASICP_NCCL_GRAPH=0
+  // launches the sharded solve eagerly instead.
+  bool capturable() const override {
+    static const bool on = [] {
+      const char* e = std::getenv("ASICP_NCCL_GRAPH");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
   void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
     NcclApi& api = NcclApi::get();
     api.check(api.all_gather(send, recv, bytes, ncclUint8, comm_, st), "ncclAllGather");
@@ -96,8 +115,18 @@ class GroupExchange final : public Exchange {
     rank = r;
     world = g->world;
   }
-  bool capturable() const override { return false; }
+  bool capturable() const override { return false; }  // host round trip: never inside a graph
   void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) override {
+    try {
+      exchange(send, recv, bytes, st);
+    } catch (...) {
+      g_->abort();
+      throw;
+    }
+  }
+
+ private:
+  void exchange(const void* send, void* recv, size_t bytes, cudaStream_t st) {
     std::vector<char>& mine = g_->slot[rank];
     mine.resize(bytes);
     if (bytes) cuda_ok(cudaMemcpyAsync(mine.data(), send, bytes, cudaMemcpyDeviceToHost, st), "D2H");
@@ -114,7 +143,6 @@ class GroupExchange final : public Exchange {
     g_->barrier();  // every rank has read every slot
   }
 
- private:
   asicp_group* g_;
 };
 

@@ -27,8 +27,10 @@ struct asicp_group {
   std::condition_variable cv;
   int arrived = 0;
   unsigned long long generation = 0;
+  bool aborted = false;  // a rank failed mid-exchange: every barrier throws from now on
   std::vector<std::vector<char>> slot;
   void barrier();
+  void abort();
 };
 
 namespace asicp {

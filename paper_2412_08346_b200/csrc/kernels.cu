@@ -33,6 +33,7 @@ __global__ void seed_rng_kernel(uint64_t* state, int* mti, uint64_t seed, int J)
 __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   const int j = blockIdx.x;
   if (!all && !S.active[j]) return;
+  if (!all && threadIdx.x == 0) atomicAdd(S.stats + 13, 1ull);  // active (not SGD-frozen) particle evaluations
   const int pre = P.part_pre[j];
   const double* th = th_of(S.theta, j);
   const M3 r = rotation_matrix(pose_q(th));

@@ -165,7 +165,13 @@ struct asicp_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t side = nullptr;  // forked work inside an iteration (median bandwidth)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> nn_events;
+  // Profile mode (ASICP_OPT_PROFILE, eager launches): per-stage event pairs.
+  enum Stage { kStNn = 0, kStCollide, kStMinibatch, kStCost, kStSvgd, kStages };
+  struct ProfEvent {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfEvent> prof_events;
   asicp_stats last_stats{};
   double nn_pairs_planned = 0.0;
   int64_t launches = 0;
@@ -224,9 +230,9 @@ struct asicp_ctx {
                          &gpop_off_d, &med_hist, &med_state, &kofs_d, &kmat};
     for (Buf* b : shard_bufs) b->release();
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    for (auto& e : nn_events) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
+    for (auto& e : prof_events) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -757,6 +763,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.final_free = c->final_free.as<int>();
   mark("buffers");
   CUDA_OK(cudaStreamSynchronize(st));
+  c->pin_off = 0;  // every staged copy has landed: the next prepare reuses the buffer from the start
   mark("sync");
   // The captured graph bakes DevProblem/DevState and the k schedule into its
   // kernel parameters: keep it only if all of them are unchanged.
@@ -769,7 +776,13 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   };
   push(c->ms.data(), c->ms.size() * sizeof(int64_t));
   push(c->gammas.data(), c->gammas.size() * sizeof(double));
-  const int64_t extra[5] = {c->k_max, c->k_stein, c->record_trace, c->max_chunks, static_cast<int64_t>(c->seed)};
+  // Host-side launch shapes the capture bakes in as well (grids of the Stein
+  // kernels, whether the grid-wide median runs and kmat is forked, the NN
+  // plan / merge shapes, the partition).
+  const int64_t extra[13] = {c->k_max,        c->k_stein,      c->record_trace,  c->max_chunks,
+                             static_cast<int64_t>(c->seed),     c->max_pop,      c->max_gpop,
+                             c->med_big_grid, c->max_ns,       c->target_items,  c->nn_grid,
+                             c->J_glob,       c->rows_per_rank};
   push(extra, sizeof(extra));
   push(&c->eta_stein, sizeof(double));
   if (sig != c->graph_sig) {
@@ -780,6 +793,24 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   }
   c->prepared = true;
 }
+
+// Profile mode: bracket a stage's launches with an event pair on the ctx stream.
+struct StageTimer {
+  asicp_ctx* c;
+  cudaEvent_t b = nullptr;
+  StageTimer(asicp_ctx* ctx, int stage, bool capture) : c(ctx) {
+    if (!c->profile || capture) return;
+    asicp_ctx::ProfEvent e{stage, nullptr, nullptr};
+    CUDA_OK(cudaEventCreate(&e.a));
+    CUDA_OK(cudaEventCreate(&e.b));
+    c->prof_events.push_back(e);
+    CUDA_OK(cudaEventRecord(e.a, c->stream));
+    b = e.b;
+  }
+  ~StageTimer() {
+    if (b) cudaEventRecord(b, c->stream);
+  }
+};
 
 NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   NnPlan plan{};
@@ -801,14 +832,17 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
 void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
   cudaStream_t st = c->stream;
   launch_nn_plan(c->P, c->S, plan, st);
-  if (minibatch_m > 0) launch_minibatch(c->P, c->S, minibatch_m, st);
-  std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
-  if (c->profile && !capture) {
-    CUDA_OK(cudaEventCreate(&e.first));
-    CUDA_OK(cudaEventCreate(&e.second));
-    c->nn_events.push_back(e);
+  if (minibatch_m > 0) {
+    StageTimer t(c, asicp_ctx::kStMinibatch, capture);
+    launch_minibatch(c->P, c->S, minibatch_m, st);
   }
-  const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.first, e.second);
+  asicp_ctx::ProfEvent e{asicp_ctx::kStNn, nullptr, nullptr};
+  if (c->profile && !capture) {
+    CUDA_OK(cudaEventCreate(&e.a));
+    CUDA_OK(cudaEventCreate(&e.b));
+    c->prof_events.push_back(e);
+  }
+  const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.a, e.b);
   c->launches += 1 + n + (minibatch_m > 0);  // fill (plan fused) + filter(s), merge, refine + minibatch
 }
 
@@ -849,7 +883,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
     // of the iteration: fork it onto the side stream so its few CTAs overlap
     // the collision test / matching / cost (unsharded runs; sharded ones need
     // the pose all-gather first).  Joined before the Stein update.
-    const bool fork_median = stein && !c->xchg && !dbg_sync;
+    const bool fork_median = stein && !c->xchg && !dbg_sync && !c->profile;  // profile: every stage on one stream
     if (fork_median) {
       CUDA_OK(cudaEventRecord(c->ev_fork, st));
       CUDA_OK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
@@ -863,7 +897,10 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
     }
     launch_pose_prep(P, S, 0, st);
     stage("pose_prep");
-    launch_collide(P, S, 0, 0, st);
+    {
+      StageTimer t(c, asicp_ctx::kStCollide, capture);
+      launch_collide(P, S, 0, 0, st);
+    }
     stage("collide");
     S.pool_map = pooled ? S.pool_idx : nullptr;
     NnPlan plan = make_plan(c, 0, m, pooled);
@@ -880,7 +917,10 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
     } else {
       enqueue_nn(c, plan, pooled ? static_cast<int>(m) : 0, capture);
     }
-    launch_cost(P, S, 0, st);
+    {
+      StageTimer t(c, asicp_ctx::kStCost, capture);
+      launch_cost(P, S, 0, st);
+    }
     stage("cost");
     c->launches += 3;
     if (c->record_trace) {
@@ -888,6 +928,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
       ++c->launches;
     }
     if (stein) {
+      StageTimer t(c, asicp_ctx::kStSvgd, capture);
       launch_drift(P, S, c->gammas[k], c->n_ref, st);
       if (c->xchg) {
         // The population's poses and drifts from every rank, in global order.
@@ -940,11 +981,11 @@ void launch(asicp_ctx* c) {
   if (c->in_flight) throw InvalidArgument("asicp_run_async: a solve is already in flight (call asicp_wait)");
   CUDA_OK(cudaSetDevice(c->device));
   cudaStream_t st = c->stream;
-  for (auto& e : c->nn_events) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
+  for (auto& e : c->prof_events) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
   }
-  c->nn_events.clear();
+  c->prof_events.clear();
   CUDA_OK(cudaEventRecord(c->ev0, st));
   const bool graph = c->use_graph && !c->profile && (!c->xchg || c->xchg->capturable());
   if (graph) {
@@ -1038,11 +1079,27 @@ void finish(asicp_ctx* c, asicp_solution* out) {
   asicp_stats& s = c->last_stats;
   s = asicp_stats{};
   s.solve_ms = ms;
-  for (auto& e : c->nn_events) {
+  for (auto& e : c->prof_events) {
     float t = 0.0f;
-    CUDA_OK(cudaEventElapsedTime(&t, e.first, e.second));
-    s.nn_ms += t;
-    ++s.nn_launches;
+    CUDA_OK(cudaEventElapsedTime(&t, e.a, e.b));
+    switch (e.stage) {
+      case asicp_ctx::kStNn:
+        s.nn_ms += t;
+        ++s.nn_launches;
+        break;
+      case asicp_ctx::kStCollide:
+        s.collide_ms += t;
+        break;
+      case asicp_ctx::kStMinibatch:
+        s.minibatch_ms += t;
+        break;
+      case asicp_ctx::kStCost:
+        s.cost_ms += t;
+        break;
+      default:
+        s.svgd_ms += t;
+        break;
+    }
   }
   s.kernel_launches = c->launches;
 

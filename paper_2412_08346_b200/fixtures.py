@@ -19,7 +19,7 @@ class Fixture:
     def __init__(self, handle):
         if not handle:
             raise ValueError("unknown fixture")
-        self.lib = L.load()
+        self.lib = L.load_fixtures()
         self.handle = handle
         self._view = self.lib.asicp_fx_view(handle)
 
@@ -68,16 +68,16 @@ class Fixture:
 
 
 def desk(seed: int = 0, n_init: int = 100, n_top: int = 6) -> Fixture:
-    return Fixture(L.load().asicp_fx_desk(seed, n_init, n_top))
+    return Fixture(L.load_fixtures().asicp_fx_desk(seed, n_init, n_top))
 
 
 def config(cfg: int, seed: int = 0, particles_per_preshape: int = 0, n_object: int = 0) -> Fixture:
-    return Fixture(L.load().asicp_fx_config(cfg, seed, particles_per_preshape, n_object))
+    return Fixture(L.load_fixtures().asicp_fx_config(cfg, seed, particles_per_preshape, n_object))
 
 
 def cylinder_cloud(radius: float = 0.03, height: float = 0.12, n: int = 1500, seed: int = 1) -> np.ndarray:
     out = np.zeros((n, 3))
-    L.load().asicp_fx_cylinder_cloud(radius, height, n, seed, out.ctypes.data_as(L.c_double_p))
+    L.load_fixtures().asicp_fx_cylinder_cloud(radius, height, n, seed, out.ctypes.data_as(L.c_double_p))
     a_side = 2.0 * np.pi * radius * height
     a_cap = np.pi * radius * radius
     n_side = int(n * a_side / (a_side + 2.0 * a_cap))
@@ -88,7 +88,7 @@ def build_sdf(cloud: np.ndarray, voxel: float, padding: float = -1.0, band: floa
     cloud = np.ascontiguousarray(cloud, dtype=np.float64)
     dims = (C.c_int32 * 3)()
     meta = (C.c_double * 5)()
-    lib = L.load()
+    lib = L.load_fixtures()
     n = lib.asicp_fx_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta, None)
     vals = np.zeros(n, dtype=np.float32)
     lib.asicp_fx_build_sdf(cloud.ctypes.data_as(L.c_double_p), len(cloud), voxel, padding, band, dims, meta,
@@ -100,7 +100,7 @@ def c2_trial(trial: int, n: int = 500):
     """Acceptance C2 trial inputs (test_acceptance.cpp:256-282): (source,
     reference, truth pose) — the reference box cloud displaced by the trial's
     seeded rigid transform."""
-    lib = L.load()
+    lib = L.load_fixtures()
     src = np.zeros((n, 3))
     ref = np.zeros((n, 3))
     truth = np.zeros(7)
@@ -112,5 +112,5 @@ def c2_trial(trial: int, n: int = 500):
 def blob_cloud(n: int, radius: float, seed: int) -> np.ndarray:
     """synthetic::blob_cloud (synthetic.cpp:69-83)."""
     out = np.zeros((n, 3))
-    L.load().asicp_fx_blob_cloud(n, radius, seed, out.ctypes.data_as(L.c_double_p))
+    L.load_fixtures().asicp_fx_blob_cloud(n, radius, seed, out.ctypes.data_as(L.c_double_p))
     return out

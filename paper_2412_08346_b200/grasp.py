@@ -467,6 +467,14 @@ class Solver:
         self.lib.asicp_get_stats(self.ctx, C.byref(st))
         return st
 
+    def raw_stats(self) -> list:
+        """The last solve's device counters (asicp_dbg_raw_stats, include/asicp_debug.h):
+        [0] uncertified NN windows, [1] full FP64 rescans, [2] NN queries, [3] pool ties,
+        [4] NN pairs, [12] forward/final filter pairs, [13] active particle evaluations."""
+        out = (C.c_uint64 * 256)()
+        self.lib.asicp_dbg_raw_stats(self.ctx, out)
+        return list(out)
+
 
 class Group:
     """An in-process exchange group for particle sharding (asicp_group)."""

@@ -22,9 +22,9 @@ from paper_2412_08346_b200 import annealing, fixtures, minibatch_schedule
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def declared_symbols():
+def declared_symbols(headers=None):
     names = set()
-    for h in (ROOT / "include").glob("*.h"):
+    for h in headers or sorted((ROOT / "include").glob("*.h")):
         text = h.read_text()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         for m in re.finditer(r"\b(asicp_\w+)\s*\(", text):
@@ -33,13 +33,22 @@ def declared_symbols():
 
 
 def test_library_exports_every_declared_symbol():
+    """libasicp.so exports everything asicp.h / asicp_debug.h declare;
+    the fixture generators live in their own library (asicp_fixtures.h)."""
+    fx_header = ROOT / "include" / "asicp_fixtures.h"
+    product = [h for h in sorted((ROOT / "include").glob("*.h")) if h != fx_header]
     lib = C.CDLL(str(L.LIB_PATH))
-    names = declared_symbols()
+    names = declared_symbols(product)
     assert len(names) >= 18
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
     assert set(L.EXPORTS) <= names
     assert L.load().asicp_abi_version() == 1
+    assert not any(hasattr(lib, n) for n in L.FIXTURE_EXPORTS), "fixtures are not part of the product library"
+    fx = C.CDLL(str(L.FIXTURES_PATH))
+    fx_names = declared_symbols([fx_header])
+    assert fx_names == set(L.FIXTURE_EXPORTS)
+    assert not [n for n in sorted(fx_names) if not hasattr(fx, n)]
 
 
 def test_schedule_kats():
@@ -136,3 +145,46 @@ def test_partial_view_and_batch_fixtures():
     assert len({c.tobytes() for c in clouds}) == 11
     full = fixtures.config(4, seed=0)
     assert full.J == 3 * 1024 and full.problem().stein.step_scale == 64.0 / 1024
+
+
+def _problem_arrays(p):
+    out = [p.object_cloud, p.scene_cloud, p.com, np.array([p.k_max, p.k_stein, p.seed, p.contact_tolerance])]
+    for s in p.preshapes:
+        out += [s.inner_surface_cloud, s.full_cloud, s.tcp, np.array([s.sdf_index])]
+    for g, off in zip(p.sdf.grids, p.sdf.offsets):
+        out += [np.asarray(g.origin), np.array([g.voxel, g.boundary_max_abs]), np.asarray(g.dims), g.values,
+                np.asarray(off)]
+    out += [np.asarray(i) for i in p.initializations]
+    return out
+
+
+def test_oracle_side_fixtures_equal_product_fixtures():
+    """bench.py's reference arm builds its inputs with the oracle-side build of
+    csrc/fixtures.cu (oracle/_build/libasicp_fixtures_oracle.so), so it maps no
+    product library: both builds must produce the same problems."""
+    if not ref.FIXTURES_PATH.exists():
+        pytest.skip("make -C oracle port")
+    for cfg, seed in [(4, 3), (2, 0), (3, 1)]:
+        a = fixtures.config(cfg, seed=seed, particles_per_preshape=16).problem()
+        b = ref.fixture_config(cfg, seed=seed, particles_per_preshape=16).problem()
+        xa, xb = _problem_arrays(a), _problem_arrays(b)
+        assert len(xa) == len(xb)
+        for u, v in zip(xa, xb):
+            assert np.array_equal(u, v)
+
+
+def test_reference_arm_maps_no_product_library():
+    """The reference arm (bench.py --impl reference) must not load libasicp.so
+    or libasicp_fixtures.so: run its input construction in a fresh process and
+    read its memory map."""
+    import subprocess
+    import sys
+
+    code = ("import bench, sys\n"
+            "fx = bench.sample_fixture('cfg4', 0, reference=True)\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "sys.exit(1 if ('libasicp.so' in maps or 'libasicp_fixtures.so' in maps) else 0)\n")
+    if not ref.FIXTURES_PATH.exists():
+        pytest.skip("make -C oracle port")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

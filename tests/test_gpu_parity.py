@@ -17,6 +17,18 @@ pytestmark = pytest.mark.gpu
 TOL = 0.0  # bit-identical, see module docstring
 
 
+def cpu_oracle(fx):
+    """The reference itself (oracle/_ref) wherever it is built, else the C
+    restatement pinned to it (oracle/port, tests/test_oracle.py)."""
+    from oracle import ref
+
+    if ref.available():
+        return ref.optimize_grasp(fx)
+    if not ref.port_available():
+        pytest.skip("neither oracle/_ref nor the oracle port is built")
+    return ref.port_optimize_grasp(fx)
+
+
 def assert_same_solution(got, want, tol=TOL):
     assert got.status == want.status
     assert got.preshape_id == want.preshape_id
@@ -191,14 +203,10 @@ def test_device_exp_is_glibc_exact():
 @pytest.mark.parametrize("seed", [0, 1])
 def test_cfg2_reduced_matches_port(solver, seed):
     """cfg2 shape (3 KG3 preshapes, 64^3 SDFs, 10k cylinder) with 8 particles per
-    preshape and 12 iterations, against the C restatement (no /root/reference needed)."""
-    from oracle import ref
-
-    if not ref.port_available():
-        pytest.skip("oracle port not built")
+    preshape and 12 iterations, against the reference (cpu_oracle)."""
     fx = fixtures.config(2, seed=seed, particles_per_preshape=8).set(k_max=12, k_stein=5, anneal_period_total=12,
                                                                      record_trace=1)
-    want = ref.port_optimize_grasp(fx)
+    want = cpu_oracle(fx)
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)
@@ -208,14 +216,10 @@ def test_cfg2_reduced_matches_port(solver, seed):
                                                  (4, 8, 8, 12)])
 def test_partial_view_and_batch_objects_match_port(solver, cfg, seed, ppp, k_max):
     """cfg3 (noisy occluded scan) and cfg4 batch objects (box / sphere / blob)
-    at reduced particle counts, full trace against the C restatement."""
-    from oracle import ref
-
-    if not ref.port_available():
-        pytest.skip("oracle port not built")
+    at reduced particle counts, full trace against the reference (cpu_oracle)."""
     fx = fixtures.config(cfg, seed=seed, particles_per_preshape=ppp)
     fx.set(k_max=k_max, k_stein=min(15, k_max // 2), anneal_period_total=k_max, record_trace=1)
-    want = ref.port_optimize_grasp(fx)
+    want = cpu_oracle(fx)
     got = solver.optimize(fx)
     np.testing.assert_array_equal(got.trace_in_collision, want.trace_in_collision)
     assert np.array_equal(got.trace_theta, want.trace_theta)
@@ -224,14 +228,10 @@ def test_partial_view_and_batch_objects_match_port(solver, cfg, seed, ppp, k_max
 
 def test_large_population_grid_median_matches_port(solver):
     """A population above kMedBigK (2048) takes the grid-wide median select;
-    2100 particles leave ragged 128-row tiles.  Full trace against the C port."""
-    from oracle import ref
-
-    if not ref.port_available():
-        pytest.skip("oracle port not built")
+    2100 particles leave ragged 128-row tiles.  Full trace against the reference."""
     fx = fixtures.config(5, seed=2, particles_per_preshape=2100, n_object=500)  # grid-wide median
     fx.set(k_max=5, k_stein=3, anneal_period_total=5, record_trace=1)  # T >= C = 5 cycles
-    want = ref.port_optimize_grasp(fx)
+    want = cpu_oracle(fx)
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)
@@ -240,14 +240,10 @@ def test_large_population_grid_median_matches_port(solver):
 @pytest.mark.parametrize("ppp", [250, 700])
 def test_mid_population_median_and_split_svgd_match_port(solver, ppp):
     """K = 250 takes the sampled-bracket median (M > 8192) and the split SVGD;
-    K = 700 the grid-wide median.  Full trace against the C port."""
-    from oracle import ref
-
-    if not ref.port_available():
-        pytest.skip("oracle port not built")
+    K = 700 the grid-wide median.  Full trace against the reference."""
     fx = fixtures.config(5, seed=4, particles_per_preshape=ppp, n_object=600)
     fx.set(k_max=6, k_stein=5, anneal_period_total=6, record_trace=1)
-    want = ref.port_optimize_grasp(fx)
+    want = cpu_oracle(fx)
     got = solver.optimize(fx)
     assert np.array_equal(got.trace_theta, want.trace_theta)
     assert_same_solution(got, want)

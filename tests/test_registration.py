@@ -121,5 +121,8 @@ def test_library_exports_registration_symbols():
 
     lib = ctypes.CDLL(str(L.LIB_PATH))
     for sym in ("asicp_register_sgd_icp", "asicp_register_sgd_icp_batch", "asicp_register_prepare",
-                "asicp_register_run", "asicp_fx_c2_trial", "asicp_fx_blob_cloud"):
+                "asicp_register_run"):
         assert hasattr(lib, sym), sym
+    fx = ctypes.CDLL(str(L.FIXTURES_PATH))
+    for sym in ("asicp_fx_c2_trial", "asicp_fx_blob_cloud"):
+        assert hasattr(fx, sym), sym

@@ -1,10 +1,14 @@
 """Multi-process (world_size 2, gloo, CPU) test of the object/preshape sharding.
 
-Two ranks split the (object, preshape) units of a 2-object batch (3 KG3
-preshapes each, cfg2 shape reduced), solve their units with the CPU
-restatement (oracle port — the GPU path is the same host logic around the
-B200 Solver), all-gather the particle summaries over gloo and select per
-object.  The sharded answers must equal the unsharded solve bit for bit.
+Two ranks split the (object, preshape) units of a 3-object batch (3 KG3
+preshapes each, cfg4 shape reduced): 9 units of 3 particles, so each rank
+takes 4 whole units and the 9th is particle-sharded over both (shard.plan).
+Units are solved with the CPU restatement (oracle port — the GPU path is the
+same host logic around the B200 Solver; a particle-sharded piece is solved
+whole here, its partition rank 0 contributing the summaries, as the B200
+partition's final all-gather does); the summaries are all-gathered over gloo
+and selected per object.  The sharded answers must equal the unsharded solve
+bit for bit.
 """
 import os
 import socket
@@ -23,8 +27,8 @@ def _problems():
     from paper_2412_08346_b200 import fixtures
 
     out = []
-    for seed in (0, 1):
-        fx = fixtures.config(2, seed=seed, particles_per_preshape=3)
+    for seed in (0, 1, 2):
+        fx = fixtures.config(4, seed=seed, particles_per_preshape=3)
         fx.set(k_max=4, k_stein=2, anneal_period_total=4)
         out.append(fx.problem())
     return out
@@ -41,8 +45,14 @@ def _worker(rank, world, port, q):
         dist.all_gather_object(out, obj)
         return out
 
-    res = solve_sharded(_problems(), ref.port_optimize_grasp, rank, world, gather)
-    q.put((rank, [(int(r["status"]), r["theta"], r["final_loss"], r["particle_loss"]) for r in res]))
+    pieces = []
+
+    def partition(sub, piece):  # a particle-sharded piece: solved whole here (see the module doc)
+        pieces.append((piece.unit, piece.world, piece.rank, piece.count))
+        return ref.port_optimize_grasp(sub)
+
+    res = solve_sharded(_problems(), ref.port_optimize_grasp, rank, world, gather, partition)
+    q.put((rank, [(int(r["status"]), r["theta"], r["final_loss"], r["particle_loss"]) for r in res], pieces))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -60,10 +70,14 @@ def test_sharded_solve_matches_unsharded():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    outs = dict(q.get(timeout=600) for _ in procs)
+    got = [q.get(timeout=600) for _ in procs]
+    outs = {r: res for r, res, _ in got}
+    split = {r: pieces for r, _, pieces in got}
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    # The 9th unit (index 8) is shared: particle 0 on rank 0, 1-2 on rank 1.
+    assert split[0] == [(8, 2, 0, 1)] and split[1] == [(8, 2, 1, 2)]
     want = [ref.port_optimize_grasp(p) for p in _problems()]
     for rank in (0, 1):
         for (status, theta, loss, ploss), w in zip(outs[rank], want):
@@ -74,13 +88,53 @@ def test_sharded_solve_matches_unsharded():
 
 
 def test_assignment_is_balanced_and_deterministic():
-    from paper_2412_08346_b200.shard import Unit, assign
+    """cfg4's 33 units of 1024 particles: whole-unit LPT alone is a 5/4 split
+    on 8 ranks (82.5 % efficiency); shard.plan particle-shards the remainder,
+    so every rank carries exactly the mean load at 2, 4 and 8 ranks."""
+    from paper_2412_08346_b200.shard import Unit, assign, plan
 
-    units = [Unit(o, p, 0, 1024) for o in range(11) for p in range(3)]
+    units = [Unit(o, p, 1024 * p, 1024) for o in range(11) for p in range(3)]
     owner = assign(units, 8)
     assert owner == assign(units, 8)
-    loads = np.bincount(owner, minlength=8)
-    assert loads.max() - loads.min() <= 1  # 33 equal units on 8 ranks -> 5/4 split
+    assert np.bincount(owner, minlength=8).max() == 5  # whole units only
+    for world in (1, 2, 3, 4, 5, 8):
+        pieces = plan(units, world)
+        assert pieces == plan(units, world)
+        loads = [sum(pc.count for pc in rp) for rp in pieces]
+        assert sum(loads) == 33 * 1024
+        assert max(loads) - min(loads) <= 1, (world, loads)
+        # every unit covered exactly once: whole, or split over all ranks
+        per_unit = {}
+        for r, rp in enumerate(pieces):
+            for pc in rp:
+                per_unit.setdefault(pc.unit, []).append((r, pc))
+        assert sorted(per_unit) == list(range(33))
+        for u, lst in per_unit.items():
+            if len(lst) == 1:
+                assert lst[0][1].world == 1 and lst[0][1].count == 1024
+            else:
+                assert len(lst) == world and sorted(pc.rank for _, pc in lst) == list(range(world))
+                assert all(pc.world == world for _, pc in lst)
+                assert sum(pc.count for _, pc in lst) == 1024
+        # the shared units come in the same order on every rank (collectives line up)
+        orders = [[pc.unit for pc in rp if pc.world > 1] for rp in pieces]
+        assert all(o == orders[0] for o in orders)
+    assert sum(1 for pc in plan(units, 8)[0] if pc.world > 1) == 1  # 4 whole + 1/8 of the 33rd
+
+
+def test_empty_preshape_units_get_no_rank():
+    """a preshape with an empty initialization list is a valid
+    problem; its unit must not reach a solver (J = 0 raises there and the
+    other ranks would hang in the gather)."""
+    from paper_2412_08346_b200.shard import Unit, assign, combine, plan
+
+    units = [Unit(0, 0, 0, 4), Unit(0, 1, 4, 0), Unit(0, 2, 4, 4)]
+    assert assign(units, 2)[1] == -1
+    assert all(pc.unit != 1 for rp in plan(units, 2) for pc in rp)
+    prob = type("P", (), {"initializations": [np.zeros((4, 7)), np.zeros((0, 7)), np.zeros((4, 7))]})()
+    rec = lambda i, k: (i, np.zeros((k, 7)), np.arange(k, dtype=float) + i, np.ones(k, bool), np.zeros(k, bool))
+    res = combine([prob], [[rec(0, 4)], [rec(2, 4)]])
+    assert res[0]["particle_loss"].shape == (8,) and res[0]["final_loss"] == 0.0
 
 
 class _RecordingSolver:
