@@ -234,6 +234,35 @@ RegistrationResult register_sgd_icp(const PointCloud& source, const PointCloud& 
   return out;
 }
 
+// Drop-in definition of graspmatch::build_sdf (sdf.hpp:60-61) in place of
+// sdf.cpp:48-175: the field is built on the GPU (csrc/sdf_build.cu), value for
+// value the reference's, so everything downstream — stack_preshapes, the
+// scenario front end's GMSDF001 cache files (io.cpp:555-580, save_sdf at
+// sdf.cpp:256-285), the collision queries — sees identical bytes.
+SdfGrid build_sdf(const PointCloud& cloud, double voxel, const SdfBuildOptions& options) {
+  const std::vector<double> pts = flatten(cloud);
+  int32_t dims[3] = {0, 0, 0};
+  double meta[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  char err[512] = {0};
+  const int64_t n = static_cast<int64_t>(cloud.size());
+  // First call sizes the grid (values == NULL), the second fills it.
+  int rc = asicp_build_sdf(thread_context(), pts.data(), n, voxel, options.padding, options.surface_band, dims, meta,
+                           nullptr, err, sizeof(err));
+  if (rc == ASICP_INVALID_ARGUMENT) throw InvalidArgument(err);
+  if (rc != ASICP_OK) throw std::runtime_error(std::string("asicp_build_sdf: ") + err);
+  SdfGrid grid;
+  grid.values.resize(static_cast<size_t>(dims[0]) * static_cast<size_t>(dims[1]) * static_cast<size_t>(dims[2]));
+  rc = asicp_build_sdf(thread_context(), pts.data(), n, voxel, options.padding, options.surface_band, dims, meta,
+                       grid.values.data(), err, sizeof(err));
+  if (rc == ASICP_INVALID_ARGUMENT) throw InvalidArgument(err);
+  if (rc != ASICP_OK) throw std::runtime_error(std::string("asicp_build_sdf: ") + err);
+  for (int a = 0; a < 3; ++a) grid.dims[a] = dims[a];
+  grid.origin = Vec3(meta[0], meta[1], meta[2]);
+  grid.voxel = meta[3];
+  grid.boundary_max_abs = meta[4];
+  return grid;
+}
+
 // Drop-in definition of graspmatch::icp_closed_form_step (optim.hpp:87-91)
 // in place of optim.cpp:51-90.  The NnIndex argument is not needed: the GPU
 // matches against the reference cloud itself (same answers, the kd-tree's

@@ -6,7 +6,9 @@ paper_2412_08346_b200/csrc/graspmatch_adapter.cpp — i.e. every
 graspmatch::optimize_grasp call in them (test_grasp.cpp:348-458, acceptance C7
 desk grasp over 10 seeds and C9 worker-count determinism) and every
 graspmatch::register_sgd_icp / icp_closed_form_step call (test_optim.cpp:69-124,
-540-584, acceptance C2's 20 recovery trials) runs on the B200 through the C-ABI.  Built here by `make -C oracle dropin`; the binaries travel
+540-584, acceptance C2's 20 recovery trials) and every graspmatch::build_sdf
+call (test_sdf.cpp, the desk scenario, the scenario front end's field cache)
+runs on the B200 through the C-ABI.  Built here by `make -C oracle dropin`; the binaries travel
 to the GPU box with the repo.
 """
 import subprocess
@@ -42,7 +44,7 @@ def test_reference_scenario_front_end_on_b200(tmp_path):
     """the reference's scenario front end —
     write_demo_scenario, load_scenario_config, run_scenario (cloud I/O, cached
     collision fields, initial poses, export_trace), report_to_json — driving
-    the B200 optimize_grasp through the drop-in.  Report (wall_seconds zeroed)
+    the B200 build_sdf and optimize_grasp through the drop-in.  Report (wall_seconds zeroed)
     and trace file must equal the reference's own run byte for byte."""
     for name in ("scenario_ref", "scenario_b200"):
         if not (REF / name).exists():
@@ -50,9 +52,18 @@ def test_reference_scenario_front_end_on_b200(tmp_path):
     d, trace = tmp_path / "demo", tmp_path / "trace.txt"  # same paths: the report echoes them
     ref = subprocess.run([str(REF / "scenario_ref"), str(d), str(trace)], capture_output=True, text=True, timeout=600)
     ref_trace = trace.read_bytes()
+    # The reference's GMSDF001 field cache (io.cpp:555-580, save_sdf at
+    # sdf.cpp:256-285): remove it so the B200 run rebuilds every field through
+    # the drop-in graspmatch::build_sdf (csrc/sdf_build.cu), then compare bytes.
+    cache = d / "cache"
+    ref_fields = {f.name: f.read_bytes() for f in sorted(cache.iterdir())}
+    assert ref_fields, "the demo scenario wrote no cached field"
+    for f in cache.iterdir():
+        f.unlink()
     b200 = subprocess.run([str(REF / "scenario_b200"), str(d), str(trace)], capture_output=True, text=True,
                           timeout=600)
     assert ref.returncode == 0 and b200.returncode == 0, ref.stderr + b200.stderr
     assert '"pose"' in b200.stdout
     assert b200.stdout == ref.stdout
     assert trace.read_bytes() == ref_trace
+    assert {f.name: f.read_bytes() for f in sorted(cache.iterdir())} == ref_fields

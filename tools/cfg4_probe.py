@@ -1,0 +1,75 @@
+"""cfg4 probe: where the 11-object batch spends its time.
+
+  python tools/cfg4_probe.py times [--objects N]
+      every (object, preshape) unit solved alone (graph replay, device time of
+      the ctx stream), their sum, and all units launched together as bench.py
+      does (wall time around launch + wait).
+  python tools/cfg4_probe.py unit [--unit U] [--objects N]
+      one warm-up solve of unit U, then one solve between
+      cudaProfilerStart/Stop (ncu --profile-from-start off): the launch list of
+      exactly one 1024-particle unit.
+"""
+import argparse
+import ctypes
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+from paper_2412_08346_b200 import Solver, fixtures, shard  # noqa: E402
+from paper_2412_08346_b200.batch import BatchSolver  # noqa: E402
+from paper_2412_08346_b200.grasp import CProblem  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("mode", choices=["times", "unit"])
+ap.add_argument("--objects", type=int, default=11)
+ap.add_argument("--unit", type=int, default=0)
+ap.add_argument("--eager", action="store_true")
+a = ap.parse_args()
+
+problems = [fixtures.config(4, seed=o).problem() for o in range(a.objects)]
+units = shard.units_of(problems)
+subs = [CProblem(shard.subproblem(problems[u.obj], u)) for u in units]
+
+if a.mode == "unit":
+    cudart = ctypes.CDLL("libcudart.so.12") if Path("/usr/local/cuda/lib64/libcudart.so.12").exists() else None
+    s = Solver(use_graph=not a.eager)
+    s.prepare(subs[a.unit])
+    s.run()
+    s.run()
+    if cudart is None:
+        import torch
+
+        torch.cuda.profiler.start()
+    else:
+        cudart.cudaProfilerStart()
+    sol = s.run()
+    if cudart is None:
+        torch.cuda.profiler.stop()
+    else:
+        cudart.cudaProfilerStop()
+    st = s.stats()
+    print(f"unit {a.unit}: solve {st.solve_ms:.3f} ms, {st.kernel_launches} launches, status {int(sol.status)}")
+    s.close()
+    sys.exit(0)
+
+iso = []
+for i, p in enumerate(subs):
+    s = Solver()
+    s.prepare(p)
+    s.run()
+    best = min((s.run(), s.stats().solve_ms)[1] for _ in range(3))
+    iso.append(best)
+    s.close()
+print("isolated unit solve ms:", " ".join(f"{t:.2f}" for t in iso))
+print(f"sum of isolated unit solves: {sum(iso):.1f} ms  (mean {sum(iso) / len(iso):.2f} ms)")
+b = BatchSolver(subs)
+b.run()
+ts = []
+for _ in range(5):
+    t0 = time.perf_counter()
+    b.run()
+    ts.append(1e3 * (time.perf_counter() - t0))
+print("concurrent batch wall ms:", " ".join(f"{t:.1f}" for t in ts))
+b.close()
