@@ -30,7 +30,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # built without FMA); the FP32 NN filter requests its FMAs explicitly.
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3",
               "-diag-suppress", "177", f"-I{ROOT / 'include'}"]
-SOURCES = ["kernels.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "register.cu", "sdf_build.cu", "solver.cu",
+# Diagnostic builds only (e.g. ASICP_NVCC_EXTRA=-DASICP_NN_PHASES, tools/nn_phases.sh).
+NVCC_FLAGS += os.environ.get("ASICP_NVCC_EXTRA", "").split()
+SOURCES = ["kernels.cu", "collide.cu", "median.cu", "nn.cu", "minibatch.cu", "exchange.cu", "register.cu", "sdf_build.cu", "solver.cu",
            "trace_io.cpp"]
 FX_SOURCE = "fixtures.cu"
 

@@ -30,6 +30,15 @@ __device__ __forceinline__ float nn_margin(double A, double B) {
   return __double2float_ru(2.0 * (e32 + e64));
 }
 
+// The same bound evaluated in FP32 with upward rounding (A, B upper bounds).
+__device__ __forceinline__ float nn_margin32(float A, float B) {
+  const float e32 = __fmul_ru(6.0206e-08f /* 1.01 u, rounded up */,
+                              __fadd_ru(__fmul_ru(6.0f, __fmul_ru(B, B)), __fmul_ru(10.0f, __fmul_ru(A, B))));
+  const float s = __fadd_ru(A, B);
+  const float e64 = __fmul_ru(8.881784197001252e-16f, __fmul_ru(s, s));
+  return __fmul_ru(2.0f, __fadd_ru(e32, e64));
+}
+
 // Forward NN candidates (the object cloud and the minibatch pools) are stored
 // pair-interleaved: candidates 2p and 2p + 1 occupy two float4s,
 // (x0, x1, y0, y1) and (z0, z1, w0, w1), so one LDS.128 yields ready-made

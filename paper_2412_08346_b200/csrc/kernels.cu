@@ -22,6 +22,56 @@ __global__ void seed_rng_kernel(uint64_t* state, int* mti, uint64_t seed, int J)
   mti[j] = mt::kN;
 }
 
+// Constants of the collision pre-test of particle j (collide.cu): the FP32
+// inverse pose, the grid box and the rigorous rounding margins.
+__device__ void col_constants(const DevProblem& P, int pre, const double* th, ColConst* out) {
+  const Grid& g = P.grids[P.pre_sdf[pre]];
+  ColConst K;
+  Q4 qi;
+  V3 ti;
+  inverse(pose_q(th), pose_t(th), &qi, &ti);
+  const M3 r = rotation_matrix(qi);
+  for (int i = 0; i < 9; ++i) K.r[i] = static_cast<float>(r.m[i]);
+  K.t[0] = static_cast<float>(ti.x);
+  K.t[1] = static_cast<float>(ti.y);
+  K.t[2] = static_cast<float>(ti.z);
+  float lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = static_cast<float>(g.origin[a]);
+    hi[a] = static_cast<float>(g.origin[a] + g.voxel * static_cast<double>(g.dims[a] - 1));
+    K.lo[a] = lo[a];
+    K.cx[a] = 0.5f * (lo[a] + hi[a]);
+    K.hx[a] = 0.5f * (hi[a] - lo[a]);
+  }
+  const float tn = fabsf(K.t[0]) + fabsf(K.t[1]) + fabsf(K.t[2]) + fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) +
+                   fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]);
+  // Box as centre +- half extent; cbox covers the rounding of cx, hx and of
+  // the |l - c| - h evaluation (a few ulps of the box coordinates).
+  const float cbox =
+      1e-6f * (fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) + fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]));
+  // |l32 - l64| <= ~5u (|p|_1 + |t|_1) per axis: d = 1e-6 |p|_1 + d0 is >= 3x that.
+  K.d0 = 1e-6f * (1.0f + tn) + cbox;
+  K.inv_vox = static_cast<float>(1.0 / g.voxel);
+  const double tol = P.contact_tolerance;
+  K.tol32 = static_cast<float>(tol);
+  float tdn = static_cast<float>(tol);
+  if (static_cast<double>(tdn) > tol) tdn = nextafterf(tdn, -INFINITY);
+  K.tol_dn = tdn;
+  const double coarse_cut = tol - 1e-12 * (1.0 + fabs(tol));
+  float cut32 = static_cast<float>(coarse_cut);
+  if (static_cast<double>(cut32) >= coarse_cut) cut32 = nextafterf(cut32, -INFINITY);
+  K.cut32 = cut32;
+  K.cull_ok = tol >= -g.boundary_max_abs ? 1 : 0;
+  // Value margins: slope x position error; fraction rounding (3 roundings of
+  // u <= max dim + 1 voxels, 2^-22 relative) and 7 FP32 lerps / the rounded
+  // tolerance (~1e-6 x magnitudes).
+  const int maxdim = max(g.dims[0], max(g.dims[1], g.dims[2]));
+  K.vm_pos = static_cast<float>(g.lip);
+  K.vm_c = static_cast<float>(g.lip * g.voxel * 2.4e-7 * (maxdim + 2) + 1e-6 * (g.vmax + fabs(tol)) + 1e-9);
+  K.lip = static_cast<float>(g.lip * (1.0 + 1e-6));
+  *out = K;
+}
+
 // ---------------------------------------------------------------------------
 // K1: pose preparation — R(q) and S_world = R s + t (apply_transform,
 // geometry.cpp:68-74) in FP64, plus two FP32 forms for the NN filter:
@@ -42,6 +92,7 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   const int64_t o = P.part_surf_off[j];
   const V3 tcp = V3{P.pre_tcp[3 * pre], P.pre_tcp[3 * pre + 1], P.pre_tcp[3 * pre + 2]};
   const V3 c = transform(r, t, tcp);
+  if (threadIdx.x == 0) col_constants(P, pre, th, S.colc + j);
   __shared__ double s_bmax[kNnThreads];
   double bmax = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -73,201 +124,7 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// K2: collision test — colliding_points (sdf.cpp:227-243) with query(stacked)
-// (sdf.cpp:220-225) and trilinear query (sdf.cpp:177-203), FP64.  Writes the
-// colliding scene indices in scene order and their FP32 reverse-match queries.
-// count_only: final ranking (only N_col == 0 matters, grasp.cpp:271-274).
-// ---------------------------------------------------------------------------
-//
-// Most scene points lie far outside the gripper's grid box, where the
-// reference returns -(distance + boundary_max_abs) <= -boundary_max_abs.  When
-// contact_tolerance >= -boundary_max_abs such points can never collide, so an
-// FP32 transform that places a point outside the box by more than a
-// conservative rounding margin decides it without the FP64 path; every other
-// point takes the exact FP64 evaluation.  Each warp owns a contiguous scene
-// range; hits are kept as a bitmask in shared memory and compacted in scene
-// order after a scan over the warps' counts.
-constexpr int kColThreads = 256;
-constexpr int kColWarps = kColThreads / 32;
-
-// The exact FP64 test of one scene point (colliding_points body,
-// sdf.cpp:237-239), kept out of line so its register needs do not throttle
-// the FP32 pre-test loop (it runs for ~1e-4 of the points).
-__device__ __noinline__ bool collide_exact(const double* th, const Grid* gp, const float* values, const double* p64,
-                                           double tol) {
-  const Grid& g = *gp;
-  Q4 qi;
-  V3 ti;
-  inverse(pose_q(th), pose_t(th), &qi, &ti);
-  const M3 r = rotation_matrix(qi);
-  const V3 off = V3{g.offset[0], g.offset[1], g.offset[2]};
-  const V3 local = sub(add(add(mul(r, V3{p64[0], p64[1], p64[2]}), ti), off), off);
-  return sdf_query(g, values, local.x, local.y, local.z) > tol;
-}
-
-__global__ void __launch_bounds__(kColThreads, 3) collide_kernel(DevProblem P, DevState S, int all, int count_only) {
-  const int j = blockIdx.x;
-  if (!all && !S.active[j]) return;
-  extern __shared__ __align__(16) unsigned int hitbits[];  // ceil(n_scene / 32) words, then the coarse grid
-  __shared__ int warp_cnt[kColWarps];
-  const int pre = P.part_pre[j];
-  const Grid g = P.grids[P.pre_sdf[pre]];
-  float* coarse_s = reinterpret_cast<float*>(hitbits + round_up((P.n_scene + 31) / 32, 4));
-  const int ncoarse = g.cdims[0] * g.cdims[1] * g.cdims[2];
-  for (int i = threadIdx.x; i < ncoarse; i += blockDim.x) coarse_s[i] = P.sdf_coarse[g.coarse_offset + i];
-  const double coarse_cut = P.contact_tolerance - 1e-12 * (1.0 + fabs(P.contact_tolerance));
-  __syncthreads();
-  const double* th = th_of(S.theta, j);
-  Q4 qi;
-  V3 ti;
-  inverse(pose_q(th), pose_t(th), &qi, &ti);
-  const M3 r = rotation_matrix(qi);
-  const V3 off = V3{g.offset[0], g.offset[1], g.offset[2]};
-  // FP32 culling box (sdf.cpp:178-182 out-of-grid test) with margin.
-  float r32[9];
-  for (int i = 0; i < 9; ++i) r32[i] = static_cast<float>(r.m[i]);
-  const float t32x = static_cast<float>(ti.x), t32y = static_cast<float>(ti.y), t32z = static_cast<float>(ti.z);
-  float lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    lo[a] = static_cast<float>(g.origin[a]);
-    hi[a] = static_cast<float>(g.origin[a] + g.voxel * static_cast<double>(g.dims[a] - 1));
-  }
-  const float tn = fabsf(t32x) + fabsf(t32y) + fabsf(t32z) + fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) +
-                   fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]);
-  // Box as centre +- half extent; cbox covers the rounding of cx, hx and of
-  // the |l - c| - h evaluation (a few ulps of the box coordinates).
-  float cx[3], hx[3];
-  for (int a = 0; a < 3; ++a) {
-    cx[a] = 0.5f * (lo[a] + hi[a]);
-    hx[a] = 0.5f * (hi[a] - lo[a]);
-  }
-  const float cbox = 1e-6f * (fabsf(lo[0]) + fabsf(lo[1]) + fabsf(lo[2]) + fabsf(hi[0]) + fabsf(hi[1]) + fabsf(hi[2]));
-  const float d0 = 1e-6f * (1.0f + tn) + cbox;
-  // Largest float below coarse_cut: cm < coarse_cut  <=>  cm <= cut32.
-  float cut32 = static_cast<float>(coarse_cut);
-  if (static_cast<double>(cut32) >= coarse_cut) cut32 = nextafterf(cut32, -INFINITY);
-  const bool cull_ok = P.contact_tolerance >= -g.boundary_max_abs;
-  const float inv_vox = static_cast<float>(1.0 / g.voxel);
-  const float tol32 = static_cast<float>(P.contact_tolerance);
-  // Value margin: slope x position error, plus fraction rounding (|u| <= dims,
-  // ~1e-5 voxel) and 7 FP32 lerps / the rounded tolerance (~1e-6 x magnitudes).
-  const float vmargin_pos = static_cast<float>(g.lip);
-  const float vmargin_c = static_cast<float>(g.lip * g.voxel * 1e-5 + 1e-6 * (g.vmax + fabs(P.contact_tolerance)) +
-                                             1e-9);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nwords = (P.n_scene + 31) / 32;
-  const int words_per_warp = (nwords + kColWarps - 1) / kColWarps;
-  const int w0 = wid * words_per_warp, w1 = min(nwords, w0 + words_per_warp);
-  int cnt = 0;
-  // Status per point: 0 clear, 1 colliding, 2 needs the exact FP64 test.
-  auto classify = [&](float4 p) -> int {
-    int status = 2;
-    {
-      {
-        const float fx = p.x, fy = p.y, fz = p.z;
-        const float lx = __fmaf_rn(r32[0], fx, __fmaf_rn(r32[1], fy, __fmaf_rn(r32[2], fz, t32x)));
-        const float ly = __fmaf_rn(r32[3], fx, __fmaf_rn(r32[4], fy, __fmaf_rn(r32[5], fz, t32y)));
-        const float lz = __fmaf_rn(r32[6], fx, __fmaf_rn(r32[7], fy, __fmaf_rn(r32[8], fz, t32z)));
-        // |l32 - l64| <= ~5u (|p|_1 + |t|_1) (+ the rounded box corners): d is
-        // >= 3x that (p.w = |p|_1, prepared on the host).
-        const float d = __fmaf_rn(1e-6f, p.w, d0);
-        // Signed distance outside the box along the worst axis (> 0: outside).
-        const float e = fmaxf(fmaxf(fabsf(lx - cx[0]) - hx[0], fabsf(ly - cx[1]) - hx[1]), fabsf(lz - cx[2]) - hx[2]);
-        const bool out_far = e > d;
-        const bool in_far = e < -d;
-        if (out_far) {
-          if (cull_ok) status = 0;  // value <= -boundary_max_abs <= contact_tolerance: never collides
-        } else if (in_far) {
-          // FP32 trilinear; the interpolant is continuous with per-axis slope
-          // <= lip, so |v32 - v64| <= lip * (|e|_1 + fraction error) + lerp rounding.
-          const float ux = (lx - lo[0]) * inv_vox, uy = (ly - lo[1]) * inv_vox, uz = (lz - lo[2]) * inv_vox;
-          const int ix = max(min(static_cast<int>(ux), g.dims[0] - 2), 0);
-          const int iy = max(min(static_cast<int>(uy), g.dims[1] - 2), 0);
-          const int iz = max(min(static_cast<int>(uz), g.dims[2] - 2), 0);
-          // Coarse bound: the FP64 cell is within one cell of this one, and its
-          // trilinear value is a convex combination of nodes the dilated block
-          // max covers — below the tolerance, the point cannot collide.
-          const float cm = coarse_s[((static_cast<unsigned>(ix) >> 2) * g.cdims[1] + (static_cast<unsigned>(iy) >> 2)) *
-                                        g.cdims[2] +
-                                    (static_cast<unsigned>(iz) >> 2)];  // kCoarse = 4
-          if (cm <= cut32) return 0;
-          const float fxx = fminf(fmaxf(ux - ix, 0.0f), 1.0f), fyy = fminf(fmaxf(uy - iy, 0.0f), 1.0f),
-                      fzz = fminf(fmaxf(uz - iz, 0.0f), 1.0f);
-          const float* v0 = P.sdf_values + g.values_offset + (static_cast<int64_t>(ix) * g.dims[1] + iy) * g.dims[2] + iz;
-          const int sy = g.dims[2], sx = g.dims[1] * g.dims[2];
-          const float c00 = __fmaf_rn(fxx, v0[sx] - v0[0], v0[0]);
-          const float c01 = __fmaf_rn(fxx, v0[sx + 1] - v0[1], v0[1]);
-          const float c10 = __fmaf_rn(fxx, v0[sx + sy] - v0[sy], v0[sy]);
-          const float c11 = __fmaf_rn(fxx, v0[sx + sy + 1] - v0[sy + 1], v0[sy + 1]);
-          const float c0 = __fmaf_rn(fyy, c10 - c00, c00);
-          const float c1 = __fmaf_rn(fyy, c11 - c01, c01);
-          const float v32 = __fmaf_rn(fzz, c1 - c0, c0);
-          const float mv = vmargin_pos * 3.0f * d + vmargin_c;
-          if (v32 > tol32 + mv)
-            status = 1;
-          else if (v32 < tol32 - mv)
-            status = 0;
-        }
-      }
-    }
-    return status;
-  };
-  constexpr int kU = 4;  // words per batch: independent loads in flight
-  for (int wb = w0; wb < w1; wb += kU) {
-    float4 pv[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = (wb + u) * 32 + lane;
-      pv[u] = (wb + u < w1 && idx < P.n_scene) ? P.scene32[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    int stt[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = (wb + u) * 32 + lane;
-      stt[u] = (wb + u < w1 && idx < P.n_scene) ? classify(pv[u]) : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (wb + u >= w1) break;
-      bool hit = stt[u] == 1;
-      if (stt[u] == 2)
-        hit = collide_exact(th, P.grids + P.pre_sdf[pre], P.sdf_values,
-                            P.scene64 + 3 * static_cast<int64_t>((wb + u) * 32 + lane), P.contact_tolerance);
-      const unsigned mask = __ballot_sync(0xffffffffu, hit);
-      if (lane == 0) hitbits[wb + u] = mask;
-      cnt += __popc(mask);
-    }
-  }
-  if (lane == 0) warp_cnt[wid] = cnt;
-  __syncthreads();
-  int base = 0, total = 0;
-  for (int w = 0; w < kColWarps; ++w) {
-    base += w < wid ? warp_cnt[w] : 0;
-    total += warp_cnt[w];
-  }
-  if (!count_only && cnt > 0) {
-    const int64_t row = static_cast<int64_t>(j) * P.n_scene;
-    const double B = S.Bs[j];
-    const V3 c = V3{S.ctr[3 * j], S.ctr[3 * j + 1], S.ctr[3 * j + 2]};
-    for (int w = w0; w < w1; ++w) {
-      const unsigned mask = hitbits[w];
-      if (mask == 0) continue;
-      if ((mask >> lane) & 1u) {
-        const int idx = w * 32 + lane;
-        const int slot = base + __popc(mask & ((1u << lane) - 1u));
-        S.col_idx[row + slot] = idx;
-        const V3 p = load3(P.scene64, idx);
-        const double ax = p.x - c.x, ay = p.y - c.y, az = p.z - c.z;
-        const double A = sqrt(ax * ax + ay * ay + az * az);
-        S.col_q[row + slot] =
-            make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az), nn_margin(A, B));
-      }
-      base += __popc(mask);
-    }
-  }
-  if (threadIdx.x == 0) S.n_col[j] = total;
-}
+// K2: collision test — collide.cu.
 
 // ---------------------------------------------------------------------------
 // K5: minibatch sampling — sample_minibatch / sample_minibatch_indices
@@ -506,7 +363,7 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
 
 // Small populations: median_kernel in median.cu.
 
-// Large populations (K >= kMedBigK, e.g. cfg5's 16384 particles: 134M pair
+// Large populations (K > kMedClusterK, e.g. cfg5's 16384 particles: 134M pair
 // keys): the same exact radix select spread over the whole GPU.  Six passes
 // of 12/12/12/12/12/4 bits; every pass recomputes the keys tile by tile
 // (128 x 128 blocks of the upper triangle, partner poses in shared memory —
@@ -522,7 +379,7 @@ __device__ __forceinline__ bool med_big(const DevProblem& P, int pop, int& b, in
   if (P.pop_off[pop + 1] == P.pop_off[pop] || P.bandwidth_mode == 1) return false;
   b = P.gpop_off[pop];
   K = P.gpop_off[pop + 1] - b;
-  return K >= kMedBigK;
+  return K > kMedClusterK;
 }
 
 __global__ void med_init_kernel(DevProblem P, DevState S) {
@@ -750,6 +607,35 @@ __global__ void __launch_bounds__(256) svgd_kmat_kernel(DevProblem P, DevState S
   }
 }
 
+__device__ __forceinline__ void acc_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void acc_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void acc_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void acc_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// The ordered sums.  One thread per (own particle, pose component) keeps the
+// reference's left-to-right accumulation over the partners; tiles of
+// kAccTile partners (kernel values, drifts, poses) are staged in shared
+// memory by cp.async through a kAccStages-deep ring, so the loads run
+// (kAccStages - 1) tiles ahead of the sums (more than the L2 latency).  Every
+// term is formed off the chain, so the chain is the DADDs alone.  The self
+// term (optim.cpp:206-212, acc = acc - d with no repulsion) enters as the
+// terms (-d, +0.0): acc + (-d) is acc - d, and acc + 0.0 is acc because a
+// running sum that starts at +0.0 is never -0.0 (an exact zero sum rounds to
+// +0.0).
+constexpr int kAccTile = 64;
+constexpr int kAccStages = 4;
+constexpr int kAccSmem = kAccStages * (kAccTile * kSvgdJ * 16 + 2 * kAccTile * 7 * 8);
 __global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevState S, double eta) {
   const int pop = blockIdx.y;
   const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;
@@ -757,10 +643,15 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevS
   const int j0 = blockIdx.x * kSvgdJ;
   if (j0 >= Kl) return;
   __shared__ double dir[kSvgdJ][7];
-  __shared__ double2 kt[kSvgdJ][kSvgdJ];  // [partner][own] of the current 32-partner tile
-  __shared__ double dt[kSvgdJ][7], tt[kSvgdJ][7];
+  extern __shared__ __align__(16) unsigned char acc_smem[];
+  // Stage s: kernel values [kAccTile][kSvgdJ] (partner-major), then drifts and
+  // poses [kAccTile * 7].
+  auto kt_of = [&](int s) {
+    return reinterpret_cast<double2*>(acc_smem + s * (kAccTile * kSvgdJ * 16 + 2 * kAccTile * 7 * 8));
+  };
+  auto dt_of = [&](int s) { return reinterpret_cast<double*>(kt_of(s) + kAccTile * kSvgdJ); };
+  auto tt_of = [&](int s) { return dt_of(s) + kAccTile * 7; };
   constexpr int kT = kSvgdJ * 7;
-  constexpr int kPer = (kSvgdJ * kSvgdJ + kT - 1) / kT;
   const int tid = threadIdx.x;
   const int comp = tid / 32, jl = tid % 32;
   const int nj = min(kSvgdJ, Kl - j0);
@@ -768,47 +659,101 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevS
   const double two_h = 2.0 / S.h[pop];
   const double own = jl < nj ? S.theta[7 * (lb + j0 + jl) + comp] : 0.0;
   const double2* km = S.kmat + P.kofs[pop];
-  // The next tile is fetched into registers while the current one is summed.
-  double2 rk[kPer];
-  double rd = 0.0, rt = 0.0;
-  auto fetch = [&](int i0) {
-    const int ni = min(kSvgdJ, K - i0);
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kT, ii = e / kSvgdJ, jj = e % kSvgdJ;
-      rk[u] = (e < kSvgdJ * kSvgdJ && ii < ni && jj < nj) ? km[static_cast<int64_t>(i0 + ii) * Kl + j0 + jj]
-                                                          : make_double2(0.0, 0.0);
-    }
-    const int r = tid / 7, a = tid % 7;
-    rd = r < ni ? S.drift_all[7 * (b + i0 + r) + a] : 0.0;
-    rt = r < ni ? S.theta_all[7 * (b + i0 + r) + a] : 0.0;
-  };
-  fetch(0);
-  double acc = 0.0;
-  for (int i0 = 0; i0 < K; i0 += kSvgdJ) {
-    __syncthreads();  // the previous tile is consumed
-#pragma unroll
-    for (int u = 0; u < kPer; ++u) {
-      const int e = tid + u * kT;
-      if (e < kSvgdJ * kSvgdJ) kt[e / kSvgdJ][e % kSvgdJ] = rk[u];
-    }
-    dt[tid / 7][tid % 7] = rd;
-    tt[tid / 7][tid % 7] = rt;
-    __syncthreads();
-    if (i0 + kSvgdJ < K) fetch(i0 + kSvgdJ);
-    const int ni = min(kSvgdJ, K - i0);
-    for (int ii = 0; ii < ni; ++ii) {
-      const double d = dt[ii][comp];
-      if (i0 + ii == jg) {
-        acc = acc - d;  // analytic self-term (optim.cpp:206-212)
-      } else if (comp < 3) {
-        const double v = kt[ii][jl].x;
-        acc = acc + (-d) * v;
-        acc = acc + (two_h * (own - tt[ii][comp])) * v;
-      } else {
-        acc = acc + (-d) * kt[ii][jl].y;
+  const int ntiles = (K + kAccTile - 1) / kAccTile;
+  auto issue = [&](int t) {  // always commits a group (possibly empty) so the wait counts stay uniform
+    if (t < ntiles) {
+      const int s = t % kAccStages, i0 = t * kAccTile;
+      const int ni = min(kAccTile, K - i0);
+      double2* kt = kt_of(s);
+      for (int e = tid; e < ni * kSvgdJ; e += kT) {
+        const int ii = e / kSvgdJ, jj = e % kSvgdJ;
+        if (jj < nj) acc_cp16(kt + ii * kSvgdJ + jj, km + static_cast<int64_t>(i0 + ii) * Kl + j0 + jj);
+      }
+      double* dt = dt_of(s);
+      double* tt = tt_of(s);
+      for (int e = tid; e < ni * 7; e += kT) {
+        acc_cp8(dt + e, S.drift_all + 7 * static_cast<int64_t>(b + i0) + e);
+        acc_cp8(tt + e, S.theta_all + 7 * static_cast<int64_t>(b + i0) + e);
       }
     }
+    acc_commit();
+  };
+  for (int t = 0; t < kAccStages - 1; ++t) issue(t);
+  double acc = 0.0;
+  for (int t = 0; t < ntiles; ++t) {
+    issue(t + kAccStages - 1);  // into the stage consumed at t - 1 (released by the barrier below)
+    acc_wait<kAccStages - 1>();
+    __syncthreads();  // tile t resident for every thread
+    const int s = t % kAccStages, i0 = t * kAccTile;
+    const int ni = min(kAccTile, K - i0);
+    const double2* kt = kt_of(s);
+    const double* dcol = dt_of(s) + comp;
+    const double* tcol = tt_of(s) + comp;
+    // Terms of block q + 1 (8 partners) are formed while block q is summed,
+    // so the chain runs at the DADD latency.
+    constexpr int kB = 8;
+    if (comp < 3) {
+      auto terms = [&](int q, double* x1, double* x2) {
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int ii = min(q * kB + u, ni - 1);
+          const double d = dcol[7 * ii];
+          const double v = kt[ii * kSvgdJ + jl].x;
+          const bool self = i0 + ii == jg;
+          x1[u] = self ? -d : (-d) * v;
+          x2[u] = self ? 0.0 : (two_h * (own - tcol[7 * ii])) * v;
+        }
+      };
+      const int nq = (ni + kB - 1) / kB;
+      double a1[kB], a2[kB], b1[kB], b2[kB];
+      terms(0, a1, a2);
+      for (int q = 0; q < nq; q += 2) {
+        terms(q + 1, b1, b2);
+        const int na = min(kB, ni - q * kB);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (u < na) {
+            acc = acc + a1[u];
+            acc = acc + a2[u];
+          }
+        if (q + 1 >= nq) break;
+        terms(q + 2, a1, a2);
+        const int nb = min(kB, ni - (q + 1) * kB);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (u < nb) {
+            acc = acc + b1[u];
+            acc = acc + b2[u];
+          }
+      }
+    } else {
+      auto terms = [&](int q, double* x1) {
+#pragma unroll
+        for (int u = 0; u < kB; ++u) {
+          const int ii = min(q * kB + u, ni - 1);
+          const double d = dcol[7 * ii];
+          const bool self = i0 + ii == jg;
+          x1[u] = self ? -d : (-d) * kt[ii * kSvgdJ + jl].y;
+        }
+      };
+      const int nq = (ni + kB - 1) / kB;
+      double a1[kB], b1[kB];
+      terms(0, a1);
+      for (int q = 0; q < nq; q += 2) {
+        terms(q + 1, b1);
+        const int na = min(kB, ni - q * kB);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (u < na) acc = acc + a1[u];
+        if (q + 1 >= nq) break;
+        terms(q + 2, a1);
+        const int nb = min(kB, ni - (q + 1) * kB);
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (u < nb) acc = acc + b1[u];
+      }
+    }
+    __syncthreads();  // stage s consumed before it is refilled (issue at t + 1)
   }
   if (jl < nj) dir[jl][comp] = acc;
   __syncthreads();
@@ -1049,13 +994,6 @@ void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st) {
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st) {
   pose_prep_kernel<<<P.J, kNnThreads, 0, st>>>(P, S, all);
 }
-void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(round_up((P.n_scene + 31) / 32, 4)) * sizeof(unsigned int) +
-                      static_cast<size_t>(P.max_coarse) * sizeof(float);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(collide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  collide_kernel<<<P.J, kColThreads, smem, st>>>(P, S, all, count_only);
-}
 int minibatch_smem_cap() { return 160 * 1024; }
 
 // Opt-in shared-memory sizes of this file's kernels on the current device
@@ -1063,6 +1001,7 @@ int minibatch_smem_cap() { return 160 * 1024; }
 void kernels_set_attrs() {
   cudaFuncSetAttribute(minibatch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, minibatch_smem_cap());
   cudaFuncSetAttribute(cost_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCostSmem);
+  cudaFuncSetAttribute(svgd_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAccSmem);
 }
 
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
@@ -1125,7 +1064,7 @@ int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_po
       launch_svgd_kmat(P, S, max_pop, max_gpop, st);
       ++n;
     }
-    svgd_acc_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
+    svgd_acc_kernel<<<grid, kSvgdJ * 7, kAccSmem, st>>>(P, S, eta);
   } else {
     svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
   }

@@ -25,6 +25,13 @@ struct DevProblem {
   const float4* obj_cand4;  // the same candidates one float4 per point (minibatch pool gathers)
   const double* scene64;    // C, n_scene x 3
   const float4* scene32;    // C rounded to FP32 (x, y, z, |p|_1 rounded up), for the collision pre-test
+  // Collision clusters (collide.cu): the scene sorted along a Morton curve and
+  // cut into clusters of kClusterPts points; FP32 centre + radius per cluster.
+  int n_clusters;
+  const float4* clusters;   // (cx, cy, cz, r), r >= max |p - c|
+  const float4* subclusters;  // n_clusters x kSubPerCluster spheres of kSubPts points
+  const float4* scene_s32;  // scene32 in sorted order, n_clusters x kClusterPts
+  const int* scene_perm;    // sorted position -> scene index (-1: padding)
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
   const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
   const double* pre_tcp;    // preshape tcp, 3 per preshape
@@ -44,6 +51,7 @@ struct DevProblem {
   // Unsharded: j_lo = 0, gpop_off = pop_off, theta_all = theta.
   const int* gpop_off;      // population -> first global particle (n_pop + 1)
   int j_lo;
+  int med_mid;              // some population takes the cluster median (kMedBigK <= K <= kMedClusterK)
   const long long* kofs;    // population -> offset of its K x K_local block in DevState::kmat (split SVGD)
   double center[3];         // FP32 re-centring origin of the forward match (object centroid)
   double B_obj;             // max |r - center| over R (with slack)
@@ -60,8 +68,24 @@ struct DevProblem {
   double conv_thr;
 };
 
-// Populations at least this large take the grid-wide median select.
+// Per-particle constants of the collision kernel's FP32 tests (collide.cu),
+// derived in pose_prep_kernel from the FP64 inverse pose and the grid.
+struct ColConst {
+  float r[9], t[3];     // FP32 rotation / translation of the inverse pose
+  float lo[3], cx[3], hx[3];  // grid box: origin, centre, half extent
+  float d0;             // per-axis transform error bound, without the |p|_1 term
+  float inv_vox;
+  float tol32, tol_dn;  // float(tol), and the largest float <= tol
+  float cut32;          // the largest float below the coarse cut
+  float vm_pos, vm_c;   // value margins: per unit of position error, constant
+  float lip;
+  int cull_ok;
+};
+
+// Median select: populations below kMedBigK in one CTA, up to kMedClusterK
+// in one thread-block cluster (median.cu), larger ones grid-wide (kernels.cu).
 constexpr int kMedBigK = 320;
+constexpr int kMedClusterK = 1536;
 struct MedState {
   unsigned long long prefix, mask;
   long long rank;
@@ -91,6 +115,7 @@ struct DevState {
   float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred
   double* ctr;         // J x 3 per-particle reverse-match centre (TCP in world)
   double* Bs;          // per particle max |s - ctr|
+  ColConst* colc;      // per particle collision-test constants
   int* col_idx;        // J x n_scene colliding scene indices (scene order)
   float4* col_q;       // J x n_scene FP32 reverse queries (particle-centred)
   int* res_fwd;        // per surface row: NN position in the candidate set
@@ -138,10 +163,12 @@ struct NnPlan {
 
 // Per-device kernel attributes (opt-in shared memory), set for every context.
 void kernels_set_attrs();
+void collide_set_attrs();
 void median_set_attrs();
 void minibatch_set_attrs();
 inline void set_all_kernel_attrs() {
   kernels_set_attrs();
+  collide_set_attrs();
   median_set_attrs();
   minibatch_set_attrs();
 }
@@ -154,7 +181,17 @@ int build_sdf_device(int device, cudaStream_t st, const double* cloud, int64_t n
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st);
 void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);
-void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);
+void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);  // collide.cu
+constexpr int kClusterPts = 32;
+constexpr int kSubPts = 8;
+constexpr int kSubPerCluster = kClusterPts / kSubPts;
+size_t scene_sort_temp_bytes(int n);
+// Builds scene32 (original order) and the collision clusters from scene64 on
+// the device: box, Morton codes, a stable radix sort, per-cluster centre and
+// radius.  code/idx buffers: n each; temp: scene_sort_temp_bytes(n).
+void launch_scene_prepare(const double* scene64, int n, float4* s32, double* box, unsigned int* code_in,
+                          unsigned int* code_out, int* idx_in, int* perm, void* temp, size_t temp_bytes,
+                          float4* clusters, float4* subclusters, float4* s32s, int* perm_pad, cudaStream_t st);
 void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
 bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st);  // minibatch.cu
 int minibatch_smem_cap();

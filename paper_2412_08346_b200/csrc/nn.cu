@@ -380,14 +380,18 @@ __device__ __noinline__ RunState subchunk_window(const DevState& S, const float4
           const int sid = r == 0 ? (s12 & 0xffff) : (s12 >> 16);
           const uint32_t sp = tiles_s + static_cast<uint32_t>(sid * kSub) * 16u;
           unsigned mask = 0;
-#pragma unroll 8
+#pragma unroll
           for (int c = 0; c < kSub; c += 2) {
-            // One interleaved pair (two 16-byte loads): candidates c and c + 1.
+            // One interleaved pair (two 16-byte loads): candidates c and c + 1,
+            // evaluated together by packed FMAs (each lane is d32()).
             const float4 A = lds128(sp + c * 16u), B = lds128(sp + (c + 1) * 16u);
-            const float d0 = d32(qx, qy, qz, make_float4(A.x, A.z, B.x, B.z));
-            const float d1 = d32(qx, qy, qz, make_float4(A.y, A.w, B.y, B.w));
-            mask |= (d0 <= thr ? 1u : 0u) << c;
-            mask |= (d1 <= thr ? 1u : 0u) << (c + 1);
+            f32x2 d = ffma2(pk2(B.x, B.y), pk2(qz, qz), pk2(B.z, B.w));
+            d = ffma2(pk2(A.z, A.w), pk2(qy, qy), d);
+            d = ffma2(pk2(A.x, A.y), pk2(qx, qx), d);
+            float d0, d1;
+            up2(d, d0, d1);
+            if (d0 <= thr) mask |= 1u << c;
+            if (d1 <= thr) mask |= 1u << (c + 1);
           }
           while (mask) {
             const int c = __ffs(mask) - 1;
@@ -477,6 +481,25 @@ __device__ __noinline__ void emit_ambiguous(const DevProblem& P, const DevState&
 // 4 CTAs (16 warps) per SM: with the packed FFMA2 main loop the kernel fits
 // 128 registers without spilling, and the extra warps hide the FFMA2 / LDS
 // latencies that stall a 2-CTA configuration.
+// -DASICP_NN_PHASES: per-warp clock() accounting of the filter's phases
+// (diagnostic build; tools/nn_phases.sh), summed into stats[240 + phase].
+#ifdef ASICP_NN_PHASES
+#define NNPH_DECL unsigned int ph_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}; unsigned int ph_t = clock();
+#define NNPH(i)                        \
+  {                                    \
+    const unsigned int ph_now = clock(); \
+    ph_acc[i] += ph_now - ph_t;        \
+    ph_t = ph_now;                     \
+  }
+#define NNPH_FLUSH                                                                               \
+  if ((threadIdx.x & 31) == 0)                                                                   \
+    for (int i_ = 0; i_ < 8; ++i_) atomicAdd(S.stats + 240 + i_, static_cast<unsigned long long>(ph_acc[i_]));
+#else
+#define NNPH_DECL
+#define NNPH(i)
+#define NNPH_FLUSH
+#endif
+
 template <int Q>
 #ifndef ASICP_NN_MINBLOCKS
 #define ASICP_NN_MINBLOCKS 4
@@ -500,6 +523,7 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
   const int n_items = list == 0 ? S.nn_dyn[1] : S.item_off[list][P.J];
   const NnItem* items = S.items[list];
   uint32_t phases = 0;  // bit s: parity of the next completion of stage s
+  NNPH_DECL
   for (;;) {
     if (tid == 0) s_item = atomicAdd(S.item_counter + list, 1);
     __syncthreads();
@@ -544,15 +568,17 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
         }
       }
       float b1[Q], b2[Q], b3[Q];
-      int s12[Q];
+      int s1v[Q], s2v[Q];
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
         b1[k] = b2[k] = b3[k] = INFINITY;
-        s12[k] = 0;
+        s1v[k] = s2v[k] = 0;
       }
+      NNPH(0)
       for (int t = 0; t < ntiles; ++t) {
         mbar_wait(&full_bar[t], (phases >> t) & 1u);
         phases ^= 1u << t;
+        NNPH(1)
         const float4* tile = tiles + t * kNnTile;
         const int nsub = min(kNnTile, nsc_pad - t * kNnTile) / kSub;
         for (int sub = 0; sub < nsub; ++sub) {
@@ -596,32 +622,71 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
               tm[k] = fminf(fminf(tm[k], fminf(l0, h0)), fminf(l1, h1));
             }
           }
+          NNPH(2)
           const int sid = t * (kNnTile / kSub) + sub;
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
-            // Running top-3 of subtile minima (strict < keeps the earliest).
+            // Running top-3 of subtile minima as a min/max network (equal
+            // values keep the earlier subtile: positions move on strict <).
             const bool lt1 = tm[k] < b1[k];
             const bool lt2 = tm[k] < b2[k];
-            b3[k] = lt2 ? b2[k] : fminf(b3[k], tm[k]);
-            const int s1 = s12[k] & 0xffff;
-            const int s2 = lt1 ? s1 : (lt2 ? sid : (s12[k] >> 16));
-            b2[k] = lt1 ? b1[k] : (lt2 ? tm[k] : b2[k]);
-            b1[k] = lt1 ? tm[k] : b1[k];
-            s12[k] = (lt1 ? sid : s1) | (s2 << 16);
+            b3[k] = fminf(b3[k], fmaxf(b2[k], tm[k]));
+            b2[k] = fminf(b2[k], fmaxf(b1[k], tm[k]));
+            b1[k] = fminf(b1[k], tm[k]);
+            s2v[k] = lt1 ? s1v[k] : (lt2 ? sid : s2v[k]);
+            s1v[k] = lt1 ? sid : s1v[k];
           }
+          NNPH(3)
         }
       }
       // Sub-chunk epilogue (candidates still resident): members of the
       // sub-chunk's window and the position of its minimum, merged into the
       // running window (an explicit member list only once it holds two).
+      // Common case, inline for all Q queries at once: a new best (b1 below
+      // the running best, which falls outside the new window) whose window
+      // lies in subtile s1 alone (b2 outside it) and holds one member — the
+      // certified position.  Anything else takes subchunk_window; a sub-chunk
+      // whose best is outside the running window leaves it unchanged.
+      {
+        const uint32_t tiles_s = static_cast<uint32_t>(__cvta_generic_to_shared(tiles));
+        unsigned msk[Q];
+        float thrv[Q];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        const RunState r = subchunk_window(S, tiles, w.c_base + sc0, qx[k], qy[k], qz[k], b1[k], b2[k], b3[k], s12[k],
-                                           MG(k), RunState{B1(k), P1(k)});
-        B1(k) = r.b;
-        P1(k) = r.p;
+        for (int k = 0; k < Q; ++k) {
+          thrv[k] = __fadd_ru(b1[k], MG(k));
+          const uint32_t sp = tiles_s + static_cast<uint32_t>(s1v[k] * kSub) * 16u;
+          unsigned m = 0;
+#pragma unroll
+          for (int c = 0; c < kSub; c += 2) {
+            const float4 A = lds128(sp + c * 16u), B = lds128(sp + (c + 1) * 16u);
+            f32x2 d = ffma2(pk2(B.x, B.y), pk2(qz[k], qz[k]), pk2(B.z, B.w));
+            d = ffma2(pk2(A.z, A.w), pk2(qy[k], qy[k]), d);
+            d = ffma2(pk2(A.x, A.y), pk2(qx[k], qx[k]), d);
+            float d0, d1;
+            up2(d, d0, d1);
+            if (d0 <= thrv[k]) m |= 1u << c;
+            if (d1 <= thrv[k]) m |= 1u << (c + 1);
+          }
+          msk[k] = m;
+        }
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const float run_b = B1(k), mg = MG(k);
+          if (b1[k] > __fadd_ru(run_b, mg)) continue;  // cannot change the running window
+          if (b1[k] < run_b && !(run_b <= thrv[k]) && b2[k] > thrv[k] && __popc(msk[k]) == 1) {
+            B1(k) = b1[k];
+            P1(k) = w.c_base + sc0 + s1v[k] * kSub + __ffs(msk[k]) - 1;
+            continue;
+          }
+          const RunState r = subchunk_window(S, tiles, w.c_base + sc0, qx[k], qy[k], qz[k], b1[k], b2[k], b3[k],
+                                             s1v[k] | (s2v[k] << 16), mg, RunState{run_b, P1(k)});
+          B1(k) = r.b;
+          P1(k) = r.p;
+        }
       }
+      NNPH(4)
       __syncthreads();  // all rescans done before the next sub-chunk overwrites the tiles
+      NNPH(5)
     }
     // Emit.
 #pragma unroll
@@ -645,7 +710,10 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
         S.partials[(static_cast<int64_t>(w.slot) * w.nchunks + w.chunk) * kFwdQB + qi] = pr;
       }
     }
+    NNPH(6)
   }
+  NNPH(7)
+  NNPH_FLUSH
 }
 
 // Merge the per-split results of forward/final queries (nchunks > 1): the

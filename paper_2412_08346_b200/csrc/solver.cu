@@ -136,7 +136,7 @@ struct asicp_ctx {
   std::unique_ptr<asicp::Exchange> xchg;
   int J_glob = 0, j_lo = 0, rows_per_rank = 0, final_stride = 0;
   Buf theta_all, drift_all, xsend, xrecv, fsend, frecv, gpop_off_d, med_hist, med_state, kofs_d, kmat;
-  int med_big_grid = 0, max_gpop = 0;
+  int med_big_grid = 0, max_gpop = 0, med_mid = 0;
   double* host_gath = nullptr;
   size_t host_gath_bytes = 0;
   char* pin = nullptr;  // pinned upload staging (upload())
@@ -148,8 +148,11 @@ struct asicp_ctx {
   // Device buffers.
   Buf obj64, obj_cand, obj_cand4, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, scene32, sdf_coarse;
+  // Collision clusters (collide.cu) and the scratch of their Morton sort.
+  Buf scene_box, scene_code, scene_idx, scene_tmp, clusters, subclusters, scene_s32, scene_perm;
+  int n_clusters = 0;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
-      Bs, ctr, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
+      Bs, ctr, colc, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
       item_count, item_off, item_counter, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
       stats, iter_stats, trace_theta,
@@ -241,9 +244,10 @@ struct asicp_ctx {
     if (side) cudaStreamDestroy(side);
     Buf* all[] = {&obj64, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
-                  &scene32, &sdf_coarse, &theta,
+                  &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
+                  &scene_s32, &scene_perm, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
-                  &S64, &Sq32, &Sc32, &Bs, &ctr, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
+                  &S64, &Sq32, &Sc32, &Bs, &ctr, &colc, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
                   &item_counter,
                   &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &iter_stats, &trace_theta,
@@ -403,17 +407,26 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   upload(c, c->obj_cand4, cand4.data(), cand4.size(), st);
   upload(c, c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
-    std::vector<float4> s32(p.n_scene);
-    for (int64_t i = 0; i < p.n_scene; ++i) {
-      // w = |p|_1 of the rounded point (rounded up): the collision pre-test's
-      // transform-error margin.
-      const float x = static_cast<float>(p.scene_cloud[3 * i]), y = static_cast<float>(p.scene_cloud[3 * i + 1]),
-                  z = static_cast<float>(p.scene_cloud[3 * i + 2]);
-      const double l1 = (std::fabs(static_cast<double>(x)) + std::fabs(static_cast<double>(y))) +
-                        std::fabs(static_cast<double>(z));
-      s32[i] = make_float4(x, y, z, std::nextafter(static_cast<float>(l1), INFINITY));
-    }
-    upload(c, c->scene32, s32.data(), s32.size(), st);
+    // FP32 scene copy and the collision clusters, built on the device
+    // (collide.cu: Morton sort, cluster centres and radii).
+    const int n = c->n_scene;
+    c->n_clusters = (n + kClusterPts - 1) / kClusterPts;
+    const size_t npad = static_cast<size_t>(c->n_clusters) * kClusterPts;
+    c->scene32.ensure(static_cast<size_t>(n) * sizeof(float4));
+    c->scene_box.ensure(6 * sizeof(double));
+    c->scene_code.ensure(2 * static_cast<size_t>(n) * sizeof(unsigned int));
+    c->scene_idx.ensure(2 * static_cast<size_t>(n) * sizeof(int));
+    const size_t tb = scene_sort_temp_bytes(n);
+    c->scene_tmp.ensure(std::max<size_t>(tb, 16));
+    c->clusters.ensure(static_cast<size_t>(c->n_clusters) * sizeof(float4));
+    c->subclusters.ensure(static_cast<size_t>(c->n_clusters) * kSubPerCluster * sizeof(float4));
+    c->scene_s32.ensure(npad * sizeof(float4));
+    c->scene_perm.ensure(npad * sizeof(int));
+    launch_scene_prepare(c->scene64.as<double>(), n, c->scene32.as<float4>(), c->scene_box.as<double>(),
+                         c->scene_code.as<unsigned int>(), c->scene_code.as<unsigned int>() + n,
+                         c->scene_idx.as<int>(), c->scene_idx.as<int>() + n, c->scene_tmp.p, c->scene_tmp.bytes,
+                         c->clusters.as<float4>(), c->subclusters.as<float4>(), c->scene_s32.as<float4>(),
+                         c->scene_perm.as<int>(), st);
   }
 
   // Preshapes.
@@ -535,12 +548,15 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   if (svgd_split) c->kmat.ensure(static_cast<size_t>(ktot) * sizeof(double2));
   upload(c, c->kofs_d, kofs.data(), kofs.size(), st);
   upload(c, c->pop_logk1, logk1.data(), logk1.size(), st);
-  // Median select: populations below kMedBigK in one CTA (median.cu), larger
-  // ones grid-wide over 128 x 128 tiles of the pair triangle (kernels.cu).
+  // Median select: populations below kMedBigK in one CTA, up to kMedClusterK
+  // in one 8-CTA cluster (median.cu), larger ones grid-wide over 128 x 128
+  // tiles of the pair triangle (kernels.cu).
   long long big_tiles = 0;
+  c->med_mid = 0;
   for (int i = 0; i < n_pre; ++i) {
     const long long K = p.init_counts[i];
-    if (K >= kMedBigK) {
+    if (K >= kMedBigK && K <= kMedClusterK) c->med_mid = 1;
+    if (K > kMedClusterK) {
       const long long nb = (K + 127) / 128;
       big_tiles = std::max(big_tiles, nb * (nb + 1) / 2);
     }
@@ -588,6 +604,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->Sc32.ensure(static_cast<size_t>(so) * 16);
   c->Bs.ensure(Jz * 8);
   c->ctr.ensure(Jz * 3 * 8);
+  c->colc.ensure(Jz * sizeof(ColConst));
   const size_t jscene = Jz * static_cast<size_t>(c->n_scene);
   c->col_idx.ensure(jscene * 4);
   c->col_q.ensure(jscene * 16);
@@ -669,6 +686,12 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.obj_cand4 = c->obj_cand4.as<float4>();
   P.scene64 = c->scene64.as<double>();
   P.scene32 = c->scene32.as<float4>();
+  P.n_clusters = c->n_clusters;
+  P.med_mid = c->med_mid;
+  P.clusters = c->clusters.as<float4>();
+  P.subclusters = c->subclusters.as<float4>();
+  P.scene_s32 = c->scene_s32.as<float4>();
+  P.scene_perm = c->scene_perm.as<int>();
   P.surf64 = c->surf64.as<double>();
   P.pre_surf_off = c->pre_surf_off.as<int>();
   P.pre_tcp = c->pre_tcp.as<double>();
@@ -726,6 +749,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.Sc32 = c->Sc32.as<float4>();
   S.Bs = c->Bs.as<double>();
   S.ctr = c->ctr.as<double>();
+  S.colc = c->colc.as<ColConst>();
   S.col_idx = c->col_idx.as<int>();
   S.col_q = c->col_q.as<float4>();
   S.res_fwd = c->res_fwd.as<int>();

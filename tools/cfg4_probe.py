@@ -51,6 +51,15 @@ if a.mode == "unit":
         cudart.cudaProfilerStop()
     st = s.stats()
     print(f"unit {a.unit}: solve {st.solve_ms:.3f} ms, {st.kernel_launches} launches, status {int(sol.status)}")
+    raw = s.raw_stats()
+    nsub = 4 * ((problems[units[a.unit].obj].scene_cloud.shape[0] + 31) // 32)
+    print(f"collision sub-clusters left to the point test: {raw[14]} of {raw[13] + 1024} x {nsub} "
+          f"({raw[14] / max(1, (raw[13] + 1024) * nsub):.3%})")
+    ph = raw[240:248]
+    if sum(ph):
+        names = ["item start", "TMA wait", "hot loop", "top-3", "window epilogue", "sub-chunk barrier", "emit",
+                 "exit"]
+        print("NN filter phases (warp-cycles): " + ", ".join(f"{n} {v / sum(ph):.1%}" for n, v in zip(names, ph)))
     s.close()
     sys.exit(0)
 
