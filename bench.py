@@ -708,9 +708,9 @@ def main():
             return shard.combine(problems, parts)
 
         def solve_e2e():
-            for s, cp in zip(runner.solvers, subs):
-                s.prepare(cp)  # asicp_prepare: H2D of the unit's host buffers
-            runner.launch()
+            # asicp_prepare (H2D of the unit's host buffers) then asicp_run_async,
+            # unit by unit: the GPU solves unit i while the host prepares i + 1.
+            runner.prepare_launch(subs)
             return finish()
 
         worker_streams = streams

@@ -37,6 +37,16 @@ class BatchSolver:
         for s in self.solvers:
             s.run_async()
 
+    def prepare_launch(self, problems: Sequence[GraspProblem]) -> None:
+        """Re-prepare every entry from host buffers and launch it at once, so
+        entry i's solve runs on the GPU while the host prepares entry i + 1
+        (the end-to-end path: asicp_prepare + asicp_run_async per entry)."""
+        if len(problems) != len(self.solvers):
+            raise ValueError("one problem per entry")
+        for s, p in zip(self.solvers, problems):
+            s.prepare(p)
+            s.run_async()
+
     def wait(self) -> List[GraspSolution]:
         return [s.wait() for s in self.solvers]
 

@@ -248,6 +248,7 @@ __device__ __forceinline__ bool cluster_clear(const ColConst& K, const Grid& g, 
 }
 
 __global__ void __launch_bounds__(kColThreads, 8) collide_kernel(DevProblem P, DevState S, int all, int count_only) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (!all && !S.active[j]) return;
   extern __shared__ __align__(16) unsigned int col_smem[];
@@ -445,7 +446,7 @@ void collide_set_attrs() {
 }
 
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st) {
-  collide_kernel<<<P.J, kColThreads, collide_smem_bytes(P), st>>>(P, S, all, count_only);
+  pdl_launch(collide_kernel, dim3(P.J), dim3(kColThreads), collide_smem_bytes(P), st, P, S, all, count_only);
 }
 
 }  // namespace asicp

@@ -16,6 +16,7 @@ namespace asicp {
 // K0: per-particle RNG seeding, std::mt19937_64(seed + j) (grasp.cpp:149-151).
 // ---------------------------------------------------------------------------
 __global__ void seed_rng_kernel(uint64_t* state, int* mti, uint64_t seed, int J) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= J) return;
   mt::seed_state(state + static_cast<int64_t>(j) * mt::kN, seed + static_cast<uint64_t>(j));
@@ -81,6 +82,7 @@ __device__ void col_constants(const DevProblem& P, int pre, const double* th, Co
 // Candidate rows are padded to a multiple of 32 with +inf.
 // ---------------------------------------------------------------------------
 __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (!all && !S.active[j]) return;
   if (!all && threadIdx.x == 0) atomicAdd(S.stats + 13, 1ull);  // active (not SGD-frozen) particle evaluations
@@ -100,10 +102,10 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
     S.S64[3 * (o + i) + 0] = w.x;
     S.S64[3 * (o + i) + 1] = w.y;
     S.S64[3 * (o + i) + 2] = w.z;
-    const double ax = w.x - P.center[0], ay = w.y - P.center[1], az = w.z - P.center[2];
+    const double ax = w.x - P.obj_meta[0], ay = w.y - P.obj_meta[1], az = w.z - P.obj_meta[2];
     const double A = sqrt(ax * ax + ay * ay + az * az);
     S.Sq32[o + i] = make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az),
-                                nn_margin(A, P.B_obj));
+                                nn_margin(A, P.obj_meta[3]));
     const double bx = w.x - c.x, by = w.y - c.y, bz = w.z - c.z;
     const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
     const double gx = fx, gy = fy, gz = fz;
@@ -143,6 +145,7 @@ __device__ __forceinline__ uint64_t serial_next(uint64_t* st, int* mti) {
 
 template <bool kSmemIdx>
 __global__ void __launch_bounds__(128) minibatch_kernel(DevProblem P, DevState S, int m) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (!S.active[j] || S.n_col[j] > 0) return;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -237,6 +240,7 @@ constexpr int kCostSmem = 2 * 8 * kCostRow * 8;  // bytes (both halves)
 // 384 CTAs of 2 x 32 KB of terms fit one wave at 3 CTAs/SM, where one
 // particle per CTA took two.
 __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevState S, int final_pass) {
+  pdl_enter();
   const int half = threadIdx.x >= kCostHalf ? 1 : 0;
   const int tid = threadIdx.x - half * kCostHalf;
   const int j = 2 * blockIdx.x + half;
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
 // Trace (grasp.cpp:197-209): pre-update pose, loss, collision flag.
 // ---------------------------------------------------------------------------
 __global__ void trace_kernel(DevProblem P, DevState S, int k) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   const int64_t r = static_cast<int64_t>(k) * P.J + j;
@@ -356,6 +361,7 @@ __global__ void trace_kernel(DevProblem P, DevState S, int k) {
 // summed over i in order; update (optim.cpp:225-237).
 // ---------------------------------------------------------------------------
 __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_ref) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
@@ -383,6 +389,7 @@ __device__ __forceinline__ bool med_big(const DevProblem& P, int pop, int& b, in
 }
 
 __global__ void med_init_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int pop = blockIdx.x;
   int b, K;
   if (!med_big(P, pop, b, K)) return;
@@ -396,6 +403,7 @@ __global__ void med_init_kernel(DevProblem P, DevState S) {
 }
 
 __global__ void __launch_bounds__(256) med_hist_kernel(DevProblem P, DevState S, int shift, int bits) {
+  pdl_enter();
   const int pop = blockIdx.y;
   int b, K;
   if (!med_big(P, pop, b, K)) return;
@@ -447,6 +455,7 @@ __global__ void __launch_bounds__(256) med_hist_kernel(DevProblem P, DevState S,
 
 __global__ void __launch_bounds__(1024) med_select_kernel(DevProblem P, DevState S, int shift, int bits,
                                                           int last) {
+  pdl_enter();
   const int pop = blockIdx.x;
   int b, K;
   if (!med_big(P, pop, b, K)) return;
@@ -507,6 +516,7 @@ __global__ void __launch_bounds__(1024) med_select_kernel(DevProblem P, DevState
 // reference's per-component left-to-right sums.
 constexpr int kSvgdJ = 32;
 __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState S, double eta) {
+  pdl_enter();
   const int pop = blockIdx.y;
   const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;  // own (local) rows
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;   // partners (global)
@@ -580,6 +590,7 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_kernel(DevProblem P, DevState
 // accumulation — one warp per pose component, one lane per own particle, the
 // same left-to-right sums and update as svgd_kernel.
 __global__ void __launch_bounds__(256) svgd_kmat_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int pop = blockIdx.z;
   const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
@@ -637,6 +648,7 @@ constexpr int kAccTile = 64;
 constexpr int kAccStages = 4;
 constexpr int kAccSmem = kAccStages * (kAccTile * kSvgdJ * 16 + 2 * kAccTile * 7 * 8);
 __global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevState S, double eta) {
+  pdl_enter();
   const int pop = blockIdx.y;
   const int lb = P.pop_off[pop], Kl = P.pop_off[pop + 1] - lb;
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
@@ -775,6 +787,7 @@ __global__ void __launch_bounds__(kSvgdJ * 7) svgd_acc_kernel(DevProblem P, DevS
 // K7: SGD update (optim.cpp:108-114) for non-frozen particles.
 // ---------------------------------------------------------------------------
 __global__ void sgd_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   double* th = S.theta + 7 * j;
@@ -799,6 +812,7 @@ __global__ void sgd_kernel(DevProblem P, DevState S) {
 // Convergence bookkeeping (grasp.cpp:242-257) and the active mask of the
 // next iteration (converged particles freeze in the SGD phase, grasp.cpp:168).
 __global__ void bookkeeping_kernel(DevProblem P, DevState S, int stein_phase, int next_stein) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   if (stein_phase) {
@@ -864,6 +878,68 @@ __global__ void grid_bounds_kernel(Grid* grids, int gi, const float* values, flo
   }
 }
 
+// Object preparation (asicp_prepare): one CTA reduces the centroid and then
+// B_obj = max |r - centroid| (with the slack of the certification bound); the
+// origin need not be the reference's exact centroid — any origin with a B_obj
+// that bounds it keeps the NN filter certified.
+__global__ void __launch_bounds__(1024) object_meta_kernel(const double* obj64, int n, double* meta) {
+  __shared__ double red[3][32];
+  __shared__ double ctr[3];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  double s[3] = {0.0, 0.0, 0.0};
+  for (int i = tid; i < n; i += blockDim.x)
+    for (int a = 0; a < 3; ++a) s[a] += obj64[3 * i + a];
+  for (int o = 16; o > 0; o >>= 1)
+    for (int a = 0; a < 3; ++a) s[a] += __shfl_xor_sync(0xffffffffu, s[a], o);
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) red[a][w] = s[a];
+  __syncthreads();
+  if (tid < 3) {
+    double t = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) t += red[tid][k];
+    ctr[tid] = t / static_cast<double>(n);
+  }
+  __syncthreads();
+  double b = 0.0;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double bx = obj64[3 * i] - ctr[0], by = obj64[3 * i + 1] - ctr[1], bz = obj64[3 * i + 2] - ctr[2];
+    b = fmax(b, sqrt(bx * bx + by * by + bz * bz));
+  }
+  for (int o = 16; o > 0; o >>= 1) b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+  __syncthreads();
+  if (lane == 0) red[0][w] = b;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int k = 0; k < static_cast<int>(blockDim.x >> 5); ++k) m = fmax(m, red[0][k]);
+    meta[0] = ctr[0];
+    meta[1] = ctr[1];
+    meta[2] = ctr[2];
+    meta[3] = m * (1.0 + 1e-6) + 1e-12;
+  }
+}
+
+__global__ void object_pack_kernel(const double* obj64, int n, int n_pad, const double* meta, float4* cand,
+                                   float4* cand4) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  float4 v = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+  if (i < n) {
+    const double bx = obj64[3 * i] - meta[0], by = obj64[3 * i + 1] - meta[1], bz = obj64[3 * i + 2] - meta[2];
+    const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
+    const double dx = fx, dy = fy, dz = fz;
+    v = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(dx * dx + dy * dy + dz * dz));
+  }
+  pc_put(cand, i, v);
+  cand4[i] = v;
+}
+
+void launch_object_prepare(const double* obj64, int n, int n_pad, double* meta, float4* cand, float4* cand4,
+                           cudaStream_t st) {
+  object_meta_kernel<<<1, 1024, 0, st>>>(obj64, n, meta);
+  object_pack_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(obj64, n, n_pad, meta, cand, cand4);
+}
+
 void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st) {
   for (int g = 0; g < n_grids; ++g) grid_bounds_kernel<<<296, 256, 0, st>>>(grids, g, values, coarse);
 }
@@ -875,6 +951,7 @@ void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* co
 // unsharded solve does.
 // ---------------------------------------------------------------------------
 __global__ void pack_stein_kernel(DevProblem P, DevState S, double* send) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   for (int a = 0; a < 7; ++a) {
@@ -885,6 +962,7 @@ __global__ void pack_stein_kernel(DevProblem P, DevState S, double* send) {
 
 __global__ void unpack_stein_kernel(const double* gathered, double* theta_all, double* drift_all, int J_glob,
                                     int world, int rows_per_rank) {
+  pdl_enter();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= world * rows_per_rank) return;
   const int r = row / rows_per_rank, i = row % rows_per_rank;
@@ -899,6 +977,7 @@ __global__ void unpack_stein_kernel(const double* gathered, double* theta_all, d
 }
 
 __global__ void pack_final_kernel(DevProblem P, DevState S, double* send, int stride, int k_max, int with_trace) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   double* o = send + static_cast<int64_t>(stride) * j;
@@ -917,11 +996,13 @@ __global__ void pack_final_kernel(DevProblem P, DevState S, double* send, int st
 }
 
 __global__ void copy_theta_kernel(double* dst, const double* src, int n) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) dst[i] = src[i];
 }
 
 __global__ void init_state_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
   S.loss[j] = __longlong_as_double(0x7ff8000000000000ll);  // quiet NaN (grasp.cpp:124-125)
@@ -986,13 +1067,13 @@ void launch_dbg_exp(const double* x, double* y, int64_t n, cudaStream_t st) {
 double host_glibc_exp(double x) { return glibc_exp(x); }
 
 void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream_t st) {
-  seed_rng_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(S.rng_state, S.rng_mti, seed, P.J);
+  pdl_launch(seed_rng_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, S.rng_state, S.rng_mti, seed, P.J);
 }
 void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st) {
-  init_state_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S);
+  pdl_launch(init_state_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S);
 }
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st) {
-  pose_prep_kernel<<<P.J, kNnThreads, 0, st>>>(P, S, all);
+  pdl_launch(pose_prep_kernel, dim3(P.J), dim3(kNnThreads), 0, st, P, S, all);
 }
 int minibatch_smem_cap() { return 160 * 1024; }
 
@@ -1008,35 +1089,35 @@ void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) 
   if (launch_minibatch_par(P, S, m, st)) return;
   const size_t need = static_cast<size_t>(P.n_obj) * sizeof(int);
   if (need <= static_cast<size_t>(minibatch_smem_cap())) {
-    minibatch_kernel<true><<<P.J, 128, need, st>>>(P, S, m);
+    pdl_launch(minibatch_kernel<true>, dim3(P.J), dim3(128), need, st, P, S, m);
   } else {
-    minibatch_kernel<false><<<P.J, 128, 0, st>>>(P, S, m);
+    pdl_launch(minibatch_kernel<false>, dim3(P.J), dim3(128), 0, st, P, S, m);
   }
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
-  cost_kernel<<<(P.J + 1) / 2, kCostThreads, kCostSmem, st>>>(P, S, final_pass);
+  pdl_launch(cost_kernel, dim3((P.J + 1) / 2), dim3(kCostThreads), kCostSmem, st, P, S, final_pass);
 }
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st) {
-  trace_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, k);
+  pdl_launch(trace_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S, k);
 }
 void launch_drift(const DevProblem& P, DevState& S, double gamma, double n_ref, cudaStream_t st) {
-  drift_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, gamma, n_ref);
+  pdl_launch(drift_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S, gamma, n_ref);
 }
 void launch_pack_stein(const DevProblem& P, const DevState& S, double* send, cudaStream_t st) {
-  pack_stein_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send);
+  pdl_launch(pack_stein_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S, send);
 }
 void launch_unpack_stein(const double* gathered, double* theta_all, double* drift_all, int J_glob, int world,
                          int rows_per_rank, cudaStream_t st) {
   const int rows = world * rows_per_rank;
-  unpack_stein_kernel<<<(rows + 127) / 128, 128, 0, st>>>(gathered, theta_all, drift_all, J_glob, world,
+  pdl_launch(unpack_stein_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, gathered, theta_all, drift_all, J_glob, world,
                                                           rows_per_rank);
 }
 void launch_pack_final(const DevProblem& P, const DevState& S, double* send, int stride, int k_max, int with_trace,
                        cudaStream_t st) {
-  pack_final_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, send, stride, k_max, with_trace);
+  pdl_launch(pack_final_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S, send, stride, k_max, with_trace);
 }
 void launch_svgd_kmat(const DevProblem& P, DevState& S, int max_pop, int max_gpop, cudaStream_t st) {
-  svgd_kmat_kernel<<<dim3((max_pop + kSvgdJ - 1) / kSvgdJ, (max_gpop + kSvgdJ - 1) / kSvgdJ, P.n_pop), 256, 0, st>>>(
+  pdl_launch(svgd_kmat_kernel, dim3(dim3((max_pop + kSvgdJ - 1) / kSvgdJ, (max_gpop + kSvgdJ - 1) / kSvgdJ, P.n_pop)), dim3(256), 0, st, 
       P, S);
 }
 
@@ -1048,11 +1129,11 @@ int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_po
     ++n;
   }
   if (big_grid > 0) {
-    med_init_kernel<<<P.n_pop, 256, 0, st>>>(P, S);
+    pdl_launch(med_init_kernel, dim3(P.n_pop), dim3(256), 0, st, P, S);
     const int shifts[6] = {52, 40, 28, 16, 4, 0}, bits[6] = {12, 12, 12, 12, 12, 4};
     for (int pass = 0; pass < 6; ++pass) {
-      med_hist_kernel<<<dim3(big_grid, P.n_pop), 256, 0, st>>>(P, S, shifts[pass], bits[pass]);
-      med_select_kernel<<<P.n_pop, 1024, 0, st>>>(P, S, shifts[pass], bits[pass], pass == 5 ? 1 : 0);
+      pdl_launch(med_hist_kernel, dim3(dim3(big_grid, P.n_pop)), dim3(256), 0, st, P, S, shifts[pass], bits[pass]);
+      pdl_launch(med_select_kernel, dim3(P.n_pop), dim3(1024), 0, st, P, S, shifts[pass], bits[pass], pass == 5 ? 1 : 0);
     }
     n += 13;
   }
@@ -1064,18 +1145,18 @@ int launch_stein_update(const DevProblem& P, DevState& S, double eta, int max_po
       launch_svgd_kmat(P, S, max_pop, max_gpop, st);
       ++n;
     }
-    svgd_acc_kernel<<<grid, kSvgdJ * 7, kAccSmem, st>>>(P, S, eta);
+    pdl_launch(svgd_acc_kernel, dim3(grid), dim3(kSvgdJ * 7), kAccSmem, st, P, S, eta);
   } else {
-    svgd_kernel<<<grid, kSvgdJ * 7, 0, st>>>(P, S, eta);
+    pdl_launch(svgd_kernel, dim3(grid), dim3(kSvgdJ * 7), 0, st, P, S, eta);
   }
-  copy_theta_kernel<<<(7 * P.J + 255) / 256, 256, 0, st>>>(S.theta, S.theta_next, 7 * P.J);
+  pdl_launch(copy_theta_kernel, dim3((7 * P.J + 255) / 256), dim3(256), 0, st, S.theta, S.theta_next, 7 * P.J);
   return n;
 }
 void launch_sgd(const DevProblem& P, DevState& S, cudaStream_t st) {
-  sgd_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S);
+  pdl_launch(sgd_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S);
 }
 void launch_bookkeeping(const DevProblem& P, DevState& S, int stein_phase, int next_stein, cudaStream_t st) {
-  bookkeeping_kernel<<<(P.J + 127) / 128, 128, 0, st>>>(P, S, stein_phase, next_stein);
+  pdl_launch(bookkeeping_kernel, dim3((P.J + 127) / 128), dim3(128), 0, st, P, S, stein_phase, next_stein);
 }
 
 }  // namespace asicp

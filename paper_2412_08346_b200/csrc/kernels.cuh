@@ -53,8 +53,9 @@ struct DevProblem {
   int j_lo;
   int med_mid;              // some population takes the cluster median (kMedBigK <= K <= kMedClusterK)
   const long long* kofs;    // population -> offset of its K x K_local block in DevState::kmat (split SVGD)
-  double center[3];         // FP32 re-centring origin of the forward match (object centroid)
-  double B_obj;             // max |r - center| over R (with slack)
+  // Forward-match re-centring (built on the device, launch_object_prepare):
+  // [0..2] origin (the object centroid), [3] B_obj >= max |r - origin|.
+  const double* obj_meta;
   double com[3];
   double contact_tolerance;
   double prior_t_mean[3];
@@ -173,6 +174,11 @@ inline void set_all_kernel_attrs() {
   minibatch_set_attrs();
 }
 void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* coarse, cudaStream_t st);
+// Object cloud -> centroid, B_obj and the FP32 NN candidates (-2b, |b|^2),
+// b = r - centroid: pair-interleaved (cand, n_pad rows, +inf padded) and plain
+// (cand4).  meta = [centroid x, y, z, B_obj].
+void launch_object_prepare(const double* obj64, int n, int n_pad, double* meta, float4* cand, float4* cand4,
+                           cudaStream_t st);
 // sdf_build.cu: graspmatch::build_sdf on the device (returns ASICP_OK or
 // ASICP_INVALID_ARGUMENT with the reference message in *err; throws on CUDA
 // errors).  values == null: geometry only (dims, meta = origin[3], voxel, 0).

@@ -56,6 +56,7 @@ __device__ void block_bitonic_sort(unsigned long long* s, int n) {
 }
 
 __global__ void __launch_bounds__(kMedThreads) median_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int pop = blockIdx.x;
   if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // no local particle reads h
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
@@ -198,6 +199,7 @@ constexpr int kMedClSmem = kMedClusterK * 3 * 8 + kMedBins * 4 + kMedGather * 8;
 
 __global__ void __cluster_dims__(kMedCl, 1, 1) __launch_bounds__(kMedThreads)
     median_cluster_kernel(DevProblem P, DevState S) {
+  pdl_enter();
   const int pop = blockIdx.y;
   if (P.pop_off[pop + 1] == P.pop_off[pop]) return;  // uniform over the cluster
   const int b = P.gpop_off[pop], K = P.gpop_off[pop + 1] - b;
@@ -357,7 +359,7 @@ void median_set_attrs() {
 }
 
 void launch_median_small(const DevProblem& P, DevState& S, cudaStream_t st) {
-  median_kernel<<<P.n_pop, kMedThreads, kMedSmem, st>>>(P, S);
+  pdl_launch(median_kernel, dim3(P.n_pop), dim3(kMedThreads), kMedSmem, st, P, S);
   if (P.med_mid) median_cluster_kernel<<<dim3(kMedCl, P.n_pop), kMedThreads, kMedClSmem, st>>>(P, S);
 }
 

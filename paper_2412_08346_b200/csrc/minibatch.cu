@@ -30,6 +30,7 @@ constexpr int kMbThreads = 1024;
 
 template <int ITEMS>
 __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P, DevState S, int m) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (!S.active[j] || S.n_col[j] > 0) return;
   using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
@@ -222,6 +223,7 @@ __host__ __device__ __forceinline__ int64_t mb_arena_ints(int n, int m) {
 constexpr int kMbArenaMax = 200 * 1024;  // bytes of dynamic shared memory
 
 __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m, int in_smem) {
+  pdl_enter();
   const int j = blockIdx.x;
   if (!S.active[j] || S.n_col[j] > 0) return;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -370,7 +372,7 @@ constexpr int par_smem() {
 
 template <int ITEMS>
 static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
-  minibatch_par_kernel<ITEMS><<<P.J, kMbThreads, par_smem<ITEMS>(), st>>>(P, S, m);
+  pdl_launch(minibatch_par_kernel<ITEMS>, dim3(P.J), dim3(kMbThreads), par_smem<ITEMS>(), st, P, S, m);
   return true;
 }
 
@@ -391,7 +393,7 @@ bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t 
     const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
     const int in_smem = arena <= kMbArenaMax ? 1 : 0;
     const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
-    minibatch_cnt_kernel<<<P.J, kMbThreads, smem, st>>>(P, S, m, in_smem);
+    pdl_launch(minibatch_cnt_kernel, dim3(P.J), dim3(kMbThreads), smem, st, P, S, m, in_smem);
     return true;
   }
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);

@@ -76,6 +76,7 @@ __device__ __forceinline__ void plan_counts(const DevProblem& P, const DevState&
 // the round's counters.
 constexpr int kFillThreads = 128;
 __global__ void __launch_bounds__(kFillThreads) nn_fill_kernel(DevProblem P, DevState S, NnPlan plan) {
+  pdl_enter();
   __shared__ int sf[kFillThreads], sr[kFillThreads];
   const int tid = threadIdx.x;
   const int per = ceil_div(P.J, kFillThreads);
@@ -507,6 +508,7 @@ template <int Q>
 __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
     nn_filter_kernel(const __grid_constant__ DevProblem P, const __grid_constant__ DevState S,
                      const __grid_constant__ NnPlan plan, int list) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float4* tiles = reinterpret_cast<float4*>(smem_raw);
   __shared__ __align__(8) uint64_t full_bar[kNnStages];
@@ -720,6 +722,7 @@ __global__ void __launch_bounds__(kNnThreads, ASICP_NN_MINBLOCKS)
 // global best is certified when exactly one split reaches the window and that
 // split was itself unambiguous.
 __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
+  pdl_enter();
   const int j = blockIdx.y;
   const int nch = S.nn_dyn[0];
   if (nch <= 1) return;  // single split: the filter emitted directly
@@ -774,6 +777,7 @@ __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
 // warp per query, lexicographic (distance, position) minimum — exactly the
 // reference's kd-tree rule.
 __global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -824,6 +828,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevState S, NnPlan plan) {
+  pdl_enter();
   extern __shared__ __align__(16) float4 rev_smem[];
   const int lane = threadIdx.x & 31;
   float4* stage = rev_smem + (threadIdx.x >> 5) * kRevMaxC;
@@ -972,7 +977,7 @@ __global__ void __launch_bounds__(kPlanThreads) nn_plan_kernel(DevProblem P, Dev
 }
 
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
-  nn_fill_kernel<<<(P.J + kFillThreads - 1) / kFillThreads, kFillThreads, 0, st>>>(P, S, plan);
+  pdl_launch(nn_fill_kernel, dim3((P.J + kFillThreads - 1) / kFillThreads), dim3(kFillThreads), 0, st, P, S, plan);
 }
 
 int nn_smem_bytes() { return kNnSmem; }
@@ -992,19 +997,19 @@ int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, in
               cudaEvent_t ev_begin, cudaEvent_t ev_end) {
   int n = 0;
   if (ev_begin) cudaEventRecord(ev_begin, st);
-  nn_filter_kernel<kFwdQ><<<grid, kNnThreads, kNnSmem, st>>>(P, S, plan, 0);
+  pdl_launch(nn_filter_kernel<kFwdQ>, dim3(grid), dim3(kNnThreads), kNnSmem, st, P, S, plan, 0);
   ++n;
   if (ev_end) cudaEventRecord(ev_end, st);
   if (plan.kind == 0) {
-    nn_rev_kernel<<<3 * refine_grid / 2, kRevThreads, kRevSmem, st>>>(P, S, plan);  // 3 CTAs per SM
+    pdl_launch(nn_rev_kernel, dim3(3 * refine_grid / 2), dim3(kRevThreads), kRevSmem, st, P, S, plan);  // 3 CTAs per SM
     ++n;
   }
   if (plan.nchunks > 1) {
     dim3 mg((plan.max_ns + 127) / 128, P.J);
-    nn_merge_kernel<<<mg, 128, 0, st>>>(P, S, plan);
+    pdl_launch(nn_merge_kernel, dim3(mg), dim3(128), 0, st, P, S, plan);
     ++n;
   }
-  nn_refine_kernel<<<refine_grid, 256, 0, st>>>(P, S, plan);
+  pdl_launch(nn_refine_kernel, dim3(refine_grid), dim3(256), 0, st, P, S, plan);
   return n + 1;
 }
 

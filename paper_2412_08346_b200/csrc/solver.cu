@@ -146,7 +146,7 @@ struct asicp_ctx {
   DevState S{};
 
   // Device buffers.
-  Buf obj64, obj_cand, obj_cand4, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
+  Buf obj64, obj_meta, obj_cand, obj_cand4, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, scene32, sdf_coarse;
   // Collision clusters (collide.cu) and the scratch of their Morton sort.
   Buf scene_box, scene_code, scene_idx, scene_tmp, clusters, subclusters, scene_s32, scene_perm;
@@ -242,7 +242,7 @@ struct asicp_ctx {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
-    Buf* all[] = {&obj64, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
+    Buf* all[] = {&obj64, &obj_meta, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
                   &scene_s32, &scene_perm, &theta,
@@ -266,11 +266,18 @@ namespace {
 // bench boxes (tools/prepare_timing.py).  Staged copies stay in flight until
 // the stream synchronizes at the end of asicp_prepare; a full buffer
 // synchronizes and restarts.
+// Copy `bytes` from host `src` to device `dst` through the pinned staging.
+void stage_copy(asicp_ctx* c, void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 template <typename T>
 void upload(asicp_ctx* c, Buf& b, const T* src, size_t n, cudaStream_t st) {
-  const size_t bytes = n * sizeof(T);
   b.ensure(std::max<size_t>(n, 1) * sizeof(T));
   if (!n) return;
+  stage_copy(c, b.p, src, n * sizeof(T), st);
+}
+
+void stage_copy(asicp_ctx* c, void* dst_dev, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
   const size_t need = (bytes + 255) / 256 * 256;
   if (c->pin_off + need > c->pin_cap) {
     CUDA_OK(cudaStreamSynchronize(st));
@@ -286,7 +293,7 @@ void upload(asicp_ctx* c, Buf& b, const T* src, size_t n, cudaStream_t st) {
   }
   char* dst = c->pin + c->pin_off;
   std::memcpy(dst, src, bytes);
-  CUDA_OK(cudaMemcpyAsync(b.p, dst, bytes, cudaMemcpyHostToDevice, st));
+  CUDA_OK(cudaMemcpyAsync(dst_dev, dst, bytes, cudaMemcpyHostToDevice, st));
   c->pin_off += need;
 }
 
@@ -370,41 +377,15 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->n_ref = static_cast<double>(p.n_object);
   c->eta_stein = p.step_scale / c->n_ref;  // grasp.cpp:154
 
-  // Object cloud: FP64 + re-centred FP32 candidates.
-  std::vector<double> obj(p.object_cloud, p.object_cloud + 3 * p.n_object);
-  double center[3] = {0.0, 0.0, 0.0};
-  for (int64_t i = 0; i < p.n_object; ++i)
-    for (int a = 0; a < 3; ++a) center[a] += obj[3 * i + a];
-  for (int a = 0; a < 3; ++a) center[a] /= static_cast<double>(p.n_object);
-  // Candidate rows are padded to the NN subtile with +inf (never selected) and
-  // stored pair-interleaved (common.cuh pc_index).
+  // Object cloud: FP64 rows; the re-centred FP32 candidates (pair-interleaved
+  // and plain, rows padded to the NN subtile with +inf) are built on the device.
   c->n_obj_pad = static_cast<int>((p.n_object + kSubRows - 1) / kSubRows * kSubRows);
-  std::vector<float4> cand(c->n_obj_pad, make_float4(0.0f, 0.0f, 0.0f, 0.0f));
-  float* cf = reinterpret_cast<float*>(cand.data());
-  auto put = [&](int64_t i, float x, float y, float z, float w) {
-    float* f = cf + pc_index(i);
-    f[0] = x;
-    f[2] = y;
-    f[4] = z;
-    f[6] = w;
-  };
-  double bmax = 0.0;
-  for (int64_t i = 0; i < p.n_object; ++i) {
-    const double bx = obj[3 * i] - center[0], by = obj[3 * i + 1] - center[1], bz = obj[3 * i + 2] - center[2];
-    const float fx = static_cast<float>(bx), fy = static_cast<float>(by), fz = static_cast<float>(bz);
-    const double dx = fx, dy = fy, dz = fz;
-    put(i, -2.0f * fx, -2.0f * fy, -2.0f * fz, static_cast<float>(dx * dx + dy * dy + dz * dz));
-    bmax = std::max(bmax, std::sqrt(bx * bx + by * by + bz * bz));
-  }
-  for (int64_t i = p.n_object; i < c->n_obj_pad; ++i) put(i, 0.0f, 0.0f, 0.0f, INFINITY);
-  std::vector<float4> cand4(c->n_obj_pad);
-  for (int64_t i = 0; i < c->n_obj_pad; ++i) {
-    const float* f = cf + pc_index(i);
-    cand4[i] = make_float4(f[0], f[2], f[4], f[6]);
-  }
-  upload(c, c->obj64, obj.data(), obj.size(), st);
-  upload(c, c->obj_cand, cand.data(), cand.size(), st);
-  upload(c, c->obj_cand4, cand4.data(), cand4.size(), st);
+  upload(c, c->obj64, p.object_cloud, 3 * p.n_object, st);
+  c->obj_meta.ensure(4 * sizeof(double));
+  c->obj_cand.ensure(static_cast<size_t>(c->n_obj_pad) * sizeof(float4));
+  c->obj_cand4.ensure(static_cast<size_t>(c->n_obj_pad) * sizeof(float4));
+  launch_object_prepare(c->obj64.as<double>(), c->n_obj, c->n_obj_pad, c->obj_meta.as<double>(),
+                        c->obj_cand.as<float4>(), c->obj_cand4.as<float4>(), st);
   upload(c, c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
     // FP32 scene copy and the collision clusters, built on the device
@@ -451,7 +432,11 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
 
   // SDF grids.
   std::vector<Grid> grids(p.n_sdf_grids);
-  std::vector<float> values;
+  int64_t values_total = 0;
+  for (int64_t g = 0; g < p.n_sdf_grids; ++g)
+    values_total += static_cast<int64_t>(p.sdf_grids[g].dims[0]) * p.sdf_grids[g].dims[1] * p.sdf_grids[g].dims[2];
+  c->sdf_values.ensure(static_cast<size_t>(std::max<int64_t>(values_total, 1)) * sizeof(float));
+  int64_t values_off = 0;
   int64_t coarse_total = 0;
   for (int64_t g = 0; g < p.n_sdf_grids; ++g) {
     const asicp_sdf_grid& s = p.sdf_grids[g];
@@ -463,9 +448,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     }
     d.voxel = s.voxel;
     d.boundary_max_abs = s.boundary_max_abs;
-    d.values_offset = static_cast<int64_t>(values.size());
+    d.values_offset = values_off;
     const size_t total = static_cast<size_t>(s.dims[0]) * s.dims[1] * s.dims[2];
-    values.insert(values.end(), s.values, s.values + total);
+    stage_copy(c, c->sdf_values.as<float>() + values_off, s.values, total * sizeof(float), st);  // grid by grid
+    values_off += static_cast<int64_t>(total);
     // Bounds of the collision kernel's FP32 pre-test (lip, vmax and the
     // dilated 4^3-block maxima) are computed on the device below.
     d.lip = 0.0;
@@ -476,7 +462,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   }
   mark("host-build");
   upload(c, c->grids, grids.data(), grids.size(), st);
-  upload(c, c->sdf_values, values.data(), values.size(), st);
   mark("sdf-upload");
   c->sdf_coarse.ensure(static_cast<size_t>(std::max<int64_t>(coarse_total, 1)) * sizeof(float));
   launch_grid_bounds(c->grids.as<Grid>(), static_cast<int>(p.n_sdf_grids), c->sdf_values.as<float>(),
@@ -619,14 +604,18 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     c->fy_scratch.ensure(Jz * static_cast<size_t>(c->n_obj) * 4);
   // Parallel Fisher-Yates scratch (5 int arrays per particle) when it takes at
   // most a quarter of the free HBM; the serial kernel covers the rest.
-  size_t free_b = 0, total_b = 0;
   mark("particles");
-  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
-  mark("memgetinfo");
   const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
   // (The parallel kernel takes draws of m <= 20480 per call; larger m and an
-  // absent scratch fall back to the serial kernel.)
-  const bool fy_par_on = fy_par_bytes <= c->fy_par.bytes || fy_par_bytes <= free_b / 4;
+  // absent scratch fall back to the serial kernel.)  cudaMemGetInfo costs
+  // 1-11 ms of host time on the bench boxes: ask only when the scratch grows.
+  bool fy_par_on = fy_par_bytes <= c->fy_par.bytes;
+  if (!fy_par_on) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+    fy_par_on = fy_par_bytes <= free_b / 4;
+  }
+  mark("memgetinfo");
   if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
   // Work items: forward < base_items + target_items (T x splits, see
   // fwd_split); reverse <= sum ceil(n_col / 32) <= J * ceil(n_scene / 32).
@@ -708,13 +697,12 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.gpop_off = c->gpop_off_d.as<int>();
   P.j_lo = lo;
   P.kofs = c->kofs_d.as<long long>();
+  P.obj_meta = c->obj_meta.as<double>();
   for (int a = 0; a < 3; ++a) {
-    P.center[a] = center[a];
     P.com[a] = p.com[a];
     P.prior_t_mean[a] = p.prior_t_mean[a];
     P.prior_t_sigma[a] = p.prior_t_sigma[a];
   }
-  P.B_obj = bmax * (1.0 + 1e-6) + 1e-12;
   P.contact_tolerance = p.contact_tolerance;
   for (int a = 0; a < 4; ++a) {
     P.prior_q_location[a] = p.prior_q_location[a];
