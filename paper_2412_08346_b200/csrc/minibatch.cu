@@ -182,7 +182,8 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P,
 // no bound on m.
 constexpr int kCountMax = 49152;
 
-__device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, int j, int m, int n, int* jv,
+template <typename IT>
+__device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, int j, int m, int n, IT* jv,
                                             uint64_t* st, uint64_t* st0, int* s_mti, int* s_mti0, int* s_reject) {
   const int tid = threadIdx.x;
   uint64_t* gst = S.rng_state + static_cast<int64_t>(j) * mt::kN;
@@ -203,7 +204,7 @@ __device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, in
     for (int t = tid; t < cnt; t += kMbThreads) {
       uint64_t u;
       if (!mt::lemire(mt::temper(st[mti + t]), static_cast<uint64_t>(n - (i0 + t)), &u)) *s_reject = 1;
-      jv[i0 + t] = i0 + t + static_cast<int>(u);
+      jv[i0 + t] = static_cast<IT>(i0 + t + static_cast<int>(u));
     }
     __syncthreads();
     if (tid == 0) *s_mti = mti + cnt;
@@ -212,16 +213,40 @@ __device__ __forceinline__ void draws_block(const DevProblem& P, DevState& S, in
   }
 }
 
-// Shared-memory arena of the counting-sort kernel (ints): the key counters /
-// group ends (cnt, max(n, m)), the draws (jv, m), the sorted steps (sval, m),
-// the W pointers and the pointer-jump buffer (ptr, jb, m each).  Sorted keys
-// are jv[sval[t]].  When the arena does not fit, everything but cnt lives in
-// the particle's global scratch.
+// Shared-memory arena of the counting-sort kernel: the key counters / group
+// ends (cnt, max(n, m)), the draws (jv, m), the sorted steps (sval, m), the W
+// pointers and the pointer-jump buffer (ptr, jb, m each).  Sorted keys are
+// jv[sval[t]].  Entries are 16-bit when n and m fit (cfg2 / cfg4: a 100 KB
+// arena, two 1024-thread CTAs per SM), else 32-bit; when even that does not
+// fit, everything but cnt lives in the particle's global scratch.
 __host__ __device__ __forceinline__ int64_t mb_arena_ints(int n, int m) {
   return static_cast<int64_t>(n > m ? n : m) + 4ll * m;
 }
 constexpr int kMbArenaMax = 200 * 1024;  // bytes of dynamic shared memory
+constexpr int kMbArena16Max = 100 * 1024;  // 16-bit arenas up to this size: 2 CTAs per SM
+constexpr int kMbNone16 = 0xffff;          // "no group end" in a 16-bit arena
 
+// Counters of the counting sort: 32-bit words, or two 16-bit halves per word
+// (atomics on the containing word; counts and offsets stay below 2^16).
+template <typename IT>
+struct MbCnt {
+  unsigned int* w;
+  __device__ unsigned int add(int k, unsigned int v) const { return atomicAdd(w + k, v); }
+  __device__ unsigned int get(int k) const { return w[k]; }
+  __device__ void set(int k, unsigned int v) const { w[k] = v; }
+};
+template <>
+struct MbCnt<uint16_t> {
+  unsigned int* w;
+  __device__ unsigned int add(int k, unsigned int v) const {
+    const int sh = 16 * (k & 1);
+    return (atomicAdd(w + (k >> 1), v << sh) >> sh) & 0xffffu;
+  }
+  __device__ unsigned int get(int k) const { return reinterpret_cast<const uint16_t*>(w)[k]; }
+  __device__ void set(int k, unsigned int v) const { reinterpret_cast<uint16_t*>(w)[k] = static_cast<uint16_t>(v); }
+};
+
+template <typename IT>
 __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m, int in_smem) {
   pdl_enter();
   const int j = blockIdx.x;
@@ -231,17 +256,24 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
   __shared__ uint64_t st0[mt::kN];
   __shared__ int s_mti, s_mti0, s_reject;
   __shared__ unsigned int part[kMbThreads];
+  constexpr bool k16 = sizeof(IT) == 2;
   const int tid = threadIdx.x;
   const int n = P.n_obj;
-  unsigned int* cnt = reinterpret_cast<unsigned int*>(dyn);  // counters -> offsets -> group ends (lk)
-  int* lk = reinterpret_cast<int*>(dyn);
+  const int ncnt = n > m ? n : m;
+  const MbCnt<IT> cnt{reinterpret_cast<unsigned int*>(dyn)};  // counters -> offsets -> group ends (lk)
   int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
-  int* base = in_smem ? reinterpret_cast<int*>(dyn) + (n > m ? n : m) : scratch;
-  int* jv = base;
-  int* sval = jv + (in_smem ? m : P.n_obj_pad);
-  int* ptr = sval + (in_smem ? m : P.n_obj_pad);
-  int* jb = ptr + (in_smem ? m : P.n_obj_pad);
+  // 16-bit counters are packed two per word: round the count area to words.
+  IT* base = in_smem ? reinterpret_cast<IT*>(dyn) + (k16 ? (ncnt + 1) / 2 * 2 : ncnt)
+                     : reinterpret_cast<IT*>(scratch);  // (IT = int whenever !in_smem)
+  IT* jv = base;
+  IT* sval = jv + (in_smem ? m : P.n_obj_pad);
+  IT* ptr = sval + (in_smem ? m : P.n_obj_pad);
+  IT* jb = ptr + (in_smem ? m : P.n_obj_pad);
   int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
+  auto lk_get = [&](int k) -> int {
+    const unsigned int v = cnt.get(k);
+    return k16 ? (v == kMbNone16 ? -1 : static_cast<int>(v)) : static_cast<int>(v);
+  };
   draws_block(P, S, j, m, n, jv, st, st0, &s_mti, &s_mti0, &s_reject);
   if (s_reject) {
     // Exact serial replay from the saved engine state (never seen in practice).
@@ -269,14 +301,14 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
     __syncthreads();
   } else {
     // 2. Counting sort of (j_s, s) by key, stable.
-    for (int k = tid; k < n; k += kMbThreads) cnt[k] = 0;
+    for (int k = tid; k < (k16 ? (n + 1) / 2 : n); k += kMbThreads) cnt.w[k] = 0u;
     __syncthreads();
-    for (int s = tid; s < m; s += kMbThreads) atomicAdd(&cnt[jv[s]], 1u);
+    for (int s = tid; s < m; s += kMbThreads) cnt.add(jv[s], 1u);
     __syncthreads();
     const int per = (n + kMbThreads - 1) / kMbThreads;
     const int k0 = tid * per, k1 = min(n, k0 + per);
     unsigned int sum = 0;
-    for (int k = k0; k < k1; ++k) sum += cnt[k];
+    for (int k = k0; k < k1; ++k) sum += cnt.get(k);
     part[tid] = sum;
     __syncthreads();
     for (int off = 1; off < kMbThreads; off <<= 1) {  // inclusive scan of the segment sums
@@ -286,13 +318,16 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
       __syncthreads();
     }
     unsigned int run = tid ? part[tid - 1] : 0u;
+    // (Per-thread ranges are even-aligned for 16-bit counters only when per is
+    // even; a half-word store next to another thread's half is still a
+    // distinct 16-bit location, so plain stores are safe.)
     for (int k = k0; k < k1; ++k) {
-      const unsigned int c = cnt[k];
-      cnt[k] = run;
+      const unsigned int c = cnt.get(k);
+      cnt.set(k, run);
       run += c;
     }
     __syncthreads();
-    for (int s = tid; s < m; s += kMbThreads) sval[atomicAdd(&cnt[jv[s]], 1u)] = s;
+    for (int s = tid; s < m; s += kMbThreads) sval[cnt.add(jv[s], 1u)] = static_cast<IT>(s);
     __syncthreads();
     // Order each key group by step (groups hold a handful of steps).
     for (int t = tid; t < m; t += kMbThreads) {
@@ -301,7 +336,7 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
       int e = t + 1;
       while (e < m && jv[sval[e]] == k) ++e;
       for (int a = t + 1; a < e; ++a) {
-        const int v = sval[a];
+        const IT v = sval[a];
         int b = a - 1;
         while (b >= t && sval[b] > v) {
           sval[b + 1] = sval[b];
@@ -313,16 +348,16 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
     __syncthreads();
     // 3. Last member of each key group (keys < m only matter for wl()); the
     // counters are dead now, so their space holds lk.
-    for (int s = tid; s < m; s += kMbThreads) lk[s] = -1;
+    for (int s = tid; s < m; s += kMbThreads) cnt.set(s, k16 ? kMbNone16 : 0xffffffffu);
     __syncthreads();
     for (int t = tid; t < m; t += kMbThreads) {
       const int k = jv[sval[t]];
-      if (k < m && (t == m - 1 || jv[sval[t + 1]] != k)) lk[k] = t;
+      if (k < m && (t == m - 1 || jv[sval[t + 1]] != k)) cnt.set(k, static_cast<unsigned int>(t));
     }
     __syncthreads();
     // 4. wl(s) -> initial pointers.
     for (int s = tid; s < m; s += kMbThreads) {
-      const int t = lk[s];
+      const int t = lk_get(s);
       int wl = -1;
       if (t >= 0) {
         if (sval[t] < s)
@@ -330,22 +365,22 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
         else if (t > 0 && jv[sval[t - 1]] == s)
           wl = sval[t - 1];
       }
-      ptr[s] = wl < 0 ? s : wl;
+      ptr[s] = static_cast<IT>(wl < 0 ? s : wl);
     }
     __syncthreads();
     // 5. Pointer jumping to the chain roots (W).
-    int* a = ptr;
-    int* b = jb;
+    IT* a = ptr;
+    IT* b = jb;
     for (;;) {
       int changed = 0;
       for (int s = tid; s < m; s += kMbThreads) {
-        const int p = a[s];
-        const int q = a[p];
+        const IT p = a[s];
+        const IT q = a[p];
         b[s] = q;
         changed |= q != p;
       }
       const int any = __syncthreads_or(changed);
-      int* t = a;
+      IT* t = a;
       a = b;
       b = t;
       if (!any) break;
@@ -354,7 +389,7 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
     for (int t = tid; t < m; t += kMbThreads) {
       const int i = sval[t];
       const int k = jv[i];
-      pool[i] = (t > 0 && jv[sval[t - 1]] == k) ? a[sval[t - 1]] : k;
+      pool[i] = (t > 0 && jv[sval[t - 1]] == k) ? static_cast<int>(a[sval[t - 1]]) : k;
     }
     __syncthreads();
   }
@@ -382,7 +417,8 @@ void minibatch_set_attrs() {
   cudaFuncSetAttribute(minibatch_par_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<4>());
   cudaFuncSetAttribute(minibatch_par_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<12>());
   cudaFuncSetAttribute(minibatch_par_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, par_smem<20>());
-  cudaFuncSetAttribute(minibatch_cnt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMbArenaMax);
+  cudaFuncSetAttribute(minibatch_cnt_kernel<int>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMbArenaMax);
+  cudaFuncSetAttribute(minibatch_cnt_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMbArena16Max);
 }
 
 // Returns false when the parallel path does not apply (no scratch, or m too
@@ -390,10 +426,17 @@ void minibatch_set_attrs() {
 bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
   if (S.fy_par == nullptr) return false;
   if (P.n_obj <= kCountMax) {
+    const int ncnt = P.n_obj > m ? P.n_obj : m;
+    const int64_t arena16 = (static_cast<int64_t>((ncnt + 1) / 2 * 2) + 4ll * m) * 2;
+    if (P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max) {
+      pdl_launch(minibatch_cnt_kernel<uint16_t>, dim3(P.J), dim3(kMbThreads), static_cast<size_t>(arena16), st, P, S,
+                 m, 1);
+      return true;
+    }
     const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
     const int in_smem = arena <= kMbArenaMax ? 1 : 0;
     const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
-    pdl_launch(minibatch_cnt_kernel, dim3(P.J), dim3(kMbThreads), smem, st, P, S, m, in_smem);
+    pdl_launch(minibatch_cnt_kernel<int>, dim3(P.J), dim3(kMbThreads), smem, st, P, S, m, in_smem);
     return true;
   }
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
