@@ -198,11 +198,11 @@ def cpu_reference(fixture, threads: int):
     """Reference optimize_grasp (oracle/_ref) on the host cores, full workload."""
     from oracle import ref
 
-    fixture.set(workers=threads)
+    fixture.struct.workers = threads  # fixtures and CProblem (cfg4 units) both hold an asicp_problem
     t0 = time.perf_counter()
     sol = ref.optimize_grasp(fixture)
     dt = time.perf_counter() - t0
-    fixture.set(workers=0)
+    fixture.struct.workers = 0
     return dt, sol
 
 

@@ -36,3 +36,28 @@ def test_default_is_one_rank():
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][0])
     assert line["n_gpus"] == 1 and line["ranks"] == [0]
+
+
+def test_reference_arm_runs_cfg4_without_the_product_library():
+    """The driver's reference arm (`bench.py --impl reference`, default cfg4):
+    one (object, preshape) unit through the unmodified reference
+    optimize_grasp on the host cores, inputs from the oracle-side fixture
+    library; the process must not map the product libasicp.so."""
+    import pytest
+
+    sys.path.insert(0, str(ROOT))
+    from oracle import ref
+
+    if not ref.available():
+        pytest.skip("oracle/_ref not built (make -C oracle)")
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0']\n"
+            "try:\n    runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n    pass\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('MAPS_PRODUCT', 'libasicp.so' in maps, 'libasicp_fixtures.so' in maps)\n")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][0])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["config"]["workload"].startswith("cfg4")
+    assert line["cpu_baseline"]["kind"] == "reference" and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert "MAPS_PRODUCT False False" in r.stdout

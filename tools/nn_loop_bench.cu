@@ -21,13 +21,13 @@ __device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
   return d;
 }
 
-constexpr int kSub = 32, kCand = 2048, Q = 8;
+constexpr int kSub = 32, kCand = 2048;
 
 // MODE 0: hot loop only, 1: + top-3 per subtile, 2: + top-3 with the queries
 // held as pre-packed register pairs (no .F32 broadcast operand), 3: scalar
 // FFMA form + top-3.  Queries come from global memory (no constant folding).
-template <int MODE>
-__global__ void __launch_bounds__(128, 4) loop_kernel(const float4* cand, const float4* qin, float* out, int reps) {
+template <int MODE, int Q = 8, int MINB = 4>
+__global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, const float4* qin, float* out, int reps) {
   __shared__ float4 tile[kCand];
   for (int i = threadIdx.x; i < kCand; i += blockDim.x) tile[i] = cand[i];
   __syncthreads();
@@ -98,7 +98,20 @@ __global__ void __launch_bounds__(128, 4) loop_kernel(const float4* cand, const 
           float l0, h0, l1, h1;
           up2(d0[k], l0, h0);
           up2(d1[k], l1, h1);
-          tm[k] = fminf(fminf(tm[k], fminf(l0, h0)), fminf(l1, h1));
+          if (MODE == 4) {  // 2-input min.f32, kept unfused
+            float m0, m1, m2, m3;
+            asm volatile("min.f32 %0, %1, %2;" : "=f"(m0) : "f"(l0), "f"(h0));
+            asm volatile("min.f32 %0, %1, %2;" : "=f"(m1) : "f"(l1), "f"(h1));
+            asm volatile("min.f32 %0, %1, %2;" : "=f"(m2) : "f"(m0), "f"(m1));
+            asm volatile("min.f32 %0, %1, %2;" : "=f"(m3) : "f"(tm[k]), "f"(m2));
+            tm[k] = m3;
+          } else if (MODE == 5) {  // integer min of the bit patterns (timing only)
+            const int a0 = min(__float_as_int(l0), __float_as_int(h0));
+            const int a1 = min(__float_as_int(l1), __float_as_int(h1));
+            tm[k] = __int_as_float(min(__float_as_int(tm[k]), min(a0, a1)));
+          } else {
+            tm[k] = fminf(fminf(tm[k], fminf(l0, h0)), fminf(l1, h1));
+          }
         }
       }
       }
@@ -134,7 +147,7 @@ int main() {
   float* out;
   cudaMalloc(&cand, kCand * sizeof(float4));
   {
-    const int nq = sms * 4 * 128 * Q;
+    const int nq = sms * 8 * 128 * 16;
     float4* hq = new float4[nq];
     for (int i = 0; i < nq; ++i) hq[i] = make_float4(1e-4f * (i % 977), -2e-4f * (i % 511), 3e-4f * (i % 263), 0.f);
     cudaMalloc(&qin, nq * sizeof(float4));
@@ -149,9 +162,35 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int reps = 40;
-  const char* names[4] = {"hot loop only", "hot loop + top-3", "packed queries + top-3", "scalar FFMA + top-3"};
-  for (int mode = 0; mode < 4; ++mode)
-    for (int per_sm = 1; per_sm <= 4; ++per_sm) {
+  // Queries per thread (register blocking) for the hot loop alone.
+  {
+    auto run = [&](auto kern, int q, int per_sm) {
+      const int blocks = sms * per_sm;
+      float best = 1e30f;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        kern<<<blocks, 128>>>(cand, qin, out, reps);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, a, b);
+        best = ms < best ? ms : best;
+      }
+      const double pairs = static_cast<double>(blocks) * 128 * q * kCand * reps;
+      const double per_clk_sm = pairs / (best * 1e-3) / (static_cast<double>(sms) * clk * 1e3);
+      printf("hot loop + top-3, Q=%d, %d CTAs/SM: %.2f pairs/clk/SM  FMA pipe %.2f\n", q, per_sm, per_clk_sm,
+             per_clk_sm * 3 / 128);
+    };
+    run(loop_kernel<1, 4, 8>, 4, 8);
+    run(loop_kernel<1, 4, 6>, 4, 6);
+    run(loop_kernel<1, 12, 2>, 12, 2);
+    run(loop_kernel<1, 12, 3>, 12, 3);
+    run(loop_kernel<1, 16, 2>, 16, 2);
+  }
+  const char* names[6] = {"hot loop only", "hot loop + top-3", "packed queries + top-3", "scalar FFMA + top-3",
+                          "2-input min.f32 + top-3", "integer min + top-3"};
+  for (int mode = 0; mode < 6; ++mode)
+    for (int per_sm = 4; per_sm <= 4; ++per_sm) {
       const int blocks = sms * per_sm;
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
@@ -160,13 +199,15 @@ int main() {
         if (mode == 1) loop_kernel<1><<<blocks, 128>>>(cand, qin, out, reps);
         if (mode == 2) loop_kernel<2><<<blocks, 128>>>(cand, qin, out, reps);
         if (mode == 3) loop_kernel<3><<<blocks, 128>>>(cand, qin, out, reps);
+        if (mode == 4) loop_kernel<4><<<blocks, 128>>>(cand, qin, out, reps);
+        if (mode == 5) loop_kernel<5><<<blocks, 128>>>(cand, qin, out, reps);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
         best = ms < best ? ms : best;
       }
-      const double pairs = static_cast<double>(blocks) * 128 * Q * kCand * reps;
+      const double pairs = static_cast<double>(blocks) * 128 * 8 * kCand * reps;
       const double per_clk_sm = pairs / (best * 1e-3) / (static_cast<double>(sms) * clk * 1e3);
       printf("mode %d (%s) %d CTAs/SM: %.3f ms  %.2f pairs/clk/SM  FMA pipe %.2f  (8-FLOP: %.1f TFLOP/s at %d MHz)\n",
              mode, names[mode], per_sm, best, per_clk_sm, per_clk_sm * 3 / 128,
