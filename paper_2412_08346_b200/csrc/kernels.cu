@@ -109,11 +109,14 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
     const double bx = w.x - c.x, by = w.y - c.y, bz = w.z - c.z;
     const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
     const double gx = fx, gy = fy, gz = fz;
-    S.Sc32[o + i] = make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(gx * gx + gy * gy + gz * gz));
+    // Pair-interleaved (pc_index), like the forward candidates: the reverse
+    // filter evaluates two of them per packed FFMA2.
+    pc_put(S.Sc32 + o, i,
+           make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(gx * gx + gy * gy + gz * gz)));
     bmax = fmax(bmax, sqrt(bx * bx + by * by + bz * bz));
   }
   for (int i = ns + threadIdx.x; i < round_up(ns, kSub); i += blockDim.x)
-    S.Sc32[o + i] = make_float4(0.0f, 0.0f, 0.0f, INFINITY);
+    pc_put(S.Sc32 + o, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
   s_bmax[threadIdx.x] = bmax;
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -113,7 +113,7 @@ struct DevState {
   double* h;           // per population bandwidth
   double* S64;         // transformed contact surface, padded rows x 3
   float4* Sq32;        // its FP32 forward queries (x, y, z, margin), object-centred
-  float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred
+  float4* Sc32;        // its FP32 reverse candidates (-2b, |b|^2), particle-centred, pair-interleaved (pc_index)
   double* ctr;         // J x 3 per-particle reverse-match centre (TCP in world)
   double* Bs;          // per particle max |s - ctr|
   ColConst* colc;      // per particle collision-test constants

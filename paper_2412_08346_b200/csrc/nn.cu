@@ -861,18 +861,37 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
     const int nsub = ceil_div(w.nc, kSub);  // candidate rows are +inf padded to the subtile
     float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
     int s1 = 0, s2 = 0;
+    const f32x2 qx2 = pk2(q.x, q.x), qy2 = pk2(q.y, q.y), qz2 = pk2(q.z, q.z);
+    const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     for (int sub = 0; sub < nsub; ++sub) {
-      const float4* sp = cand + sub * kSub;
-      float t0 = INFINITY, t1 = INFINITY, t2 = INFINITY, t3 = INFINITY;
+      float tm;
+      if (staged) {
+        // Candidates are pair-interleaved (pc_index): per 4 candidates four
+        // broadcast LDS.128, six packed FFMA2 (each lane is d32()), two mins.
+        const uint32_t sp = stage_s + static_cast<uint32_t>(sub * kSub) * 16u;
+        float t0 = INFINITY, t1 = INFINITY;
 #pragma unroll
-      for (int c = 0; c < kSub; c += 4) {
-        const float4 v0 = sp[c], v1 = sp[c + 1], v2 = sp[c + 2], v3 = sp[c + 3];
-        t0 = fminf(t0, __fmaf_rn(q.x, v0.x, __fmaf_rn(q.y, v0.y, __fmaf_rn(q.z, v0.z, v0.w))));
-        t1 = fminf(t1, __fmaf_rn(q.x, v1.x, __fmaf_rn(q.y, v1.y, __fmaf_rn(q.z, v1.z, v1.w))));
-        t2 = fminf(t2, __fmaf_rn(q.x, v2.x, __fmaf_rn(q.y, v2.y, __fmaf_rn(q.z, v2.z, v2.w))));
-        t3 = fminf(t3, __fmaf_rn(q.x, v3.x, __fmaf_rn(q.y, v3.y, __fmaf_rn(q.z, v3.z, v3.w))));
+        for (int c = 0; c < kSub; c += 4) {
+          const float4 A0 = lds128(sp + c * 16u), B0 = lds128(sp + (c + 1) * 16u);
+          const float4 A1 = lds128(sp + (c + 2) * 16u), B1 = lds128(sp + (c + 3) * 16u);
+          f32x2 d0 = ffma2(pk2(B0.x, B0.y), qz2, pk2(B0.z, B0.w));
+          f32x2 d1 = ffma2(pk2(B1.x, B1.y), qz2, pk2(B1.z, B1.w));
+          d0 = ffma2(pk2(A0.z, A0.w), qy2, d0);
+          d1 = ffma2(pk2(A1.z, A1.w), qy2, d1);
+          d0 = ffma2(pk2(A0.x, A0.y), qx2, d0);
+          d1 = ffma2(pk2(A1.x, A1.y), qx2, d1);
+          float l0, h0, l1, h1;
+          up2(d0, l0, h0);
+          up2(d1, l1, h1);
+          t0 = fminf(t0, fminf(l0, h0));
+          t1 = fminf(t1, fminf(l1, h1));
+        }
+        tm = fminf(t0, t1);
+      } else {
+        float t0 = INFINITY;
+        for (int c = 0; c < kSub; ++c) t0 = fminf(t0, d32(q.x, q.y, q.z, pc_get(cand, sub * kSub + c)));
+        tm = t0;
       }
-      const float tm = fminf(fminf(t0, t1), fminf(t2, t3));
       // Running top-3 of subtile minima (strict < keeps the earliest).
       const bool lt1 = tm < b1, lt2 = tm < b2;
       b3 = lt2 ? b2 : fminf(b3, tm);
@@ -895,15 +914,15 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
     const int nscan = b2 <= thr ? 2 : 1;
     for (int r = 0; r < nscan; ++r) {
       const int sid = r == 0 ? s1 : s2;
-      const float4* sp = cand + sid * kSub;
       // Member bitmask in one pass, then the members in increasing position.
       unsigned mask = 0;
 #pragma unroll 8
-      for (int c = 0; c < kSub; ++c) mask |= (d32(q.x, q.y, q.z, sp[c]) <= thr ? 1u : 0u) << c;
+      for (int c = 0; c < kSub; ++c)
+        mask |= (d32(q.x, q.y, q.z, pc_get(cand, sid * kSub + c)) <= thr ? 1u : 0u) << c;
       while (mask) {
         const int c = __ffs(mask) - 1;
         mask &= mask - 1;
-        const float d = d32(q.x, q.y, q.z, sp[c]);
+        const float d = d32(q.x, q.y, q.z, pc_get(cand, sid * kSub + c));
         const int p = sid * kSub + c;
         if (np < kWinCap) pos[np] = p;
         ++np;
