@@ -1088,14 +1088,15 @@ void kernels_set_attrs() {
   cudaFuncSetAttribute(svgd_acc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAccSmem);
 }
 
-void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
-  if (launch_minibatch_par(P, S, m, st)) return;
+int launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  if (const int n = launch_minibatch_par(P, S, m, st)) return n;
   const size_t need = static_cast<size_t>(P.n_obj) * sizeof(int);
   if (need <= static_cast<size_t>(minibatch_smem_cap())) {
     pdl_launch(minibatch_kernel<true>, dim3(P.J), dim3(128), need, st, P, S, m);
   } else {
     pdl_launch(minibatch_kernel<false>, dim3(P.J), dim3(128), 0, st, P, S, m);
   }
+  return 1;
 }
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st) {
   pdl_launch(cost_kernel, dim3((P.J + 1) / 2), dim3(kCostThreads), kCostSmem, st, P, S, final_pass);

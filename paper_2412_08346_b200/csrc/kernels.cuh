@@ -126,8 +126,9 @@ struct DevState {
   int* pool_idx;       // J x n_obj_pad minibatch object indices (sample order)
   float4* pool32;      // J x n_obj_pad gathered FP32 candidates (+inf padded)
   int* fy_scratch;     // J x n_obj Fisher-Yates scratch (large clouds only)
-  int* fy_par;         // J x fy_stride scratch of the parallel Fisher-Yates (or null)
+  int* fy_par;         // fy_batch x fy_stride scratch of the parallel Fisher-Yates (or null)
   int64_t fy_stride;   // 5 x n_obj_pad
+  int fy_batch;        // particles the scratch covers (the minibatch launches in batches of these)
   const int* pool_map; // = pool_idx when this iteration's forward match is pooled
   NnItem* items[2];    // work lists: [0] forward / final, [1] reverse
   int* item_count[2];  // J + 1 each
@@ -198,8 +199,9 @@ size_t scene_sort_temp_bytes(int n);
 void launch_scene_prepare(const double* scene64, int n, float4* s32, double* box, unsigned int* code_in,
                           unsigned int* code_out, int* idx_in, int* perm, void* temp, size_t temp_bytes,
                           float4* clusters, float4* subclusters, float4* s32s, int* perm_pad, cudaStream_t st);
-void launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
-bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st);  // minibatch.cu
+// Both return the number of launches (0: the parallel path does not apply).
+int launch_minibatch(const DevProblem& P, DevState& S, int m, cudaStream_t st);
+int launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st);  // minibatch.cu
 int minibatch_smem_cap();
 void launch_cost(const DevProblem& P, DevState& S, int final_pass, cudaStream_t st);
 void launch_trace(const DevProblem& P, DevState& S, int k, cudaStream_t st);

@@ -29,9 +29,9 @@ namespace asicp {
 constexpr int kMbThreads = 1024;
 
 template <int ITEMS>
-__global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P, DevState S, int m) {
+__global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P, DevState S, int m, int j0) {
   pdl_enter();
-  const int j = blockIdx.x;
+  const int j = j0 + blockIdx.x;  // scratch slot blockIdx.x (the scratch covers S.fy_batch particles)
   if (!S.active[j] || S.n_col[j] > 0) return;
   using Sort = cub::BlockRadixSort<int, kMbThreads, ITEMS, int>;
   extern __shared__ __align__(16) unsigned char dyn[];
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_par_kernel(DevProblem P,
   __shared__ int s_mti, s_mti0, s_reject;
   const int tid = threadIdx.x;
   const int n = P.n_obj;
-  int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
+  int* scratch = S.fy_par + static_cast<int64_t>(blockIdx.x) * S.fy_stride;
   int* jv = scratch;                 // draw targets j_i, later pointer-jump buffer
   int* skey = scratch + P.n_obj_pad; // sorted keys
   int* sval = skey + P.n_obj_pad;    // sorted step indices
@@ -246,10 +246,14 @@ struct MbCnt<uint16_t> {
   __device__ void set(int k, unsigned int v) const { reinterpret_cast<uint16_t*>(w)[k] = static_cast<uint16_t>(v); }
 };
 
+// in_smem: 1 arena in shared memory; 0 counters in shared memory, the rest in
+// the particle's scratch; 2 everything in the scratch (clouds too large for
+// shared counters: the counters follow the four m-arrays).
 template <typename IT>
-__global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m, int in_smem) {
+__global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P, DevState S, int m, int in_smem,
+                                                                   int j0) {
   pdl_enter();
-  const int j = blockIdx.x;
+  const int j = j0 + blockIdx.x;  // scratch slot blockIdx.x (the scratch covers S.fy_batch particles)
   if (!S.active[j] || S.n_col[j] > 0) return;
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ uint64_t st[mt::kN];
@@ -260,15 +264,18 @@ __global__ void __launch_bounds__(kMbThreads) minibatch_cnt_kernel(DevProblem P,
   const int tid = threadIdx.x;
   const int n = P.n_obj;
   const int ncnt = n > m ? n : m;
-  const MbCnt<IT> cnt{reinterpret_cast<unsigned int*>(dyn)};  // counters -> offsets -> group ends (lk)
-  int* scratch = S.fy_par + static_cast<int64_t>(j) * S.fy_stride;
+  int* scratch = S.fy_par + static_cast<int64_t>(blockIdx.x) * S.fy_stride;
+  // counters -> offsets -> group ends (lk)
+  const MbCnt<IT> cnt{in_smem == 2 ? reinterpret_cast<unsigned int*>(scratch + 4ll * P.n_obj_pad)
+                                   : reinterpret_cast<unsigned int*>(dyn)};
   // 16-bit counters are packed two per word: round the count area to words.
-  IT* base = in_smem ? reinterpret_cast<IT*>(dyn) + (k16 ? (ncnt + 1) / 2 * 2 : ncnt)
-                     : reinterpret_cast<IT*>(scratch);  // (IT = int whenever !in_smem)
+  const bool arena = in_smem == 1;
+  IT* base = arena ? reinterpret_cast<IT*>(dyn) + (k16 ? (ncnt + 1) / 2 * 2 : ncnt)
+                   : reinterpret_cast<IT*>(scratch);  // (IT = int whenever the arena is not in shared memory)
   IT* jv = base;
-  IT* sval = jv + (in_smem ? m : P.n_obj_pad);
-  IT* ptr = sval + (in_smem ? m : P.n_obj_pad);
-  IT* jb = ptr + (in_smem ? m : P.n_obj_pad);
+  IT* sval = jv + (arena ? m : P.n_obj_pad);
+  IT* ptr = sval + (arena ? m : P.n_obj_pad);
+  IT* jb = ptr + (arena ? m : P.n_obj_pad);
   int* pool = S.pool_idx + static_cast<int64_t>(j) * P.n_obj_pad;
   auto lk_get = [&](int k) -> int {
     const unsigned int v = cnt.get(k);
@@ -406,9 +413,12 @@ constexpr int par_smem() {
 }
 
 template <int ITEMS>
-static bool launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
-  pdl_launch(minibatch_par_kernel<ITEMS>, dim3(P.J), dim3(kMbThreads), par_smem<ITEMS>(), st, P, S, m);
-  return true;
+static int launch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  int n = 0;
+  for (int j0 = 0; j0 < P.J; j0 += S.fy_batch, ++n)
+    pdl_launch(minibatch_par_kernel<ITEMS>, dim3(min(S.fy_batch, P.J - j0)), dim3(kMbThreads), par_smem<ITEMS>(), st,
+               P, S, m, j0);
+  return n;
 }
 
 // Opt-in shared-memory sizes on the current device (per context: function
@@ -421,28 +431,33 @@ void minibatch_set_attrs() {
   cudaFuncSetAttribute(minibatch_cnt_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMbArena16Max);
 }
 
-// Returns false when the parallel path does not apply (no scratch, or m too
-// large for one CTA's sort); the caller then uses the serial kernel.
-bool launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
-  if (S.fy_par == nullptr) return false;
+// Returns the number of launches, or 0 when the parallel path does not apply
+// (no scratch at all); the caller then uses the serial kernel.  The scratch
+// covers S.fy_batch particles: larger populations take several launches.
+int launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t st) {
+  if (S.fy_par == nullptr) return 0;
+  auto cnt_launches = [&](auto kern, size_t smem, int in_smem) {
+    int n = 0;
+    for (int j0 = 0; j0 < P.J; j0 += S.fy_batch, ++n)
+      pdl_launch(kern, dim3(min(S.fy_batch, P.J - j0)), dim3(kMbThreads), smem, st, P, S, m, in_smem, j0);
+    return n;
+  };
   if (P.n_obj <= kCountMax) {
     const int ncnt = P.n_obj > m ? P.n_obj : m;
     const int64_t arena16 = (static_cast<int64_t>((ncnt + 1) / 2 * 2) + 4ll * m) * 2;
-    if (P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max) {
-      pdl_launch(minibatch_cnt_kernel<uint16_t>, dim3(P.J), dim3(kMbThreads), static_cast<size_t>(arena16), st, P, S,
-                 m, 1);
-      return true;
-    }
+    if (P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max)
+      return cnt_launches(minibatch_cnt_kernel<uint16_t>, static_cast<size_t>(arena16), 1);
     const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
     const int in_smem = arena <= kMbArenaMax ? 1 : 0;
     const size_t smem = in_smem ? static_cast<size_t>(arena) : static_cast<size_t>(P.n_obj) * 4;
-    pdl_launch(minibatch_cnt_kernel<int>, dim3(P.J), dim3(kMbThreads), smem, st, P, S, m, in_smem);
-    return true;
+    return cnt_launches(minibatch_cnt_kernel<int>, smem, in_smem);
   }
   if (m <= kMbThreads * 4) return launch_par<4>(P, S, m, st);
   if (m <= kMbThreads * 12) return launch_par<12>(P, S, m, st);
   if (m <= kMbThreads * 20) return launch_par<20>(P, S, m, st);
-  return false;
+  // Large clouds and draws: the counting sort with every array (counters
+  // included) in the particle's global scratch.
+  return cnt_launches(minibatch_cnt_kernel<int>, 0, 2);
 }
 
 }  // namespace asicp

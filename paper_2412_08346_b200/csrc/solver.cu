@@ -605,18 +605,24 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   // Parallel Fisher-Yates scratch (5 int arrays per particle) when it takes at
   // most a quarter of the free HBM; the serial kernel covers the rest.
   mark("particles");
-  const size_t fy_par_bytes = Jz * 5 * static_cast<size_t>(c->n_obj_pad) * 4;
-  // (The parallel kernel takes draws of m <= 20480 per call; larger m and an
-  // absent scratch fall back to the serial kernel.)  cudaMemGetInfo costs
-  // 1-11 ms of host time on the bench boxes: ask only when the scratch grows.
-  bool fy_par_on = fy_par_bytes <= c->fy_par.bytes;
-  if (!fy_par_on) {
+  // Parallel Fisher-Yates scratch: 5 int arrays per particle, for the whole
+  // population when that takes at most a quarter of the free HBM, else for a
+  // batch of particles the minibatch launches cover in turn (large clouds,
+  // SURVEY cfg5 at 50k-200k points).  cudaMemGetInfo costs 1-11 ms of host
+  // time on the bench boxes: ask only when the scratch grows.
+  const size_t fy_per = 5 * static_cast<size_t>(c->n_obj_pad) * 4;
+  int fy_batch = J;
+  if (Jz * fy_per > c->fy_par.bytes) {
     size_t free_b = 0, total_b = 0;
     CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
-    fy_par_on = fy_par_bytes <= free_b / 4;
+    const size_t budget = c->fy_par.bytes + free_b / 4;
+    fy_batch = static_cast<int>(std::min<size_t>(Jz, budget / fy_per));
   }
+  const bool fy_par_on = fy_batch >= 1;
+  if (fy_par_on) c->fy_par.ensure(static_cast<size_t>(fy_batch) * fy_per);
+  if (fy_par_on && static_cast<size_t>(fy_batch) * fy_per < c->fy_par.bytes)  // an earlier, larger scratch
+    fy_batch = static_cast<int>(std::min<size_t>(Jz, c->fy_par.bytes / fy_per));
   mark("memgetinfo");
-  if (fy_par_on) c->fy_par.ensure(fy_par_bytes);
   // Work items: forward < base_items + target_items (T x splits, see
   // fwd_split); reverse <= sum ceil(n_col / 32) <= J * ceil(n_scene / 32).
   c->items0.ensure((fwd_slots + Jz) * sizeof(NnItem));
@@ -749,6 +755,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.fy_scratch = c->fy_scratch.as<int>();
   S.fy_par = fy_par_on ? c->fy_par.as<int>() : nullptr;
   S.fy_stride = 5 * static_cast<int64_t>(c->n_obj_pad);
+  S.fy_batch = fy_par_on ? fy_batch : 0;
   S.pool_map = nullptr;
   S.items[0] = c->items0.as<NnItem>();
   S.items[1] = c->items1.as<NnItem>();
@@ -844,9 +851,10 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
 void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
   cudaStream_t st = c->stream;
   launch_nn_plan(c->P, c->S, plan, st);
+  int mb_launches = 0;
   if (minibatch_m > 0) {
     StageTimer t(c, asicp_ctx::kStMinibatch, capture);
-    launch_minibatch(c->P, c->S, minibatch_m, st);
+    mb_launches = launch_minibatch(c->P, c->S, minibatch_m, st);
   }
   asicp_ctx::ProfEvent e{asicp_ctx::kStNn, nullptr, nullptr};
   if (c->profile && !capture) {
@@ -855,7 +863,7 @@ void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture)
     c->prof_events.push_back(e);
   }
   const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.a, e.b);
-  c->launches += 1 + n + (minibatch_m > 0);  // fill (plan fused) + filter(s), merge, refine + minibatch
+  c->launches += 1 + n + mb_launches;  // fill (plan fused) + filter(s), merge, refine + minibatch
 }
 
 // The whole optimize_grasp as a kernel sequence on c->stream.
@@ -1441,6 +1449,7 @@ int asicp_dbg_minibatch(uint64_t seed, int64_t n, const int64_t* ms, int64_t cal
     if (par) fyp.ensure(5 * static_cast<size_t>(P.n_obj_pad) * 4);
     S.fy_par = par ? fyp.as<int>() : nullptr;
     S.fy_stride = 5 * static_cast<int64_t>(P.n_obj_pad);
+    S.fy_batch = P.J;
     P.obj_cand = cand.as<float4>();
     P.obj_cand4 = cand.as<float4>();  // all-zero candidates: either layout
     S.active = active.as<int>();

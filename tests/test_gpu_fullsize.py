@@ -91,3 +91,16 @@ def test_cfg5_full_population(solver):
     t_gpu = time.perf_counter() - t0
     print(f"cfg5 16384 particles: reference {t_ref:.1f} s (host cores), B200 {t_gpu:.3f} s end to end")
     assert_bit_identical(got, want)
+
+
+def test_cfg5_large_cloud_parallel_minibatch(solver):
+    """cfg5's 50k-point cloud: minibatches of up to
+    50,000 draws from a 50,000-point cloud take the all-global counting sort
+    (no serial fallback); 512 particles of the population, full trajectory
+    bit-identical to the reference."""
+    ref = _ref()
+    fx = fixtures.config(5, seed=0, particles_per_preshape=512, n_object=50000).set(record_trace=1)
+    assert fx.struct.n_object > 49152 and fx.J == 512  # the cylinder sampler rounds the count
+    want = ref.optimize_grasp(fx)
+    got = solver.optimize(fx)
+    assert_bit_identical(got, want, trace=True)

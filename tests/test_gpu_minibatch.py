@@ -2,9 +2,11 @@
 rng.hpp:16-44 / spatial_index.cpp:111-123) against the reference draws.
 
 Covers every path: the counting-sort kernel (clouds of <= 49152 points, any
-m), the radix-sort kernel at its three sizes (m <= 4096, 12288, 20480) for
-larger clouds, and the serial swap kernel (larger m, or parallel disabled),
-over consecutive calls on one engine stream.
+m; 16-bit shared arena, 32-bit shared arena, shared counters + global
+arrays), the radix-sort kernel at its three sizes (m <= 4096, 12288, 20480)
+for larger clouds, the all-global counting sort beyond that (cfg5's 200k-point
+clouds), and the serial swap kernel (parallel disabled), over consecutive
+calls on one engine stream.
 """
 import ctypes as C
 
@@ -17,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 CASES = [(208, 10000, [1, 150, 300, 450, 2400, 4500, 5250, 10000]), (5, 1500, [844, 1500, 1500]),
          (7, 30000, [3000, 12000, 16000, 20000, 24000]), (9, 50000, [30000]), (3, 64, [64, 64]),
-         (11, 60000, [3000, 9000, 15000, 22000])]
+         (11, 60000, [3000, 9000, 15000, 22000]), (13, 200000, [20000, 60000, 150000])]
 
 
 def draws(seed, n, ms, parallel):
