@@ -94,18 +94,23 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
   const int64_t o = P.part_surf_off[j];
   const V3 tcp = V3{P.pre_tcp[3 * pre], P.pre_tcp[3 * pre + 1], P.pre_tcp[3 * pre + 2]};
   const V3 c = transform(r, t, tcp);
-  if (threadIdx.x == 0) col_constants(P, pre, th, S.colc + j);
-  __shared__ double s_bmax[kNnThreads];
-  double bmax = 0.0;
+  // The collision constants need an FP64 inverse pose: the last warp's lane 0
+  // (its loop share is one point shorter for 1,008-point surfaces).
+  if (threadIdx.x == blockDim.x - 32) col_constants(P, pre, th, S.colc + j);
+  __shared__ double s_b2[kNnThreads / 32];
+  const float B_obj = __double2float_ru(P.obj_meta[3]);
+  double b2max = 0.0;
   for (int i = threadIdx.x; i < ns; i += blockDim.x) {
     const V3 w = transform(r, t, load3(P.surf64, s0 + i));
     S.S64[3 * (o + i) + 0] = w.x;
     S.S64[3 * (o + i) + 1] = w.y;
     S.S64[3 * (o + i) + 2] = w.z;
     const double ax = w.x - P.obj_meta[0], ay = w.y - P.obj_meta[1], az = w.z - P.obj_meta[2];
-    const double A = sqrt(ax * ax + ay * ay + az * az);
+    // Certification margin from an FP32 upper bound of |a| (any upper bound
+    // keeps the window valid; the FP64 square root is off the path).
+    const float A = __fsqrt_ru(__double2float_ru(ax * ax + ay * ay + az * az));
     S.Sq32[o + i] = make_float4(__double2float_rn(ax), __double2float_rn(ay), __double2float_rn(az),
-                                nn_margin(A, P.obj_meta[3]));
+                                nn_margin32(A, B_obj));
     const double bx = w.x - c.x, by = w.y - c.y, bz = w.z - c.z;
     const float fx = __double2float_rn(bx), fy = __double2float_rn(by), fz = __double2float_rn(bz);
     const double gx = fx, gy = fy, gz = fz;
@@ -113,16 +118,18 @@ __global__ void pose_prep_kernel(DevProblem P, DevState S, int all) {
     // filter evaluates two of them per packed FFMA2.
     pc_put(S.Sc32 + o, i,
            make_float4(-2.0f * fx, -2.0f * fy, -2.0f * fz, __double2float_rn(gx * gx + gy * gy + gz * gz)));
-    bmax = fmax(bmax, sqrt(bx * bx + by * by + bz * bz));
+    b2max = fmax(b2max, bx * bx + by * by + bz * bz);  // max |s - ctr|^2: one square root at the end
   }
   for (int i = ns + threadIdx.x; i < round_up(ns, kSub); i += blockDim.x)
     pc_put(S.Sc32 + o, i, make_float4(0.0f, 0.0f, 0.0f, INFINITY));
-  s_bmax[threadIdx.x] = bmax;
+  for (int off = 16; off > 0; off >>= 1) b2max = fmax(b2max, __shfl_xor_sync(0xffffffffu, b2max, off));
+  if ((threadIdx.x & 31) == 0) s_b2[threadIdx.x >> 5] = b2max;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int i = 0; i < blockDim.x; ++i) m = fmax(m, s_bmax[i]);
-    S.Bs[j] = m * (1.0 + 1e-6) + 1e-12;
+    double m2 = 0.0;
+    for (int w = 0; w < kNnThreads / 32; ++w) m2 = fmax(m2, s_b2[w]);
+    // sqrt is monotone and correctly rounded: sqrt(max |b|^2) = max |b|.
+    S.Bs[j] = sqrt(m2) * (1.0 + 1e-6) + 1e-12;
     S.ctr[3 * j] = c.x;
     S.ctr[3 * j + 1] = c.y;
     S.ctr[3 * j + 2] = c.z;
