@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace asicp {
 
@@ -445,7 +446,11 @@ int launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t s
   if (P.n_obj <= kCountMax) {
     const int ncnt = P.n_obj > m ? P.n_obj : m;
     const int64_t arena16 = (static_cast<int64_t>((ncnt + 1) / 2 * 2) + 4ll * m) * 2;
-    if (P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max)
+    static const bool mb16 = [] {
+      const char* e = std::getenv("ASICP_MB16");
+      return !(e && e[0] == '0');
+    }();
+    if (mb16 && P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max)
       return cnt_launches(minibatch_cnt_kernel<uint16_t>, static_cast<size_t>(arena16), 1);
     const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;
     const int in_smem = arena <= kMbArenaMax ? 1 : 0;
