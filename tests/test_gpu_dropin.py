@@ -67,3 +67,53 @@ def test_reference_scenario_front_end_on_b200(tmp_path):
     assert b200.stdout == ref.stdout
     assert trace.read_bytes() == ref_trace
     assert {f.name: f.read_bytes() for f in sorted(cache.iterdir())} == ref_fields
+
+
+def test_reference_cli_on_b200(tmp_path):
+    """SURVEY.md §8(f) rank 2 end to end: the reference's OWN command-line
+    front end (proj/tools/graspmatch_cli.cpp, unmodified; CLI11 from
+    oracle/shim) built on the reference library (graspmatch_ref) and on the
+    B200 drop-in (graspmatch_b200).  `grasp -c scenario.json` (cloud I/O,
+    fields built on the GPU into the GMSDF001 cache, solve, report, trace),
+    `sdf` (a field file) and the error path must match the reference's own
+    run byte for byte (wall-clock seconds masked)."""
+    import json
+    import re
+
+    exes = {k: REF / f"graspmatch_{k}" for k in ("ref", "b200")}
+    for e in exes.values():
+        if not e.exists():
+            pytest.skip(f"{e} not built (make -C oracle ref dropin)")
+
+    def run(kind, *args):
+        return subprocess.run([str(exes[kind]), *args], capture_output=True, text=True, timeout=600, cwd=tmp_path)
+
+    assert run("ref", "make-demo", "-d", "demo").returncode == 0
+    cfg = "demo/scenario.json"
+    ref = run("ref", "grasp", "-c", cfg, "--trace", "trace.txt", "--report", "report.json")
+    assert ref.returncode == 0, ref.stderr
+    ref_trace = (tmp_path / "trace.txt").read_bytes()
+    ref_report = json.loads((tmp_path / "report.json").read_text())
+    cache = tmp_path / "demo" / "cache"
+    ref_fields = {f.name: f.read_bytes() for f in sorted(cache.iterdir())}
+    for f in cache.iterdir():
+        f.unlink()
+    b200 = run("b200", "grasp", "-c", cfg, "--trace", "trace.txt", "--report", "report.json")
+    assert b200.returncode == 0, b200.stderr
+    mask = lambda s: re.sub(r"\d+\.\d\ds\)", "T s)", s)  # noqa: E731  (the wall-clock seconds)
+    assert "grasp found (preshape 0, 16/100 collision-free particles" in b200.stdout
+    assert mask(b200.stdout) == mask(ref.stdout)
+    assert (tmp_path / "trace.txt").read_bytes() == ref_trace
+    got_report = json.loads((tmp_path / "report.json").read_text())
+    for rep in (ref_report, got_report):
+        rep.pop("wall_seconds", None)
+    assert got_report == ref_report
+    assert {f.name: f.read_bytes() for f in sorted(cache.iterdir())} == ref_fields
+    # `sdf`: a field file from the gripper cloud, built on the GPU.
+    for kind in ("ref", "b200"):
+        r = run(kind, "sdf", "--cloud", "demo/gripper_full.ply", "--voxel", "0.004", "-o", f"field_{kind}.bin")
+        assert r.returncode == 0, r.stderr
+    assert (tmp_path / "field_b200.bin").read_bytes() == (tmp_path / "field_ref.bin").read_bytes()
+    # Error path: same message, same exit code.
+    ref_err, b200_err = run("ref", "grasp", "-c", "missing.json"), run("b200", "grasp", "-c", "missing.json")
+    assert ref_err.returncode == b200_err.returncode != 0 and ref_err.stderr == b200_err.stderr
