@@ -99,3 +99,27 @@ def test_minibatch_golden():
     g = np.load(GOLD / "minibatch.npz")
     for i, (s, n, m, skip) in enumerate(g["cases"]):
         assert np.array_equal(ref.sample_minibatch_indices(int(s), int(n), int(m), int(skip)), g[f"idx_{i}"])
+
+
+def test_reference_cli_builds_on_the_cli11_shim(tmp_path):
+    """oracle/shim/CLI11.hpp carries the reference's command-line front end
+    (proj/tools/graspmatch_cli.cpp, unmodified): make-demo + grasp -c print
+    README.md:43-46, options are validated like CLI11 (exit codes)."""
+    import subprocess
+
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "graspmatch_ref"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/graspmatch_ref not built (make -C oracle ref)")
+    run = lambda *a: subprocess.run([str(exe), *a], capture_output=True, text=True, timeout=300,  # noqa: E731
+                                    cwd=tmp_path)
+    assert run("make-demo", "-d", "demo").returncode == 0
+    r = run("grasp", "-c", "demo/scenario.json")
+    assert r.returncode == 0, r.stderr
+    assert "grasp found (preshape 0, 16/100 collision-free particles" in r.stdout
+    assert "t = [ 0.005176  0.000263  0.103996]" in r.stdout
+    assert "q = [ 0.995938 -0.005412  0.089213 -0.010885]" in r.stdout
+    assert "loss = 0.00022030658, converged = no" in r.stdout
+    assert run("bogus").returncode != 0
+    bad = run("sdf", "--cloud", "demo/gripper_full.ply", "--voxel", "-1", "-o", "f.bin")
+    assert bad.returncode != 0 and "positive" in bad.stderr
+    assert run("grasp").returncode != 0  # -c is required
