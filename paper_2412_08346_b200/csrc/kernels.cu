@@ -270,7 +270,11 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   const double* th = th_of(S.theta, j);
   const Q4 q = pose_q(th);
   const V3 t = pose_t(th);
-  const M3 r = rotation_matrix(q);
+  // rotation_matrix(q) (9 FP64 divisions) once per particle, shared.
+  __shared__ M3 sr[2];
+  if (tid == 0) sr[half] = rotation_matrix(q);
+  half_sync();
+  const M3 r = sr[half];
   M3 dR[4];
   rotation_matrix_derivatives(q, dR);
   const int s0 = P.pre_surf_off[pre];
@@ -341,13 +345,6 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
     for (int a = 0; a < 7; ++a) g[a] = acc[a] / m;
     S.loss[j] = loss;
     S.in_col[j] = reverse ? 1 : 0;
-    // prior_log_gradient (optim.cpp:146-156)
-    double* pg = S.prior + 7 * j;
-    for (int a = 0; a < 3; ++a) {
-      const double var = P.prior_t_sigma[a] * P.prior_t_sigma[a];
-      pg[a] = -(th[a] - P.prior_t_mean[a]) / var;
-    }
-    for (int a = 0; a < 4; ++a) pg[3 + a] = -P.prior_q_kappa[a] * sin(th[3 + a] - P.prior_q_location[a]);
   }
 }
 
@@ -374,7 +371,16 @@ __global__ void drift_kernel(DevProblem P, DevState S, double gamma, double n_re
   pdl_enter();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.J) return;
-  for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + S.prior[7 * j + a]);
+  // prior_log_gradient (optim.cpp:146-156) of the iteration's pose (Stein
+  // iterations only need it; theta is unchanged since the evaluation).
+  const double* th = th_of(S.theta, j);
+  double pg[7];
+  for (int a = 0; a < 3; ++a) {
+    const double var = P.prior_t_sigma[a] * P.prior_t_sigma[a];
+    pg[a] = -(th[a] - P.prior_t_mean[a]) / var;
+  }
+  for (int a = 0; a < 4; ++a) pg[3 + a] = -P.prior_q_kappa[a] * sin(th[3 + a] - P.prior_q_location[a]);
+  for (int a = 0; a < 7; ++a) S.drift[7 * j + a] = gamma * (n_ref * S.grad[7 * j + a] + pg[a]);
 }
 
 // Small populations: median_kernel in median.cu.

@@ -106,7 +106,6 @@ struct DevState {
   int* active;
   int* n_col;
   double* grad;        // J x 7 likelihood gradient
-  double* prior;       // J x 7 prior log-gradient
   double* drift;       // J x 7
   const double* theta_all;  // global J x 7 poses (SVGD partners / median)
   const double* drift_all;  // global J x 7 drifts

@@ -151,7 +151,7 @@ struct asicp_ctx {
   // Collision clusters (collide.cu) and the scratch of their Morton sort.
   Buf scene_box, scene_code, scene_idx, scene_tmp, clusters, subclusters, scene_s32, scene_perm;
   int n_clusters = 0;
-  Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, prior, drift, h, S64, Sq32, Sc32,
+  Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, drift, h, S64, Sq32, Sc32,
       Bs, ctr, colc, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
       item_count, item_off, item_counter, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
@@ -246,7 +246,7 @@ struct asicp_ctx {
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
                   &scene_s32, &scene_perm, &theta,
-                  &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &prior, &drift, &h,
+                  &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &drift, &h,
                   &S64, &Sq32, &Sc32, &Bs, &ctr, &colc, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
                   &item_counter,
@@ -581,7 +581,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->active.ensure(Jz * 4);
   c->n_col.ensure(Jz * 4);
   c->grad.ensure(Jz * 7 * 8);
-  c->prior.ensure(Jz * 7 * 8);
   c->drift.ensure(Jz * 7 * 8);
   c->h.ensure(static_cast<size_t>(n_pre) * 8);
   c->S64.ensure(static_cast<size_t>(so) * 24);
@@ -730,7 +729,6 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.active = c->active.as<int>();
   S.n_col = c->n_col.as<int>();
   S.grad = c->grad.as<double>();
-  S.prior = c->prior.as<double>();
   S.drift = c->drift.as<double>();
   S.theta_all = c->xchg ? c->theta_all.as<double>() : S.theta;
   S.drift_all = c->xchg ? c->drift_all.as<double>() : S.drift;
