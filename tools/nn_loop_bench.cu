@@ -26,7 +26,7 @@ constexpr int kSub = 32, kCand = 2048;
 // MODE 0: hot loop only, 1: + top-3 per subtile, 2: + top-3 with the queries
 // held as pre-packed register pairs (no .F32 broadcast operand), 3: scalar
 // FFMA form + top-3.  Queries come from global memory (no constant folding).
-template <int MODE, int Q = 8, int MINB = 4>
+template <int MODE, int Q = 8, int MINB = 4, int UNR = 2>
 __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, const float4* qin, float* out, int reps) {
   __shared__ float4 tile[kCand];
   for (int i = threadIdx.x; i < kCand; i += blockDim.x) tile[i] = cand[i];
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, con
           }
         }
       } else {
-#pragma unroll 2
+#pragma unroll UNR
       for (int c = 0; c < kSub; c += 4) {
         const float4 a0 = sp[c], c0 = sp[c + 1];
         const float4 a1 = sp[c + 2], c1 = sp[c + 3];
@@ -181,6 +181,11 @@ int main() {
       printf("hot loop + top-3, Q=%d, %d CTAs/SM: %.2f pairs/clk/SM  FMA pipe %.2f\n", q, per_sm, per_clk_sm,
              per_clk_sm * 3 / 128);
     };
+    run(loop_kernel<1, 8, 4, 1>, 8, 4);
+    run(loop_kernel<1, 8, 4, 4>, 8, 4);
+    run(loop_kernel<1, 8, 4, 8>, 8, 4);
+    run(loop_kernel<0, 8, 4, 4>, 8, 4);
+    run(loop_kernel<0, 8, 4, 8>, 8, 4);
     run(loop_kernel<1, 4, 8>, 4, 8);
     run(loop_kernel<1, 4, 6>, 4, 6);
     run(loop_kernel<1, 12, 2>, 12, 2);
