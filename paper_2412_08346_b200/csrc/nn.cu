@@ -49,8 +49,24 @@ constexpr int kMinChunk = 2 * kNnTile;       // smallest candidate split
 // kMinChunk candidates per split.  Reverse: warp items of kRevWQ points.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_out, int* chunk_out) {
-  int nch = T > 0 ? min(plan.nchunks, max(1, ceil_div(plan.target_items, T))) : 1;
-  nch = max(1, min(nch, plan.m / kMinChunk));
+  const int nmax = T > 0 ? max(1, min(plan.nchunks, min(plan.m / kMinChunk, ceil_div(plan.target_items, T)))) : 1;
+  // Among 1..nmax splits, the one with the shortest estimated makespan on the
+  // persistent grid (target_items / 4 CTAs): rounds of items x (candidates
+  // per item + a per-item overhead), so the last round of equal items is as
+  // full as it can be.  T x splits <= target_items keeps the item lists in
+  // their preallocated size.
+  const int grid = max(1, plan.target_items / 4);
+  int nch = nmax;
+  long long best = -1;
+  for (int s = 1; s <= nmax; ++s) {
+    const int chunk = round_up(ceil_div(plan.m, s), kNnTile);
+    const int items = T * ceil_div(plan.m, chunk);
+    const long long cost = static_cast<long long>(ceil_div(items, grid)) * (chunk + 512);
+    if (best < 0 || cost < best) {  // ties: fewer splits (less merging)
+      best = cost;
+      nch = s;
+    }
+  }
   const int chunk = round_up(ceil_div(plan.m, nch), kNnTile);
   *chunk_out = chunk;
   *nch_out = ceil_div(plan.m, chunk);

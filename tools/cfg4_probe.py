@@ -26,6 +26,7 @@ ap.add_argument("mode", choices=["times", "unit"])
 ap.add_argument("--objects", type=int, default=11)
 ap.add_argument("--unit", type=int, default=0)
 ap.add_argument("--eager", action="store_true")
+ap.add_argument("--max-chunks", type=int, default=0, help="ASICP_OPT_MAX_CHUNKS of the batch contexts")
 a = ap.parse_args()
 
 problems = [fixtures.config(4, seed=o).problem() for o in range(a.objects)]
@@ -73,7 +74,7 @@ for i, p in enumerate(subs):
     s.close()
 print("isolated unit solve ms:", " ".join(f"{t:.2f}" for t in iso))
 print(f"sum of isolated unit solves: {sum(iso):.1f} ms  (mean {sum(iso) / len(iso):.2f} ms)")
-b = BatchSolver(subs)
+b = BatchSolver(subs, max_chunks=a.max_chunks)
 b.run()
 ts = []
 for _ in range(5):
