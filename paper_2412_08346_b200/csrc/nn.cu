@@ -61,7 +61,7 @@ __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_ou
   for (int s = 1; s <= nmax; ++s) {
     const int chunk = round_up(ceil_div(plan.m, s), kNnTile);
     const int items = T * ceil_div(plan.m, chunk);
-    const long long cost = static_cast<long long>(ceil_div(items, grid)) * (chunk + 512);
+    const long long cost = static_cast<long long>(ceil_div(items, grid)) * (chunk + plan.item_overhead);
     if (best < 0 || cost < best) {  // ties: fewer splits (less merging)
       best = cost;
       nch = s;

@@ -839,6 +839,11 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   // least 2 tiles of candidates each.
   plan.nchunks = std::max(1, std::min(c->max_chunks, static_cast<int>(m / (2 * kNnTile))));
   plan.target_items = c->target_items;
+  static const int item_overhead = [] {  // ASICP_NN_ITEM_OVERHEAD: split-model experiments
+    const char* e = std::getenv("ASICP_NN_ITEM_OVERHEAD");
+    return e ? std::max(0, std::atoi(e)) : 512;
+  }();
+  plan.item_overhead = item_overhead;
   plan.max_ns = c->max_ns;
   return plan;
 }
