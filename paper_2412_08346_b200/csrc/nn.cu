@@ -792,24 +792,44 @@ __global__ void nn_merge_kernel(DevProblem P, DevState S, NnPlan plan) {
 // Full FP64 rescan (ambiguous windows, and the FP64 validation mode): one
 // warp per query, lexicographic (distance, position) minimum — exactly the
 // reference's kd-tree rule.
-__global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
+// Full FP64 rescans (validation mode, overflowing or unlisted windows): one
+// CTA per entry, every thread scanning a stride of the candidates with its
+// loads batched (the candidate map and rows are L2 gathers), then a block
+// argmin with the reference's tie rule (equal distance -> lowest position).
+__global__ void __launch_bounds__(256) nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
   pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  __shared__ double s_best[8];
+  __shared__ int s_bi[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int total = min(*S.refine_count, S.refine_cap);
-  for (int e = warp; e < total; e += nwarps) {
+  for (int e = blockIdx.x; e < total; e += gridDim.x) {
     const int4 r = S.refine_list[e];
     const int kind = r.x, j = r.y, qlocal = r.z;
     const NnGeom g = nn_geom(P, S, plan, kind, j, qlocal);
     const int nc = kind == 1 ? surf_count(P, j) : plan.m;
+    const V3 qp = V3{g.qpt[0], g.qpt[1], g.qpt[2]};
     double best = INFINITY;
     int bi = 0x7fffffff;
-    for (int c = lane; c < nc; c += 32) {
-      const double d = nn_d64(g, c);
-      if (d < best || (d == best && c < bi)) {
-        best = d;
-        bi = c;
+    constexpr int kU = 4;
+    for (int c0 = threadIdx.x; c0 < nc; c0 += kU * blockDim.x) {
+      int64_t row[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = c0 + u * blockDim.x;
+        row[u] = c < nc ? (g.cmap ? g.cmap[c] : c) : 0;
+      }
+      V3 p[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) p[u] = load3(g.cbase, row[u]);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int c = c0 + u * blockDim.x;
+        if (c >= nc) continue;
+        const double d = sqnorm(sub(p[u], qp));  // spatial_index.cpp:69
+        if (d < best || (d == best && c < bi)) {
+          best = d;
+          bi = c;
+        }
       }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -820,7 +840,20 @@ __global__ void nn_refine_kernel(DevProblem P, DevState S, NnPlan plan) {
         bi = oi;
       }
     }
-    if (lane == 0) *nn_result_slot(P, S, kind, j, qlocal) = bi;
+    if (lane == 0) {
+      s_best[wid] = best;
+      s_bi[wid] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+        if (s_best[w] < best || (s_best[w] == best && s_bi[w] < bi)) {
+          best = s_best[w];
+          bi = s_bi[w];
+        }
+      *nn_result_slot(P, S, kind, j, qlocal) = bi;
+    }
+    __syncthreads();
   }
 }
 

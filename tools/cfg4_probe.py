@@ -56,6 +56,8 @@ if a.mode == "unit":
     nsub = 4 * ((problems[units[a.unit].obj].scene_cloud.shape[0] + 31) // 32)
     print(f"collision sub-clusters left to the point test: {raw[14]} of {raw[13] + 1024} x {nsub} "
           f"({raw[14] / max(1, (raw[13] + 1024) * nsub):.3%})")
+    print(f"NN: uncertified windows {raw[0]}, full FP64 rescans {raw[1]} (validation {raw[8]}, ambiguous window "
+          f"{raw[9]}, across splits {raw[11]}), queries {raw[2]}")
     ph = raw[240:248]
     if sum(ph):
         names = ["item start", "TMA wait", "hot loop", "top-3", "window epilogue", "sub-chunk barrier", "emit",
