@@ -905,87 +905,117 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
       atomicAdd(S.iter_stats + 4 * plan.iter + 1, pairs);
       atomicAdd(S.iter_stats + 4 * plan.iter + 3, static_cast<unsigned long long>(w.nq));
     }
-    const bool has = lane < w.nq;
-    const float4 q = has ? w.q[lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // Two queries per lane (lane and lane + 32): the staged candidates are read
+    // once for both, and four packed FMA chains per step keep the lane busy.
+    constexpr int QR = kRevWQ / 32;
+    float4 q[QR];
+    bool has[QR];
+#pragma unroll
+    for (int r = 0; r < QR; ++r) {
+      has[r] = lane + 32 * r < w.nq;
+      q[r] = has[r] ? w.q[lane + 32 * r] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     const int nsub = ceil_div(w.nc, kSub);  // candidate rows are +inf padded to the subtile
-    float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
-    int s1 = 0, s2 = 0;
-    const f32x2 qx2 = pk2(q.x, q.x), qy2 = pk2(q.y, q.y), qz2 = pk2(q.z, q.z);
+    float b1[QR], b2[QR], b3[QR];
+    int s1[QR], s2[QR];
+    f32x2 qx2[QR], qy2[QR], qz2[QR];
+#pragma unroll
+    for (int r = 0; r < QR; ++r) {
+      b1[r] = b2[r] = b3[r] = INFINITY;
+      s1[r] = s2[r] = 0;
+      qx2[r] = pk2(q[r].x, q[r].x);
+      qy2[r] = pk2(q[r].y, q[r].y);
+      qz2[r] = pk2(q[r].z, q[r].z);
+    }
     const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
     for (int sub = 0; sub < nsub; ++sub) {
-      float tm;
+      float tm[QR];
       if (staged) {
         // Candidates are pair-interleaved (pc_index): per 4 candidates four
-        // broadcast LDS.128, six packed FFMA2 (each lane is d32()), two mins.
+        // broadcast LDS.128, six packed FFMA2 per query (each lane is d32()).
         const uint32_t sp = stage_s + static_cast<uint32_t>(sub * kSub) * 16u;
-        float t0 = INFINITY, t1 = INFINITY;
+        float t0[QR], t1[QR];
+#pragma unroll
+        for (int r = 0; r < QR; ++r) t0[r] = t1[r] = INFINITY;
 #pragma unroll
         for (int c = 0; c < kSub; c += 4) {
           const float4 A0 = lds128(sp + c * 16u), B0 = lds128(sp + (c + 1) * 16u);
           const float4 A1 = lds128(sp + (c + 2) * 16u), B1 = lds128(sp + (c + 3) * 16u);
-          f32x2 d0 = ffma2(pk2(B0.x, B0.y), qz2, pk2(B0.z, B0.w));
-          f32x2 d1 = ffma2(pk2(B1.x, B1.y), qz2, pk2(B1.z, B1.w));
-          d0 = ffma2(pk2(A0.z, A0.w), qy2, d0);
-          d1 = ffma2(pk2(A1.z, A1.w), qy2, d1);
-          d0 = ffma2(pk2(A0.x, A0.y), qx2, d0);
-          d1 = ffma2(pk2(A1.x, A1.y), qx2, d1);
-          float l0, h0, l1, h1;
-          up2(d0, l0, h0);
-          up2(d1, l1, h1);
-          t0 = fminf(t0, fminf(l0, h0));
-          t1 = fminf(t1, fminf(l1, h1));
+#pragma unroll
+          for (int r = 0; r < QR; ++r) {
+            f32x2 d0 = ffma2(pk2(B0.x, B0.y), qz2[r], pk2(B0.z, B0.w));
+            f32x2 d1 = ffma2(pk2(B1.x, B1.y), qz2[r], pk2(B1.z, B1.w));
+            d0 = ffma2(pk2(A0.z, A0.w), qy2[r], d0);
+            d1 = ffma2(pk2(A1.z, A1.w), qy2[r], d1);
+            d0 = ffma2(pk2(A0.x, A0.y), qx2[r], d0);
+            d1 = ffma2(pk2(A1.x, A1.y), qx2[r], d1);
+            float l0, h0, l1, h1;
+            up2(d0, l0, h0);
+            up2(d1, l1, h1);
+            t0[r] = fminf(t0[r], fminf(l0, h0));
+            t1[r] = fminf(t1[r], fminf(l1, h1));
+          }
         }
-        tm = fminf(t0, t1);
+#pragma unroll
+        for (int r = 0; r < QR; ++r) tm[r] = fminf(t0[r], t1[r]);
       } else {
-        float t0 = INFINITY;
-        for (int c = 0; c < kSub; ++c) t0 = fminf(t0, d32(q.x, q.y, q.z, pc_get(cand, sub * kSub + c)));
-        tm = t0;
+#pragma unroll
+        for (int r = 0; r < QR; ++r) {
+          float t0 = INFINITY;
+          for (int c = 0; c < kSub; ++c) t0 = fminf(t0, d32(q[r].x, q[r].y, q[r].z, pc_get(cand, sub * kSub + c)));
+          tm[r] = t0;
+        }
       }
-      // Running top-3 of subtile minima (strict < keeps the earliest).
-      const bool lt1 = tm < b1, lt2 = tm < b2;
-      b3 = lt2 ? b2 : fminf(b3, tm);
-      s2 = lt1 ? s1 : (lt2 ? sub : s2);
-      b2 = lt1 ? b1 : (lt2 ? tm : b2);
-      s1 = lt1 ? sub : s1;
-      b1 = lt1 ? tm : b1;
+#pragma unroll
+      for (int r = 0; r < QR; ++r) {
+        // Running top-3 of subtile minima (strict < keeps the earliest).
+        const bool lt1 = tm[r] < b1[r], lt2 = tm[r] < b2[r];
+        b3[r] = lt2 ? b2[r] : fminf(b3[r], tm[r]);
+        s2[r] = lt1 ? s1[r] : (lt2 ? sub : s2[r]);
+        b2[r] = lt1 ? b1[r] : (lt2 ? tm[r] : b2[r]);
+        s1[r] = lt1 ? sub : s1[r];
+        b1[r] = lt1 ? tm[r] : b1[r];
+      }
     }
-    if (!has) continue;
-    const int qlocal = w.q_first + lane;
-    int* slot = S.res_rev + static_cast<int64_t>(w.owner) * P.n_scene + qlocal;
-    if (plan.fp64_mode) {
-      push_refine(S, 1, w.owner, qlocal, 0, plan.iter);
-      continue;
-    }
-    const float thr = __fadd_ru(b1, q.w);
-    bool ovf = b3 <= thr;
-    int pos[kWinCap];
-    int np = 0, pmin = -1;
-    const int nscan = b2 <= thr ? 2 : 1;
-    for (int r = 0; r < nscan; ++r) {
-      const int sid = r == 0 ? s1 : s2;
-      // Member bitmask in one pass, then the members in increasing position.
-      unsigned mask = 0;
+    for (int r = 0; r < QR; ++r) {
+      if (!has[r]) continue;
+      const int qlocal = w.q_first + lane + 32 * r;
+      int* slot = S.res_rev + static_cast<int64_t>(w.owner) * P.n_scene + qlocal;
+      if (plan.fp64_mode) {
+        push_refine(S, 1, w.owner, qlocal, 0, plan.iter);
+        continue;
+      }
+      const float thr = __fadd_ru(b1[r], q[r].w);
+      bool ovf = b3[r] <= thr;
+      int pos[kWinCap];
+      int np = 0, pmin = -1;
+      const int nscan = b2[r] <= thr ? 2 : 1;
+      for (int sc = 0; sc < nscan; ++sc) {
+        const int sid = sc == 0 ? s1[r] : s2[r];
+        // Member bitmask in one pass, then the members in increasing position.
+        unsigned mask = 0;
 #pragma unroll 8
-      for (int c = 0; c < kSub; ++c)
-        mask |= (d32(q.x, q.y, q.z, pc_get(cand, sid * kSub + c)) <= thr ? 1u : 0u) << c;
-      while (mask) {
-        const int c = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const float d = d32(q.x, q.y, q.z, pc_get(cand, sid * kSub + c));
-        const int p = sid * kSub + c;
-        if (np < kWinCap) pos[np] = p;
-        ++np;
-        if (d == b1 && (pmin < 0 || p < pmin)) pmin = p;
+        for (int c = 0; c < kSub; ++c)
+          mask |= (d32(q[r].x, q[r].y, q[r].z, pc_get(cand, sid * kSub + c)) <= thr ? 1u : 0u) << c;
+        while (mask) {
+          const int c = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const float d = d32(q[r].x, q[r].y, q[r].z, pc_get(cand, sid * kSub + c));
+          const int p = sid * kSub + c;
+          if (np < kWinCap) pos[np] = p;
+          ++np;
+          if (d == b1[r] && (pmin < 0 || p < pmin)) pmin = p;
+        }
       }
-    }
-    ovf = ovf || np > kWinCap;
-    if (ovf) {
-      push_refine(S, 1, w.owner, qlocal, 1, plan.iter);
-    } else if (np == 1) {
-      *slot = pmin;  // certified
-    } else {
-      const NnGeom g = nn_geom(P, S, plan, 1, w.owner, qlocal);
-      *slot = nn_decide(g, pos, np, false, S.stats);
+      ovf = ovf || np > kWinCap;
+      if (ovf) {
+        push_refine(S, 1, w.owner, qlocal, 1, plan.iter);
+      } else if (np == 1) {
+        *slot = pmin;  // certified
+      } else {
+        const NnGeom g = nn_geom(P, S, plan, 1, w.owner, qlocal);
+        *slot = nn_decide(g, pos, np, false, S.stats);
+      }
     }
   }
 }

@@ -30,7 +30,7 @@ constexpr int kNnTile = 256;                    // candidates per TMA tile (4 KB
 constexpr int kNnStages = 8;                    // whole chunk resident: rescans read shared memory
 constexpr int kNnMaxChunk = kNnStages * kNnTile; // candidates per work item (2048, 32 KB)
 constexpr int kNnL = 4;                         // window list entries per query
-constexpr int kRevWQ = 32;                      // reverse: queries per warp item
+constexpr int kRevWQ = 64;                      // reverse: queries per warp item (two per lane)
 
 // One NN work item: a block of <= kNnQB queries against a contiguous
 // candidate chunk.
