@@ -22,7 +22,8 @@ from paper_2412_08346_b200.batch import BatchSolver  # noqa: E402
 from paper_2412_08346_b200.grasp import CProblem  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("mode", choices=["times", "unit"])
+ap.add_argument("mode", choices=["times", "unit", "subset"])
+ap.add_argument("--units", type=str, default="4,8,17,33", help="subset: batch sizes (first U units) to time")
 ap.add_argument("--objects", type=int, default=11)
 ap.add_argument("--unit", type=int, default=0)
 ap.add_argument("--eager", action="store_true")
@@ -64,6 +65,21 @@ if a.mode == "unit":
                  "exit"]
         print("NN filter phases (warp-cycles): " + ", ".join(f"{n} {v / sum(ph):.1%}" for n, v in zip(names, ph)))
     s.close()
+    sys.exit(0)
+
+if a.mode == "subset":
+    # Device time of a batch of the first U units (the per-rank share of the
+    # cfg4 plan at 8 / 4 / 2 ranks is 4 / 8 / 16 whole units + a slice).
+    for u in [int(x) for x in a.units.split(",")]:
+        b = BatchSolver(subs[:u])
+        b.run()
+        ts = []
+        for _ in range(5):
+            t0 = time.perf_counter()
+            b.run()
+            ts.append(1e3 * (time.perf_counter() - t0))
+        b.close()
+        print(f"{u:3d} units ({u * 1024} particles): {sorted(ts)[2]:.1f} ms (median of 5)", flush=True)
     sys.exit(0)
 
 iso = []
