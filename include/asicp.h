@@ -52,6 +52,8 @@ extern "C" {
 #define ASICP_OPT_USE_GRAPH 2      /* 1 = capture the iteration loop in a CUDA graph (default 1) */
 #define ASICP_OPT_PROFILE 3        /* 1 = record per-kernel CUDA events (asicp_get_stats) */
 #define ASICP_OPT_MAX_CHUNKS 4     /* cap on the forward match's candidate split (default 16) */
+#define ASICP_OPT_THROUGHPUT 6     /* 1 = this context shares the GPU with other solves (batch): the forward
+                                      match splits its candidates for throughput, not for one solve's latency */
 #define ASICP_OPT_WINDOW_POOL 5    /* ambiguous-window blocks per NN round (0 = sized automatically);
                                       an exhausted pool falls back to full FP64 rescans (testing) */
 

@@ -26,6 +26,7 @@ class BatchSolver:
         if streams is not None and len(streams) != len(problems):
             raise ValueError("one stream per problem")
         self.solvers: List[Solver] = []
+        solver_kw.setdefault("throughput", True)  # the entries share the GPU: split the NN for throughput
         for i, p in enumerate(problems):
             s = Solver(device=device, stream=streams[i] if streams is not None else None, **solver_kw)
             if setup is not None:

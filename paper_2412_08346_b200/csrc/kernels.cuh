@@ -158,6 +158,7 @@ struct NnPlan {
   int nchunks;   // upper bound on forward candidate splits (split-K); the device picks <= this
   int target_items;  // forward items the device split aims for (fills the persistent grid)
   int item_overhead; // per-item cost of the split model, in candidates (fwd_split)
+  int throughput;    // split model for a GPU shared with other solves (ASICP_OPT_THROUGHPUT)
   int fp64_mode; // resolve every query by FP64 brute force (validation mode)
   int max_ns;    // largest contact surface (merge grid)
   int iter;      // iteration index (diagnostic counters)

@@ -55,13 +55,19 @@ __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_ou
   // per item + a per-item overhead), so the last round of equal items is as
   // full as it can be.  T x splits <= target_items keeps the item lists in
   // their preallocated size.
+  // Throughput mode (contexts that share the GPU, batch.py): other solves
+  // fill a round's idle CTAs, so only the per-item cost of full rounds counts.
+  // Latency mode (one solve alone): list-scheduling makespan — the work spread
+  // over every CTA slot plus the last item's length.
   const int grid = max(1, plan.target_items / 4);
   int nch = nmax;
   long long best = -1;
   for (int s = 1; s <= nmax; ++s) {
     const int chunk = round_up(ceil_div(plan.m, s), kNnTile);
     const int items = T * ceil_div(plan.m, chunk);
-    const long long cost = static_cast<long long>(ceil_div(items, grid)) * (chunk + plan.item_overhead);
+    const long long per = chunk + plan.item_overhead;
+    const long long cost = plan.throughput ? static_cast<long long>(ceil_div(items, grid)) * per
+                                           : static_cast<long long>(items) * per / grid + per;
     if (best < 0 || cost < best) {  // ties: fewer splits (less merging)
       best = cost;
       nch = s;

@@ -114,6 +114,7 @@ struct asicp_ctx {
   int nn_grid = 296;
   int max_chunks = 16;
   int window_pool = 0;  // ASICP_OPT_WINDOW_POOL (0: automatic)
+  int throughput = 0;   // ASICP_OPT_THROUGHPUT: the NN split model of a shared GPU
 
   // Prepared problem (host side).
   bool prepared = false;
@@ -844,6 +845,7 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
     return e ? std::max(0, std::atoi(e)) : 512;
   }();
   plan.item_overhead = item_overhead;
+  plan.throughput = c->throughput;
   plan.max_ns = c->max_ns;
   return plan;
 }
@@ -1230,6 +1232,9 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
       break;
     case ASICP_OPT_PROFILE:
       ctx->profile = static_cast<int>(value);
+      break;
+    case ASICP_OPT_THROUGHPUT:
+      ctx->throughput = value ? 1 : 0;
       break;
     default:
       return ASICP_INVALID_ARGUMENT;
