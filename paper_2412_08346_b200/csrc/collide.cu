@@ -255,7 +255,10 @@ __global__ void __launch_bounds__(kColThreads, 8) collide_kernel(DevProblem P, D
   const int nwords = (P.n_scene + 31) / 32;
   const int ncl = P.n_clusters;
   unsigned int* hitbits = col_smem;                                      // bit per scene point (original order)
-  int* list1 = reinterpret_cast<int*>(col_smem + round_up(nwords, 4));  // clusters left after level 1
+  // Cluster lists in shared memory, or (scenes beyond ~270k points) in the
+  // particle's global scratch.
+  int* list1 = P.col_lists_global ? S.col_lists + static_cast<int64_t>(j) * ncl * (1 + kSubPerCluster)
+                                  : reinterpret_cast<int*>(col_smem + round_up(nwords, 4));  // left after level 1
   int* list2 = list1 + ncl;                                              // sub-clusters left after level 2
   __shared__ ColConst K;
   __shared__ int s_n1, s_n2;
@@ -436,13 +439,22 @@ __global__ void __launch_bounds__(kColThreads, 8) collide_kernel(DevProblem P, D
   }
 }
 
-size_t collide_smem_bytes(const DevProblem& P) {
+constexpr size_t kColSmemMax = 200 * 1024;
+
+static size_t collide_smem_full(const DevProblem& P) {
   return static_cast<size_t>(round_up((P.n_scene + 31) / 32, 4)) * sizeof(unsigned int) +
          static_cast<size_t>(P.n_clusters) * (1 + kSubPerCluster) * sizeof(int);
 }
 
+bool collide_lists_global(const DevProblem& P) { return collide_smem_full(P) > kColSmemMax; }
+
+size_t collide_smem_bytes(const DevProblem& P) {
+  return P.col_lists_global ? static_cast<size_t>(round_up((P.n_scene + 31) / 32, 4)) * sizeof(unsigned int)
+                            : collide_smem_full(P);
+}
+
 void collide_set_attrs() {
-  cudaFuncSetAttribute(collide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(collide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kColSmemMax));
 }
 
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st) {

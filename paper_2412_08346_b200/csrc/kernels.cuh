@@ -32,6 +32,7 @@ struct DevProblem {
   const float4* subclusters;  // n_clusters x kSubPerCluster spheres of kSubPts points
   const float4* scene_s32;  // scene32 in sorted order, n_clusters x kClusterPts
   const int* scene_perm;    // sorted position -> scene index (-1: padding)
+  int col_lists_global;     // the collision kernel's cluster lists live in DevState::col_lists (large scenes)
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
   const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
   const double* pre_tcp;    // preshape tcp, 3 per preshape
@@ -116,6 +117,7 @@ struct DevState {
   double* ctr;         // J x 3 per-particle reverse-match centre (TCP in world)
   double* Bs;          // per particle max |s - ctr|
   ColConst* colc;      // per particle collision-test constants
+  int* col_lists;      // J x 5 x n_clusters cluster lists (only when DevProblem::col_lists_global)
   int* col_idx;        // J x n_scene colliding scene indices (scene order)
   float4* col_q;       // J x n_scene FP32 reverse queries (particle-centred)
   int* res_fwd;        // per surface row: NN position in the candidate set
@@ -190,6 +192,7 @@ void launch_seed_rng(const DevProblem& P, DevState& S, uint64_t seed, cudaStream
 void launch_init_state(const DevProblem& P, DevState& S, cudaStream_t st);
 void launch_pose_prep(const DevProblem& P, DevState& S, int all, cudaStream_t st);
 void launch_collide(const DevProblem& P, DevState& S, int all, int count_only, cudaStream_t st);  // collide.cu
+bool collide_lists_global(const DevProblem& P);  // the lists do not fit the kernel's shared memory
 constexpr int kClusterPts = 32;
 constexpr int kSubPts = 8;
 constexpr int kSubPerCluster = kClusterPts / kSubPts;

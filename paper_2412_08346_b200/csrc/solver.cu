@@ -153,7 +153,7 @@ struct asicp_ctx {
   Buf scene_box, scene_code, scene_idx, scene_tmp, clusters, subclusters, scene_s32, scene_perm;
   int n_clusters = 0;
   Buf theta, theta_next, loss, prev_loss, in_col, converged, active, n_col, grad, drift, h, S64, Sq32, Sc32,
-      Bs, ctr, colc, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
+      Bs, ctr, colc, col_lists, col_idx, col_q, res_fwd, res_rev, rng_state, rng_mti, pool_idx, pool32, fy_scratch, fy_par, items0,
       items1,
       item_count, item_off, item_counter, partials, amb_pool, amb_n, amb_count, refine_list, refine_count,
       stats, iter_stats, trace_theta,
@@ -248,7 +248,7 @@ struct asicp_ctx {
                   &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
                   &scene_s32, &scene_perm, &theta,
                   &theta_next, &loss, &prev_loss, &in_col, &converged, &active, &n_col, &grad, &drift, &h,
-                  &S64, &Sq32, &Sc32, &Bs, &ctr, &colc, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
+                  &S64, &Sq32, &Sc32, &Bs, &ctr, &colc, &col_lists, &col_idx, &col_q, &res_fwd, &res_rev, &rng_state, &rng_mti,
                   &pool_idx, &pool32, &fy_scratch, &fy_par, &items0, &items1, &item_count, &item_off,
                   &item_counter,
                   &partials, &amb_pool, &amb_n, &amb_count, &refine_list, &refine_count, &stats, &iter_stats, &trace_theta,
@@ -350,6 +350,8 @@ void validate(const asicp_problem& p) {
   for (int64_t g = 0; g < p.n_sdf_grids; ++g)
     for (int a = 0; a < 3; ++a) require(p.sdf_grids[g].dims[a] >= 2, "asicp: SDF grid needs >= 2 nodes per axis");
   require(p.n_object < (1ll << 30) && p.n_scene < (1ll << 30), "asicp: cloud too large");
+  // The collision kernel keeps one bit per scene point in shared memory.
+  require(p.n_scene <= 1600000, "asicp: scene cloud above 1,600,000 points");
 }
 
 void prepare(asicp_ctx* c, const asicp_problem& p) {
@@ -683,6 +685,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.scene32 = c->scene32.as<float4>();
   P.n_clusters = c->n_clusters;
   P.med_mid = c->med_mid;
+  P.col_lists_global = 0;
+  P.col_lists_global = collide_lists_global(P) ? 1 : 0;
   P.clusters = c->clusters.as<float4>();
   P.subclusters = c->subclusters.as<float4>();
   P.scene_s32 = c->scene_s32.as<float4>();
@@ -743,6 +747,9 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.Bs = c->Bs.as<double>();
   S.ctr = c->ctr.as<double>();
   S.colc = c->colc.as<ColConst>();
+  if (P.col_lists_global)
+    c->col_lists.ensure(Jz * (1 + kSubPerCluster) * static_cast<size_t>(c->n_clusters) * sizeof(int));
+  S.col_lists = P.col_lists_global ? c->col_lists.as<int>() : nullptr;
   S.col_idx = c->col_idx.as<int>();
   S.col_q = c->col_q.as<float4>();
   S.res_fwd = c->res_fwd.as<int>();

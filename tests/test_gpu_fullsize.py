@@ -104,3 +104,16 @@ def test_cfg5_large_cloud_parallel_minibatch(solver):
     want = ref.optimize_grasp(fx)
     got = solver.optimize(fx)
     assert_bit_identical(got, want, trace=True)
+
+
+def test_large_scene_collision_lists_in_global(solver):
+    """A 300k-point scene: the collision kernel's cluster lists no longer fit
+    its shared memory and move to global scratch (collide.cu); 8 particles x 5
+    iterations, full trajectory bit-identical to the reference."""
+    ref = _ref()
+    fx = fixtures.config(5, seed=0, particles_per_preshape=8, n_object=300000).set(
+        record_trace=1, k_max=5, k_stein=2, anneal_period_total=5)
+    assert fx.struct.n_scene > 270000
+    want = ref.optimize_grasp(fx)
+    got = solver.optimize(fx)
+    assert_bit_identical(got, want, trace=True)
