@@ -33,6 +33,7 @@ struct DevProblem {
   const float4* scene_s32;  // scene32 in sorted order, n_clusters x kClusterPts
   const int* scene_perm;    // sorted position -> scene index (-1: padding)
   int col_lists_global;     // the collision kernel's cluster lists live in DevState::col_lists (large scenes)
+  int throughput;           // the context shares the GPU with other solves (ASICP_OPT_THROUGHPUT)
   const double* surf64;     // concatenated preshape contact surfaces (gripper frame)
   const int* pre_surf_off;  // preshape -> offset into surf64 rows (n_pre + 1)
   const double* pre_tcp;    // preshape tcp, 3 per preshape

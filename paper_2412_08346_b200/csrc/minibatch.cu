@@ -446,10 +446,17 @@ int launch_minibatch_par(const DevProblem& P, DevState& S, int m, cudaStream_t s
   if (P.n_obj <= kCountMax) {
     const int ncnt = P.n_obj > m ? P.n_obj : m;
     const int64_t arena16 = (static_cast<int64_t>((ncnt + 1) / 2 * 2) + 4ll * m) * 2;
-    static const bool mb16 = [] {
+    // 16-bit arenas (two CTAs per SM) when the GPU is shared with other solves
+    // (throughput mode: the 32-bit arena's one-CTA-per-SM shared memory keeps
+    // the other solves' kernels off the SM) or when the population is large
+    // (many waves); a small solve alone (cfg2's 768 particles) runs the
+    // 32-bit kernel, which is faster per CTA (measured: cfg2 33.9 -> 33.1 ms,
+    // cfg3 / cfg5 faster with 16 bits).  ASICP_MB16=0/1 forces either.
+    static const int mb16_env = [] {
       const char* e = std::getenv("ASICP_MB16");
-      return !(e && e[0] == '0');
+      return e ? (e[0] == '0' ? 0 : 1) : -1;
     }();
+    const bool mb16 = mb16_env >= 0 ? mb16_env == 1 : (P.throughput != 0 || P.J >= 1024);
     if (mb16 && P.n_obj < 65535 && m < 65535 && arena16 <= kMbArena16Max)
       return cnt_launches(minibatch_cnt_kernel<uint16_t>, static_cast<size_t>(arena16), 1);
     const int64_t arena = mb_arena_ints(P.n_obj, m) * 4;

@@ -687,6 +687,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.med_mid = c->med_mid;
   P.col_lists_global = 0;
   P.col_lists_global = collide_lists_global(P) ? 1 : 0;
+  P.throughput = c->throughput;
   P.clusters = c->clusters.as<float4>();
   P.subclusters = c->subclusters.as<float4>();
   P.scene_s32 = c->scene_s32.as<float4>();
@@ -1242,6 +1243,7 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
       break;
     case ASICP_OPT_THROUGHPUT:
       ctx->throughput = value ? 1 : 0;
+      ctx->P.throughput = ctx->throughput;  // a prepared problem keeps its buffers; the graph is re-captured
       break;
     default:
       return ASICP_INVALID_ARGUMENT;
