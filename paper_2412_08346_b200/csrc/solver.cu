@@ -620,6 +620,8 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
     const size_t budget = c->fy_par.bytes + free_b / 4;
     fy_batch = static_cast<int>(std::min<size_t>(Jz, budget / fy_per));
   }
+  if (const char* e = std::getenv("ASICP_FY_BATCH"))  // test knob: force particle batches of the scratch
+    fy_batch = std::max(1, std::min(fy_batch, std::atoi(e)));
   const bool fy_par_on = fy_batch >= 1;
   if (fy_par_on) c->fy_par.ensure(static_cast<size_t>(fy_batch) * fy_per);
   if (fy_par_on && static_cast<size_t>(fy_batch) * fy_per < c->fy_par.bytes)  // an earlier, larger scratch

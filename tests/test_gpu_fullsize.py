@@ -117,3 +117,22 @@ def test_large_scene_collision_lists_in_global(solver):
     want = ref.optimize_grasp(fx)
     got = solver.optimize(fx)
     assert_bit_identical(got, want, trace=True)
+
+
+def test_minibatch_scratch_in_particle_batches(monkeypatch):
+    """The Fisher-Yates scratch sized to a batch of particles (large clouds
+    where the whole population's scratch exceeds a quarter of the free HBM):
+    forced to 100-particle batches here (ASICP_FY_BATCH), the minibatch
+    launches once per batch; cfg3 trajectory (3 x 40 particles, 20k-point scan)
+    bit-identical to the reference."""
+    ref = _ref()
+    monkeypatch.setenv("ASICP_FY_BATCH", "100")
+    fx = fixtures.config(3, seed=0, particles_per_preshape=40).set(record_trace=1, k_max=12, k_stein=5,
+                                                                    anneal_period_total=12)
+    want = ref.optimize_grasp(fx)
+    s = Solver()
+    try:
+        got = s.optimize(fx)
+    finally:
+        s.close()
+    assert_bit_identical(got, want, trace=True)
