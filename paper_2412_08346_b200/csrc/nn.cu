@@ -31,6 +31,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 namespace asicp {
@@ -866,61 +867,84 @@ __global__ void __launch_bounds__(256) nn_refine_kernel(DevProblem P, DevState S
 // ---------------------------------------------------------------------------
 // Reverse match (collision_loss_and_gradients, grasp.cpp:68-84): each
 // colliding scene point against the particle's transformed contact surface.
-// Colliding points are few per particle (tens to hundreds), so work items are
-// per WARP: <= 32 points of one particle, one per lane, against the particle's
-// <= ~1k candidates read through L1 (broadcast loads).  Same filter and
-// certification as nn_filter_kernel with a single split: the window members
-// are listed on the spot and decided in FP64 at once.
+// Colliding points are few per particle (tens to hundreds), so a work item is
+// <= kRevWQ points of one particle against its <= ~1k candidates, and the
+// whole CTA works on one item: the surface is staged once into shared memory
+// (cp.async, reused by the particle's next item), each warp scans every
+// kRevWarps-th subtile for all the item's points (two per lane), and the
+// per-warp top-3 subtile minima are merged in (value, subtile) order -- the
+// same top-3 a single sequential scan keeps.  Same filter and certification
+// as nn_filter_kernel with a single split: the window members are listed on
+// the spot and decided in FP64 at once.
 // ---------------------------------------------------------------------------
 constexpr int kRevWarps = 4;
 constexpr int kRevThreads = 32 * kRevWarps;
-constexpr int kRevMaxC = 1024;  // candidates staged per warp (16 KB); larger surfaces read L1
-constexpr int kRevSmem = kRevWarps * kRevMaxC * 16;
+constexpr int kRevMaxC = 1024;  // candidates staged per CTA (16 KB); larger surfaces are read through L1
+struct RevTop {
+  float b1, b2, b3;
+  int s1, s2;
+};
+constexpr int kRevSmem = kRevMaxC * 16 + kRevWarps * kRevWQ * static_cast<int>(sizeof(RevTop));
+static int g_rev_blocks_per_sm = 1;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// (v, s) into a top-3 ordered by (value, subtile).
+__device__ __forceinline__ void top3_insert(float& b1, int& s1, float& b2, int& s2, float& b3, float v, int s) {
+  if (v < b1 || (v == b1 && s < s1)) {
+    b3 = b2;
+    b2 = b1;
+    s2 = s1;
+    b1 = v;
+    s1 = s;
+  } else if (v < b2 || (v == b2 && s < s2)) {
+    b3 = b2;
+    b2 = v;
+    s2 = s;
+  } else {
+    b3 = fminf(b3, v);
+  }
+}
+
 __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevState S, NnPlan plan) {
   pdl_enter();
   extern __shared__ __align__(16) float4 rev_smem[];
-  const int lane = threadIdx.x & 31;
-  float4* stage = rev_smem + (threadIdx.x >> 5) * kRevMaxC;
+  float4* stage = rev_smem;
+  RevTop* tops = reinterpret_cast<RevTop*>(rev_smem + kRevMaxC);
+  const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
   const int n_items = S.item_off[1][P.J];
-  // Items cost about the same (<= 32 points x one contact surface): a static
-  // warp-stride assignment, no shared counter for thousands of warps to hit.
-  // The item's candidates are staged into the warp's shared slice with one
-  // round of cp.async (every load in flight at once) before the scan.
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < n_items; it += nwarps) {
+  // Contiguous item ranges per CTA: a particle's items are consecutive, so
+  // its surface is staged once.
+  const int i0 = static_cast<int>(static_cast<long long>(blockIdx.x) * n_items / gridDim.x);
+  const int i1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n_items / gridDim.x);
+  const float4* staged_c = nullptr;
+  constexpr int QR = kRevWQ / 32;
+  for (int it = i0; it < i1; ++it) {
     const NnItem w = S.items[1][it];
     const int ncp = round_up(w.nc, kSub);
     const bool staged = ncp <= kRevMaxC;
-    __syncwarp();  // the previous item's rescans are done with the slice
-    if (staged) {
-      for (int c = lane; c < ncp; c += 32) cp_async16(stage + c, w.c + c);
+    __syncthreads();  // the previous item's epilogue is done with the stage and the tops
+    if (staged && w.c != staged_c) {
+      for (int c = tid; c < ncp; c += kRevThreads) cp_async16(stage + c, w.c + c);
       cp_async_wait_all();
-      __syncwarp();
+      __syncthreads();
+      staged_c = w.c;
     }
     const float4* cand = staged ? stage : w.c;
-    if (lane == 0) {
+    if (tid == 0) {
       const unsigned long long pairs = static_cast<unsigned long long>(w.nq) * w.nc;
       atomicAdd(S.stats + 2, static_cast<unsigned long long>(w.nq));
       atomicAdd(S.stats + 4, pairs);
       atomicAdd(S.iter_stats + 4 * plan.iter + 1, pairs);
       atomicAdd(S.iter_stats + 4 * plan.iter + 3, static_cast<unsigned long long>(w.nq));
     }
-    // Two queries per lane (lane and lane + 32): the staged candidates are read
-    // once for both, and four packed FMA chains per step keep the lane busy.
-    constexpr int QR = kRevWQ / 32;
     float4 q[QR];
-    bool has[QR];
 #pragma unroll
-    for (int r = 0; r < QR; ++r) {
-      has[r] = lane + 32 * r < w.nq;
-      q[r] = has[r] ? w.q[lane + 32 * r] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int r = 0; r < QR; ++r)
+      q[r] = lane + 32 * r < w.nq ? w.q[lane + 32 * r] : make_float4(0.f, 0.f, 0.f, 0.f);
     const int nsub = ceil_div(w.nc, kSub);  // candidate rows are +inf padded to the subtile
     float b1[QR], b2[QR], b3[QR];
     int s1[QR], s2[QR];
@@ -934,7 +958,7 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
       qz2[r] = pk2(q[r].z, q[r].z);
     }
     const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
-    for (int sub = 0; sub < nsub; ++sub) {
+    for (int sub = wi; sub < nsub; sub += kRevWarps) {
       float tm[QR];
       if (staged) {
         // Candidates are pair-interleaved (pc_index): per 4 candidates four
@@ -983,45 +1007,57 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
         b1[r] = lt1 ? tm[r] : b1[r];
       }
     }
-    for (int r = 0; r < QR; ++r) {
-      if (!has[r]) continue;
-      const int qlocal = w.q_first + lane + 32 * r;
-      int* slot = S.res_rev + static_cast<int64_t>(w.owner) * P.n_scene + qlocal;
-      if (plan.fp64_mode) {
-        push_refine(S, 1, w.owner, qlocal, 0, plan.iter);
-        continue;
-      }
-      const float thr = __fadd_ru(b1[r], q[r].w);
-      bool ovf = b3[r] <= thr;
-      int pos[kWinCap];
-      int np = 0, pmin = -1;
-      const int nscan = b2[r] <= thr ? 2 : 1;
-      for (int sc = 0; sc < nscan; ++sc) {
-        const int sid = sc == 0 ? s1[r] : s2[r];
-        // Member bitmask in one pass, then the members in increasing position.
-        unsigned mask = 0;
+#pragma unroll
+    for (int r = 0; r < QR; ++r) tops[wi * kRevWQ + lane + 32 * r] = RevTop{b1[r], b2[r], b3[r], s1[r], s2[r]};
+    __syncthreads();
+    if (tid >= w.nq) continue;
+    // Epilogue: one thread per point merges the warps' top-3 lists and
+    // certifies or decides the window.
+    const int qlocal = w.q_first + tid;
+    if (plan.fp64_mode) {
+      push_refine(S, 1, w.owner, qlocal, 0, plan.iter);
+      continue;
+    }
+    RevTop t = tops[tid];
+#pragma unroll
+    for (int k = 1; k < kRevWarps; ++k) {
+      const RevTop o = tops[k * kRevWQ + tid];
+      top3_insert(t.b1, t.s1, t.b2, t.s2, t.b3, o.b1, o.s1);
+      top3_insert(t.b1, t.s1, t.b2, t.s2, t.b3, o.b2, o.s2);
+      t.b3 = fminf(t.b3, o.b3);
+    }
+    const float4 qq = w.q[tid];
+    int* slot = S.res_rev + static_cast<int64_t>(w.owner) * P.n_scene + qlocal;
+    const float thr = __fadd_ru(t.b1, qq.w);
+    bool ovf = t.b3 <= thr;
+    int pos[kWinCap];
+    int np = 0, pmin = -1;
+    const int nscan = t.b2 <= thr ? 2 : 1;
+    for (int sc = 0; sc < nscan; ++sc) {
+      const int sid = sc == 0 ? t.s1 : t.s2;
+      // Member bitmask in one pass, then the members in increasing position.
+      unsigned mask = 0;
 #pragma unroll 8
-        for (int c = 0; c < kSub; ++c)
-          mask |= (d32(q[r].x, q[r].y, q[r].z, pc_get(cand, sid * kSub + c)) <= thr ? 1u : 0u) << c;
-        while (mask) {
-          const int c = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const float d = d32(q[r].x, q[r].y, q[r].z, pc_get(cand, sid * kSub + c));
-          const int p = sid * kSub + c;
-          if (np < kWinCap) pos[np] = p;
-          ++np;
-          if (d == b1[r] && (pmin < 0 || p < pmin)) pmin = p;
-        }
+      for (int c = 0; c < kSub; ++c)
+        mask |= (d32(qq.x, qq.y, qq.z, pc_get(cand, sid * kSub + c)) <= thr ? 1u : 0u) << c;
+      while (mask) {
+        const int c = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float d = d32(qq.x, qq.y, qq.z, pc_get(cand, sid * kSub + c));
+        const int p = sid * kSub + c;
+        if (np < kWinCap) pos[np] = p;
+        ++np;
+        if (d == t.b1 && (pmin < 0 || p < pmin)) pmin = p;
       }
-      ovf = ovf || np > kWinCap;
-      if (ovf) {
-        push_refine(S, 1, w.owner, qlocal, 1, plan.iter);
-      } else if (np == 1) {
-        *slot = pmin;  // certified
-      } else {
-        const NnGeom g = nn_geom(P, S, plan, 1, w.owner, qlocal);
-        *slot = nn_decide(g, pos, np, false, S.stats);
-      }
+    }
+    ovf = ovf || np > kWinCap;
+    if (ovf) {
+      push_refine(S, 1, w.owner, qlocal, 1, plan.iter);
+    } else if (np == 1) {
+      *slot = pmin;  // certified
+    } else {
+      const NnGeom g = nn_geom(P, S, plan, 1, w.owner, qlocal);
+      *slot = nn_decide(g, pos, np, false, S.stats);
     }
   }
 }
@@ -1089,6 +1125,8 @@ int nn_smem_bytes() { return kNnSmem; }
 void nn_set_attrs() {
   cudaFuncSetAttribute(nn_filter_kernel<kFwdQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
   cudaFuncSetAttribute(nn_rev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRevSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_rev_blocks_per_sm, nn_rev_kernel, kRevThreads, kRevSmem);
+  g_rev_blocks_per_sm = std::max(1, g_rev_blocks_per_sm);
 }
 
 int nn_blocks_per_sm() {
@@ -1105,7 +1143,9 @@ int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, in
   ++n;
   if (ev_end) cudaEventRecord(ev_end, st);
   if (plan.kind == 0) {
-    pdl_launch(nn_rev_kernel, dim3(3 * refine_grid / 2), dim3(kRevThreads), kRevSmem, st, P, S, plan);  // 3 CTAs per SM
+    // refine_grid is two CTAs per SM; the reverse grid fills every SM.
+    pdl_launch(nn_rev_kernel, dim3(refine_grid / 2 * g_rev_blocks_per_sm), dim3(kRevThreads), kRevSmem, st, P, S,
+               plan);
     ++n;
   }
   if (plan.nchunks > 1) {
