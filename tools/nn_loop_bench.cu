@@ -26,7 +26,7 @@ constexpr int kSub = 32, kCand = 2048;
 // MODE 0: hot loop only, 1: + top-3 per subtile, 2: + top-3 with the queries
 // held as pre-packed register pairs (no .F32 broadcast operand), 3: scalar
 // FFMA form + top-3.  Queries come from global memory (no constant folding).
-template <int MODE, int Q = 8, int MINB = 4, int UNR = 2>
+template <int MODE, int Q = 8, int MINB = 4, int UNR = 2, int TRACK = 32, bool NET = false>
 __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, const float4* qin, float* out, int reps) {
   __shared__ float4 tile[kCand];
   for (int i = threadIdx.x; i < kCand; i += blockDim.x) tile[i] = cand[i];
@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, con
     s12[k] = 0;
   }
   for (int r = 0; r < reps; ++r) {
-    for (int sub = 0; sub < kCand / kSub; ++sub) {
-      const float4* sp = tile + sub * kSub;
+    for (int sub = 0; sub < kCand / TRACK; ++sub) {
+      const float4* sp = tile + sub * TRACK;
       float tm[Q];
 #pragma unroll
       for (int k = 0; k < Q; ++k) tm[k] = INFINITY;
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, con
         }
       } else {
 #pragma unroll UNR
-      for (int c = 0; c < kSub; c += 4) {
+      for (int c = 0; c < TRACK; c += 4) {
         const float4 a0 = sp[c], c0 = sp[c + 1];
         const float4 a1 = sp[c + 2], c1 = sp[c + 3];
         const f32x2 x0 = pk2(a0.x, a0.y), y0 = pk2(a0.z, a0.w), z0 = pk2(c0.x, c0.y), w0 = pk2(c0.z, c0.w);
@@ -120,6 +120,14 @@ __global__ void __launch_bounds__(128, MINB) loop_kernel(const float4* cand, con
       for (int k = 0; k < Q; ++k) {
         if (MODE == 0) {
           b1[k] = fminf(b1[k], tm[k]);
+        } else if (NET) {
+          const bool lt1 = tm[k] < b1[k];
+          const bool lt2 = tm[k] < b2[k];
+          b3[k] = fminf(b3[k], fmaxf(b2[k], tm[k]));
+          b2[k] = fminf(b2[k], fmaxf(b1[k], tm[k]));
+          b1[k] = fminf(b1[k], tm[k]);
+          const int s1 = s12[k] & 0xffff;
+          s12[k] = (lt1 ? sid : s1) | ((lt1 ? s1 : (lt2 ? sid : (s12[k] >> 16))) << 16);
         } else {
           const bool lt1 = tm[k] < b1[k];
           const bool lt2 = tm[k] < b2[k];
@@ -181,12 +189,12 @@ int main() {
       printf("hot loop + top-3, Q=%d, %d CTAs/SM: %.2f pairs/clk/SM  FMA pipe %.2f\n", q, per_sm, per_clk_sm,
              per_clk_sm * 3 / 128);
     };
-    run(loop_kernel<1, 8, 4, 1>, 8, 4);
-    run(loop_kernel<1, 8, 4, 4>, 8, 4);
-    run(loop_kernel<1, 8, 4, 8>, 8, 4);
-    run(loop_kernel<0, 8, 4, 4>, 8, 4);
-    run(loop_kernel<0, 8, 4, 8>, 8, 4);
-    run(loop_kernel<1, 4, 8>, 4, 8);
+    run(loop_kernel<1, 8, 4, 8>, 8, 4);                 // select top-3, full subtile unroll
+    run(loop_kernel<1, 8, 4, 8, 32, true>, 8, 4);       // min/max-network top-3 (the kernel's)
+    run(loop_kernel<1, 8, 4, 16, 64, true>, 8, 4);      // top-3 per 64 candidates
+    run(loop_kernel<0, 8, 4, 8>, 8, 4);                 // no top-3
+    run(loop_kernel<1, 8, 3, 8, 32, true>, 8, 3);
+    run(loop_kernel<1, 12, 3, 8, 32, true>, 12, 3);
     run(loop_kernel<1, 4, 6>, 4, 6);
     run(loop_kernel<1, 12, 2>, 12, 2);
     run(loop_kernel<1, 12, 3>, 12, 3);

@@ -5,7 +5,7 @@ set -x
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/m2_smoke.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -rs --durations=15 > gpurun_out/m2_gputest.log 2>&1
 timeout 900 python bench.py > gpurun_out/m2_bench_cfg4.log 2>&1
-timeout 600 python bench.py --workload cfg2 > gpurun_out/m2_bench_cfg2.log 2>&1
+timeout 900 python bench.py --workload cfg2 --cpu-1worker > gpurun_out/m2_bench_cfg2.log 2>&1
 timeout 600 python bench.py --workload cfg3 > gpurun_out/m2_bench_cfg3.log 2>&1
 timeout 900 python bench.py --workload cfg5 > gpurun_out/m2_bench_cfg5.log 2>&1
 timeout 600 python bench.py --workload reg > gpurun_out/m2_bench_reg.log 2>&1
