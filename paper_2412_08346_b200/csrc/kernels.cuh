@@ -246,6 +246,9 @@ int nn_blocks_per_sm();
 // Launches the forward/final list (and the reverse list when kind == 0),
 // the merge (nchunks > 1) and the FP64 refine.  Returns the launch count.
 int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, int refine_grid, cudaStream_t st,
-              cudaEvent_t ev_begin, cudaEvent_t ev_end);
+              cudaEvent_t ev_begin, cudaEvent_t ev_end, cudaEvent_t rev_done = nullptr);
+// The reverse match alone (forked beside the minibatch draw and the forward
+// filter; launch_nn then joins it through rev_done).
+void launch_nn_rev(const DevProblem& P, DevState& S, const NnPlan& plan, int refine_grid, cudaStream_t st);
 
 }  // namespace asicp

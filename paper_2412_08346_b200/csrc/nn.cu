@@ -1135,14 +1135,19 @@ int nn_blocks_per_sm() {
   return n;
 }
 
+void launch_nn_rev(const DevProblem& P, DevState& S, const NnPlan& plan, int refine_grid, cudaStream_t st) {
+  pdl_launch(nn_rev_kernel, dim3(refine_grid / 2 * g_rev_blocks_per_sm), dim3(kRevThreads), kRevSmem, st, P, S,
+             plan);
+}
+
 int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, int refine_grid, cudaStream_t st,
-              cudaEvent_t ev_begin, cudaEvent_t ev_end) {
+              cudaEvent_t ev_begin, cudaEvent_t ev_end, cudaEvent_t rev_done) {
   int n = 0;
   if (ev_begin) cudaEventRecord(ev_begin, st);
   pdl_launch(nn_filter_kernel<kFwdQ>, dim3(grid), dim3(kNnThreads), kNnSmem, st, P, S, plan, 0);
   ++n;
   if (ev_end) cudaEventRecord(ev_end, st);
-  if (plan.kind == 0) {
+  if (!rev_done && plan.kind == 0) {
     // refine_grid is two CTAs per SM; the reverse grid fills every SM.
     pdl_launch(nn_rev_kernel, dim3(refine_grid / 2 * g_rev_blocks_per_sm), dim3(kRevThreads), kRevSmem, st, P, S,
                plan);
@@ -1153,6 +1158,9 @@ int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, in
     pdl_launch(nn_merge_kernel, dim3(mg), dim3(128), 0, st, P, S, plan);
     ++n;
   }
+  // A reverse match forked onto a side stream (launch_nn_rev) joins before
+  // the refine, which serves both kinds' refine lists.
+  if (rev_done) cudaStreamWaitEvent(st, rev_done, 0);
   pdl_launch(nn_refine_kernel, dim3(refine_grid), dim3(256), 0, st, P, S, plan);
   return n + 1;
 }

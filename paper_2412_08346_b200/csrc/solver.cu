@@ -169,6 +169,12 @@ struct asicp_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t side = nullptr;  // forked work inside an iteration (median bandwidth)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t rev_side = nullptr;  // the reverse match beside the minibatch draw / forward filter
+  cudaEvent_t ev_rev_fork = nullptr, ev_rev_join = nullptr;
+  bool fork_rev = [] {  // ASICP_FORK_REV=0: the reverse match in line
+    const char* e = std::getenv("ASICP_FORK_REV");
+    return !(e && e[0] == '0');
+  }();
   // Profile mode (ASICP_OPT_PROFILE, eager launches): per-stage event pairs.
   enum Stage { kStNn = 0, kStCollide, kStMinibatch, kStCost, kStSvgd, kStages };
   struct ProfEvent {
@@ -243,6 +249,9 @@ struct asicp_ctx {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    if (ev_rev_fork) cudaEventDestroy(ev_rev_fork);
+    if (ev_rev_join) cudaEventDestroy(ev_rev_join);
+    if (rev_side) cudaStreamDestroy(rev_side);
     Buf* all[] = {&obj64, &obj_meta, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
@@ -866,6 +875,15 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
 void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
   cudaStream_t st = c->stream;
   launch_nn_plan(c->P, c->S, plan, st);
+  // The reverse match (colliding particles) needs neither the minibatch pools
+  // nor the forward filter: fork it so it fills the SMs the draw leaves idle.
+  const bool fork_rev = plan.kind == 0 && c->fork_rev && !c->profile;
+  if (fork_rev) {
+    CUDA_OK(cudaEventRecord(c->ev_rev_fork, st));
+    CUDA_OK(cudaStreamWaitEvent(c->rev_side, c->ev_rev_fork, 0));
+    launch_nn_rev(c->P, c->S, plan, 2 * c->num_sms, c->rev_side);
+    CUDA_OK(cudaEventRecord(c->ev_rev_join, c->rev_side));
+  }
   int mb_launches = 0;
   if (minibatch_m > 0) {
     StageTimer t(c, asicp_ctx::kStMinibatch, capture);
@@ -877,8 +895,9 @@ void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture)
     CUDA_OK(cudaEventCreate(&e.b));
     c->prof_events.push_back(e);
   }
-  const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.a, e.b);
-  c->launches += 1 + n + mb_launches;  // fill (plan fused) + filter(s), merge, refine + minibatch
+  const int n = launch_nn(c->P, c->S, plan, c->nn_grid, 2 * c->num_sms, st, e.a, e.b,
+                          fork_rev ? c->ev_rev_join : nullptr);
+  c->launches += 1 + n + mb_launches + (fork_rev ? 1 : 0);  // fill (plan fused) + filter(s), merge, refine + minibatch
 }
 
 // The whole optimize_grasp as a kernel sequence on c->stream.
@@ -1213,6 +1232,9 @@ asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->rev_side, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_rev_fork, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_rev_join, cudaEventDisableTiming));
     c->nn_grid = c->num_sms * std::max(1, nn_blocks_per_sm());
   });
   if (rc != ASICP_OK) {
