@@ -23,6 +23,7 @@ struct DevProblem {
   const double* obj64;      // R, n_obj x 3
   const float4* obj_cand;   // R as FP32 NN candidates (-2b, |b|^2), b = r - center
   const float4* obj_cand4;  // the same candidates one float4 per point (minibatch pool gathers)
+  const float4* obj_tc;     // their TF32 splits, 3 x float4 per point (tensor-core filter, nn.cu)
   const double* scene64;    // C, n_scene x 3
   const float4* scene32;    // C rounded to FP32 (x, y, z, |p|_1 rounded up), for the collision pre-test
   // Collision clusters (collide.cu): the scene sorted along a Morton curve and
@@ -138,6 +139,7 @@ struct DevState {
   int* item_counter;   // 2 ints
   int* nn_dyn;         // device-chosen forward split: [0] splits, [1] forward items
   NnPartial* partials; // padded surface rows x max chunks
+  float4* tc_top;      // tensor-core filter: per (query, split) top-3 subtile minima (b1, b2, b3, s1 | s2 << 16)
   int2* amb_pool;      // ambiguous-window member lists (kWinCap entries per block)
   int* amb_n;          // members per block (> kWinCap: overflow)
   int* amb_count;      // blocks allocated in the current NN round
@@ -165,6 +167,7 @@ struct NnPlan {
   int fp64_mode; // resolve every query by FP64 brute force (validation mode)
   int max_ns;    // largest contact surface (merge grid)
   int iter;      // iteration index (diagnostic counters)
+  int use_tc;    // forward / final filter on the tensor cores (nn_tc_kernel)
 };
 
 // Per-device kernel attributes (opt-in shared memory), set for every context.
@@ -182,6 +185,7 @@ void launch_grid_bounds(Grid* grids, int n_grids, const float* values, float* co
 // Object cloud -> centroid, B_obj and the FP32 NN candidates (-2b, |b|^2),
 // b = r - centroid: pair-interleaved (cand, n_pad rows, +inf padded) and plain
 // (cand4).  meta = [centroid x, y, z, B_obj].
+void launch_obj_tc(const float4* cand4, int n, float4* tc, cudaStream_t st);  // nn.cu
 void launch_object_prepare(const double* obj64, int n, int n_pad, double* meta, float4* cand, float4* cand4,
                            cudaStream_t st);
 // sdf_build.cu: graspmatch::build_sdf on the device (returns ASICP_OK or

@@ -62,6 +62,16 @@ __device__ __forceinline__ void fwd_split(int T, const NnPlan& plan, int* nch_ou
   // over every CTA slot plus the last item's length.
   const int grid = max(1, plan.target_items / 4);
   int nch = nmax;
+  if (plan.use_tc) {
+    // Tensor-core filter: every item is 8 units of 128 queries on one CTA
+    // per SM; split only as far as needed for about target_items / 2 units
+    // (each unit boundary costs a pipeline refill).
+    nch = max(1, min(nmax, ceil_div(plan.target_items / 2, 8 * max(T, 1))));
+    const int chunk = round_up(ceil_div(plan.m, nch), kNnTile);
+    *chunk_out = chunk;
+    *nch_out = ceil_div(plan.m, chunk);
+    return;
+  }
   long long best = -1;
   for (int s = 1; s <= nmax; ++s) {
     const int chunk = round_up(ceil_div(plan.m, s), kNnTile);
@@ -1063,6 +1073,526 @@ __global__ void __launch_bounds__(kRevThreads) nn_rev_kernel(DevProblem P, DevSt
 }
 
 // ---------------------------------------------------------------------------
+// Forward / final filter on the tensor cores (ASICP_NN_TC=1).
+//
+// The distances of a (128 queries) x (256 candidates) tile are one K = 16
+// tcgen05 MMA pair (kind::tf32, FP32 accumulators in TMEM) with a three-term
+// TF32 split, hi*hi + hi*lo + lo*hi, which carries ~FP32 accuracy:
+//   A row (query)     [qh 1 | qh 1 | ql 0 | 0]         (qh, ql: 3 floats each)
+//   B row (candidate) [Bh nh | Bl nl | Bh 0 | 0]       (B = -2b, n = |b|^2)
+// h = TF32-rounded (cvt.rna), l = the exact FP32 remainder; products of TF32
+// operands are exact in FP32, so the error is the accumulation (<= 18 FP32
+// roundings of partial sums bounded by S) plus the truncation of the l
+// operands and the dropped l*l term: |d_tc - d| <= kTcErr * S with
+// S = |b|^2 + 2 |q| |b| (measured <= 6.5 u S, tools/tc_nn_bench.cu; kTcErr =
+// 64 u).
+//
+// nn_tc_kernel (one CTA per SM, warp-specialised): warps 0-1 gather the B
+// tiles (candidate rows of the object's TF32 split, P.obj_tc, through the
+// minibatch pool map) with cp.async into a 6-stage ring and build the A tile
+// of each 128-query unit; warp 2 issues the MMAs into a double-buffered
+// 2 x 256-column accumulator; warps 3-10 drain it (tcgen05.ld, one query per
+// lane, two warps per lane quarter splitting the columns) into a running
+// top-3 of 32-candidate subtile minima per query and split, written to
+// S.tc_top.  nn_tc_window_kernel then certifies each (query, split) exactly
+// as the FFMA2 filter's sub-chunk epilogue does, from the FP32 candidates:
+// every candidate of the split's d32 window {d32 <= b1_32 + mg} has
+// d_tc <= b1_tc + mg + 2 Et, so the subtiles s1 (and s2 when b2_tc is within
+// that bound) hold the whole window and the split's d32 minimum; b3_tc within
+// the bound sends the query to the full FP64 rescan.
+// ---------------------------------------------------------------------------
+constexpr int kTcM = 128, kTcN = 256, kTcK = 16;
+constexpr int kTcStages = 6;
+constexpr int kTcABytes = kTcM * kTcK * 4;
+constexpr int kTcBBytes = kTcN * kTcK * 4;
+constexpr int kTcProdWarps = 2, kTcEpiWarps = 8;  // + one MMA warp and one A-tile warp
+constexpr int kTcMmaWarp = kTcProdWarps, kTcAWarp = kTcProdWarps + 1;
+constexpr int kTcThreads = 32 * (kTcProdWarps + 2 + kTcEpiWarps);
+constexpr int kTcBars = 2 * kTcStages + 2 + 2 + 2 + 2;  // full, empty, acc full/empty, A full/empty
+// Dynamic shared memory: 1 KB alignment slack, A x 2, B ring, barriers; sized
+// so that one CTA fits per SM (the kernel owns all 512 TMEM columns).
+constexpr int kTcSmem = 1024 + 2 * kTcABytes + kTcStages * kTcBBytes + 256;
+constexpr int kTcUnitsPerItem = kNnQB / kTcM;
+constexpr float kTcErr = 3.8147e-06f;  // 64 u, u = 2^-24
+constexpr uint32_t kTcIdesc =
+    (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kTcN >> 3) << 17) | (static_cast<uint32_t>(kTcM >> 4) << 24);
+
+// Float offset of (row r, k) in a K-major SWIZZLE_NONE tile: core matrices of
+// 8 rows x 16 B, the next 4-float k chunk at +128 B (LBO), the next 8 rows at
+// +512 B (SBO).
+__host__ __device__ __forceinline__ int tc_off(int r, int k) {
+  return (((r >> 3) * 4 + (k >> 2)) * 8 + (r & 7)) * 4 + (k & 3);
+}
+__device__ __forceinline__ uint64_t tc_sdesc(uint32_t saddr) {
+  return ((saddr >> 4) & 0x3fffu) | (static_cast<uint64_t>(128 >> 4) << 16) | (static_cast<uint64_t>(512 >> 4) << 32) |
+         (static_cast<uint64_t>(1) << 46);
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(kTcIdesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16_tc(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+#define TC_LD32(taddr, v)                                                                                        \
+  asm volatile(                                                                                                  \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"  \
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                              \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),  \
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),       \
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),      \
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                    \
+      : "r"(taddr))
+
+// Minimum of 32 accumulator values: a tree of 3-input mins (FMNMX3).
+__device__ __forceinline__ float tc_min32(const uint32_t* x) {
+  float m[11];
+#pragma unroll
+  for (int i = 0; i < 10; ++i)
+    m[i] = fminf(fminf(__uint_as_float(x[3 * i]), __uint_as_float(x[3 * i + 1])), __uint_as_float(x[3 * i + 2]));
+  m[10] = fminf(__uint_as_float(x[30]), __uint_as_float(x[31]));
+  const float a0 = fminf(fminf(m[0], m[1]), m[2]), a1 = fminf(fminf(m[3], m[4]), m[5]);
+  const float a2 = fminf(fminf(m[6], m[7]), m[8]), a3 = fminf(m[9], m[10]);
+  return fminf(fminf(a0, a1), fminf(a2, a3));
+}
+
+// (v, s, mask) into a top-3 ordered by (value, subtile).
+__device__ __forceinline__ void tc_top3_insert(float& b1, int& s1, unsigned& m1, float& b2, int& s2, unsigned& m2,
+                                               float& b3, float v, int s, unsigned m) {
+  if (v < b1 || (v == b1 && s < s1)) {
+    b3 = b2;
+    b2 = b1;
+    s2 = s1;
+    m2 = m1;
+    b1 = v;
+    s1 = s;
+    m1 = m;
+  } else if (v < b2 || (v == b2 && s < s2)) {
+    b3 = b2;
+    b2 = v;
+    s2 = s;
+    m2 = m;
+  } else {
+    b3 = fminf(b3, v);
+  }
+}
+
+// The object's candidates as TF32 splits, 3 x 16 B per point:
+// (Bh, nh), (Bl, nl), (Bh, 0) with B = -2b, n = |b|^2 from obj_cand4.
+__global__ void obj_tc_kernel(const float4* cand4, int n, float4* tc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 v = cand4[i];
+  const float hx = tf32_rna(v.x), hy = tf32_rna(v.y), hz = tf32_rna(v.z), hn = tf32_rna(v.w);
+  tc[3 * i] = make_float4(hx, hy, hz, hn);
+  tc[3 * i + 1] = make_float4(v.x - hx, v.y - hy, v.z - hz, v.w - hn);
+  tc[3 * i + 2] = make_float4(hx, hy, hz, 0.0f);
+}
+
+void launch_obj_tc(const float4* cand4, int n, float4* tc, cudaStream_t st) {
+  obj_tc_kernel<<<ceil_div(n, 256), 256, 0, st>>>(cand4, n, tc);
+}
+
+// The TC error bound of a query, Et = kTcErr (|b|^2 + 2 |q| |b|) over the
+// object (B_obj = Bo), and its selection slack mg + 2 Et (see nn_tc_kernel),
+// rounded up.
+__device__ __forceinline__ float tc_et(float4 q, float Bo) {
+  const float qa = __fsqrt_ru(__fmaf_ru(q.x, q.x, __fmaf_ru(q.y, q.y, __fmul_ru(q.z, q.z))));
+  return __fmul_ru(kTcErr, __fmaf_ru(__fmul_ru(2.0f, qa), Bo, __fmul_ru(Bo, Bo)));
+}
+__device__ __forceinline__ float tc_slack(float4 q, float Bo) { return __fadd_ru(q.w, __fmul_ru(2.0f, tc_et(q, Bo))); }
+// Candidates of a subtile whose TC value is within the slack of its minimum.
+__device__ __forceinline__ unsigned tc_mask(const uint32_t* v, float lim) {
+  unsigned m = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m |= (__uint_as_float(v[i]) <= lim ? 1u : 0u) << i;
+  return m;
+}
+
+struct TcUnit {
+  int item, qt, nq;  // nq = 0: nothing to do
+};
+__device__ __forceinline__ TcUnit tc_unit(const DevState& S, int u) {
+  TcUnit r;
+  r.item = u / kTcUnitsPerItem;
+  r.qt = u % kTcUnitsPerItem;
+  r.nq = max(0, min(kTcM, S.items[0][r.item].nq - r.qt * kTcM));
+  return r;
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_constant__ DevProblem P,
+                                                              const __grid_constant__ DevState S,
+                                                              const __grid_constant__ NnPlan plan) {
+  pdl_enter();
+  extern __shared__ __align__(1024) unsigned char tc_raw[];
+  unsigned char* sm =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  float* sA = reinterpret_cast<float*>(sm);                   // 2 A tiles
+  float* sB = reinterpret_cast<float*>(sm + 2 * kTcABytes);   // B ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + 2 * kTcABytes + kTcStages * kTcBBytes);
+  uint64_t *full = bars, *empty = bars + kTcStages, *accf = bars + 2 * kTcStages, *acce = accf + 2, *afull = acce + 2,
+           *aempty = afull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kTcBars);
+  __shared__ float xb[3][kTcM];
+  __shared__ int xs[kTcM];
+  __shared__ unsigned xm[2][kTcM];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // Zero both A tiles and every B stage once: the k = 12..15 chunk is never
+  // written again and must hold zeros (0 * garbage could be NaN).
+  for (int i = tid; i < (2 * kTcABytes + kTcStages * kTcBBytes) / 16; i += kTcThreads)
+    reinterpret_cast<float4*>(sm)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(full + s, 32 * kTcProdWarps);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(accf + b, 1);
+      mbar_init(acce + b, 32 * kTcEpiWarps);
+      mbar_init(afull + b, 32);
+      mbar_init(aempty + b, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == kTcMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+  const int n_units = S.nn_dyn[1] * kTcUnitsPerItem;
+  const uint32_t sA_s = smem_u32(sA), sB_s = smem_u32(sB);
+  const float Bo = __double2float_ru(P.obj_meta[3]);
+
+  if (warp < kTcProdWarps) {
+    // B producer: the B tiles of every unit (cp.async gathers whose
+    // completion arrives on the stage barrier).
+    const int ptid = tid;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const TcUnit U = tc_unit(S, u);
+      if (U.nq == 0) continue;
+      const NnItem w = S.items[0][U.item];
+      const int* map = plan.pooled ? S.pool_idx + static_cast<int64_t>(w.owner) * P.n_obj_pad + w.c_base : nullptr;
+      const int ntiles = ceil_div(w.nc, kTcN);
+      // Candidate rows of this thread for tile t, loaded one tile ahead.
+      constexpr int kPer = kTcN / (32 * kTcProdWarps);
+      int rows[kPer], rows_next[kPer];
+      auto load_rows = [&](int t, int* out) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int p = t * kTcN + ptid + i * 32 * kTcProdWarps;
+          out[i] = p < w.nc ? (map ? __ldg(map + p) : w.c_base + p) : -1;
+        }
+      };
+      load_rows(0, rows_next);
+      for (int t = 0; t < ntiles; ++t) {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) rows[i] = rows_next[i];
+        if (t + 1 < ntiles) load_rows(t + 1, rows_next);
+        mbar_wait(empty + s, ph ^ 1);
+        const uint32_t bs = sB_s + static_cast<uint32_t>(s) * kTcBBytes;
+        float* bg = sB + s * (kTcBBytes / 4);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+          const int cnd = ptid + i * 32 * kTcProdWarps;
+          if (rows[i] >= 0) {
+            const float4* src = P.obj_tc + 3 * static_cast<int64_t>(rows[i]);
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+              cp_async16_tc(bs + static_cast<uint32_t>(tc_off(cnd, 4 * ch)) * 4u, src + ch);
+          } else {
+            // Padding rows: d = 1e30 (A's k = 3 entry is 1), never a minimum.
+            *reinterpret_cast<float4*>(bg + tc_off(cnd, 0)) = make_float4(0.f, 0.f, 0.f, 1e30f);
+            *reinterpret_cast<float4*>(bg + tc_off(cnd, 4)) = make_float4(0.f, 0.f, 0.f, 0.f);
+            *reinterpret_cast<float4*>(bg + tc_off(cnd, 8)) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        // The stage barrier counts this thread once its copies have landed
+        // (no wait here); the MMA thread fences the generic-proxy writes.
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(full + s)) : "memory");
+        if (++s == kTcStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kTcAWarp) {
+    // A producer: the TF32 split of each unit's 128 queries, one unit ahead
+    // of the MMAs (double-buffered), so unit boundaries do not stall the B
+    // stream.
+    int n = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const TcUnit U = tc_unit(S, u);
+      if (U.nq == 0) continue;
+      const float4* qs = S.items[0][U.item].q + U.qt * kTcM;
+      float4 qv[kTcM / 32];
+#pragma unroll
+      for (int i = 0; i < kTcM / 32; ++i) {
+        const int r = lane + 32 * i;
+        qv[i] = r < U.nq ? qs[r] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      const int ua = n & 1;
+      mbar_wait(aempty + ua, ((n >> 1) & 1) ^ 1);
+      float* a = sA + ua * (kTcABytes / 4);
+#pragma unroll
+      for (int i = 0; i < kTcM / 32; ++i) {
+        const int r = lane + 32 * i;
+        const float4 q = qv[i];
+        const float hx = tf32_rna(q.x), hy = tf32_rna(q.y), hz = tf32_rna(q.z);
+        *reinterpret_cast<float4*>(a + tc_off(r, 0)) = make_float4(hx, hy, hz, 1.0f);
+        *reinterpret_cast<float4*>(a + tc_off(r, 4)) = make_float4(hx, hy, hz, 1.0f);
+        *reinterpret_cast<float4*>(a + tc_off(r, 8)) = make_float4(q.x - hx, q.y - hy, q.z - hz, 0.0f);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(afull + ua);
+      ++n;
+    }
+  } else if (warp == kTcMmaWarp) {
+    // MMA issuer (one lane).
+    if (lane == 0) {
+      int s = 0, b = 0;
+      uint32_t ph = 0, aph = 0;
+      int n = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const TcUnit U = tc_unit(S, u);
+        if (U.nq == 0) continue;
+        const int nc = S.items[0][U.item].nc;
+        const int ua = n & 1;
+        mbar_wait(afull + ua, (n >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t as = sA_s + static_cast<uint32_t>(ua) * kTcABytes;
+        const int ntiles = ceil_div(nc, kTcN);
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(full + s, ph);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the gathered rows -> tensor core
+          mbar_wait(acce + b, aph ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t bs = sB_s + static_cast<uint32_t>(s) * kTcBBytes;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)  // k chunks 2kk, 2kk + 1: +256 B
+            tc_mma(tmem + b * kTcN, tc_sdesc(as + kk * 256), tc_sdesc(bs + kk * 256), kk);
+          tc_commit(empty + s);
+          tc_commit(accf + b);
+          if (++s == kTcStages) {
+            s = 0;
+            ph ^= 1;
+          }
+          if (++b == 2) {
+            b = 0;
+            aph ^= 1;
+          }
+        }
+        tc_commit(aempty + ua);
+        ++n;
+      }
+    }
+  } else {
+    // Epilogue: lane quarter (warp % 4), column half.
+    const int ew = warp - kTcProdWarps - 2;
+    const int quarter = warp & 3, half = ew >> 2;
+    const int row = quarter * 32 + lane;
+    int b = 0;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      const TcUnit U = tc_unit(S, u);
+      if (U.nq == 0) continue;
+      const NnItem w = S.items[0][U.item];
+      float b1 = INFINITY, b2 = INFINITY, b3 = INFINITY;
+      int s1 = 0, s2 = 0;
+      unsigned m1 = 0, m2 = 0;  // candidates of s1 / s2 within the slack of the subtile's minimum
+      const float slack = row < U.nq ? tc_slack(w.q[U.qt * kTcM + row], Bo) : 0.0f;
+      const int ntiles = ceil_div(w.nc, kTcN);
+      for (int t = 0; t < ntiles; ++t) {
+        mbar_wait(accf + b, aph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * kTcN + half * (kTcN / 2);
+#pragma unroll
+        for (int sp = 0; sp < kTcN / 64; sp += 2) {
+          uint32_t v0[32], v1[32];
+          TC_LD32(t0 + sp * 32, v0);
+          TC_LD32(t0 + sp * 32 + 32, v1);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const float tm0 = tc_min32(v0), tm1 = tc_min32(v1);
+          const int sid = t * (kTcN / 32) + half * (kTcN / 64) + sp;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float tm = h ? tm1 : tm0;
+            // Subtiles arrive in increasing order within the half: strict <
+            // keeps the earliest (min/max network as in the FFMA2 filter).
+            const bool lt1 = tm < b1, lt2 = tm < b2;
+            b3 = fminf(b3, fmaxf(b2, tm));
+            b2 = fminf(b2, fmaxf(b1, tm));
+            b1 = fminf(b1, tm);
+            s2 = lt1 ? s1 : (lt2 ? sid + h : s2);
+            s1 = lt1 ? sid + h : s1;
+            if (lt2) {  // rare after the first tiles
+              const unsigned m = tc_mask(h ? v1 : v0, __fadd_ru(tm, slack));
+              m2 = lt1 ? m1 : m;
+              m1 = lt1 ? m : m1;
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        mbar_arrive(acce + b);
+        if (++b == 2) {
+          b = 0;
+          aph ^= 1;
+        }
+      }
+      // Merge the column halves (lexicographic (value, subtile) top-3).
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcEpiWarps));
+      if (half == 1) {
+        xb[0][row] = b1;
+        xb[1][row] = b2;
+        xb[2][row] = b3;
+        xs[row] = s1 | (s2 << 16);
+        xm[0][row] = m1;
+        xm[1][row] = m2;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kTcEpiWarps));
+      if (half == 0 && row < U.nq) {
+        const int o12 = xs[row];
+        tc_top3_insert(b1, s1, m1, b2, s2, m2, b3, xb[0][row], o12 & 0xffff, xm[0][row]);
+        tc_top3_insert(b1, s1, m1, b2, s2, m2, b3, xb[1][row], o12 >> 16, xm[1][row]);
+        b3 = fminf(b3, xb[2][row]);
+        float4* o = S.tc_top + 2 * ((static_cast<int64_t>(w.slot) * w.nchunks + w.chunk) * kNnQB + U.qt * kTcM + row);
+        o[0] = make_float4(b1, b2, b3, __int_as_float(s1 | (s2 << 16)));
+        o[1] = make_float4(__uint_as_float(m1), __uint_as_float(m2), 0.0f, 0.0f);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == kTcMmaWarp) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Certification of the tensor-core top-3 (comment above nn_tc_kernel): one
+// thread per (query, split).
+__global__ void __launch_bounds__(kTcM) nn_tc_window_kernel(DevProblem P, DevState S, NnPlan plan) {
+  pdl_enter();
+  const int n_units = S.nn_dyn[1] * kTcUnitsPerItem;
+  const float Bo = __double2float_ru(P.obj_meta[3]);
+  for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+    const TcUnit U = tc_unit(S, u);
+    if (U.nq == 0) continue;
+    const NnItem w = S.items[0][U.item];
+    if (threadIdx.x == 0) {
+      const unsigned long long pairs = static_cast<unsigned long long>(U.nq) * w.nc;
+      const unsigned long long nq0 = w.chunk == 0 ? U.nq : 0;
+      atomicAdd(S.stats + 2, nq0);
+      atomicAdd(S.stats + 4, pairs);
+      atomicAdd(S.stats + 12, pairs);
+      unsigned long long* is = S.iter_stats + 4 * plan.iter;
+      atomicAdd(is, pairs);
+      atomicAdd(is + 2, nq0);
+    }
+    const int r = threadIdx.x;
+    if (r >= U.nq) continue;
+    const int qi = U.qt * kTcM + r;
+    const int qlocal = w.q_first + qi;
+    const float4 q = w.q[qi];
+    const float mg = q.w;
+    const float4* tp = S.tc_top + 2 * ((static_cast<int64_t>(w.slot) * w.nchunks + w.chunk) * kNnQB + qi);
+    const float4 T = tp[0];
+    const float4 Tm = tp[1];
+    const int s12 = __float_as_int(T.w);
+    const float thr_sel = __fadd_ru(T.x, tc_slack(q, Bo));
+    bool ovf = T.z <= thr_sel;
+    const int nscan = T.y <= thr_sel ? 2 : 1;
+    // The candidates of s1 (and s2) whose TC value is within the slack of
+    // their subtile's minimum — a superset of the split's d32 window and of
+    // its d32 minimum — in increasing position: their d32 values.
+    const int sa = s12 & 0xffff, sb = s12 >> 16;
+    const unsigned ma = __float_as_uint(Tm.x), mb = nscan == 2 ? __float_as_uint(Tm.y) : 0u;
+    const bool a_first = nscan == 1 || sa < sb;
+    int cpos[kWinCap + 1];
+    float cd[kWinCap + 1];
+    int nc = 0;
+    float b1 = INFINITY;
+    for (int sc = 0; sc < 2; ++sc) {
+      const int sid = (sc == 0) == a_first ? sa : sb;
+      unsigned m = (sc == 0) == a_first ? ma : mb;
+      while (m) {
+        const int c = __ffs(m) - 1;
+        m &= m - 1;
+        const float d = d32(q.x, q.y, q.z, pc_get(w.c, sid * kSub + c));
+        b1 = fminf(b1, d);
+        if (nc <= kWinCap) {
+          cpos[nc] = w.c_base + sid * kSub + c;
+          cd[nc] = d;
+        }
+        ++nc;
+      }
+    }
+    if (nc > kWinCap) ovf = true;  // (not seen: masks hold one or two candidates)
+    const float thr = __fadd_ru(b1, mg);
+    int pos[kWinCap];
+    float md[kWinCap];
+    int np = 0, pmin = -1;
+    for (int e = 0; e < min(nc, kWinCap); ++e) {
+      if (cd[e] <= thr) {
+        pos[np] = cpos[e];
+        md[np] = cd[e];
+        ++np;
+        if (cd[e] == b1 && pmin < 0) pmin = cpos[e];
+      }
+    }
+    ovf = ovf || np > kWinCap;
+    if (w.nchunks == 1) {
+      if (ovf) {
+        push_refine(S, w.kind, w.owner, qlocal, 1, plan.iter);
+      } else if (np == 1) {
+        *nn_result_slot(P, S, w.kind, w.owner, qlocal) = pmin;  // certified
+      } else {
+        const NnGeom g = nn_geom(P, S, plan, w.kind, w.owner, qlocal);
+        *nn_result_slot(P, S, w.kind, w.owner, qlocal) = nn_decide(g, pos, np, w.kind == 0 && !plan.pooled, S.stats);
+      }
+    } else {
+      NnPartial pr;
+      if (ovf) {
+        // The split's minimum may lie in an unscanned subtile: a lower bound
+        // keeps it in the merge's reach, and the unlisted window forces the
+        // full rescan whenever it is.
+        pr.b1 = __fsub_rd(T.x, tc_et(q, Bo));
+        pr.pos = kAmbiguous | kNoBlock;
+      } else if (np == 1) {
+        pr.b1 = b1;
+        pr.pos = pmin;
+      } else {
+        const int blk = win_alloc(S);
+        if (blk >= 0) {
+          S.amb_n[blk] = 0;
+          for (int e = 0; e < np; ++e) win_push(S, blk, pos[e], md[e]);
+        }
+        pr.b1 = b1;
+        pr.pos = kAmbiguous | (blk >= 0 ? blk : kNoBlock);
+      }
+      S.partials[(static_cast<int64_t>(w.slot) * w.nchunks + w.chunk) * kFwdQB + qi] = pr;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
 // Counts, exclusive scans and the per-round counter resets in one CTA (one
@@ -1125,6 +1655,7 @@ int nn_smem_bytes() { return kNnSmem; }
 void nn_set_attrs() {
   cudaFuncSetAttribute(nn_filter_kernel<kFwdQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, kNnSmem);
   cudaFuncSetAttribute(nn_rev_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRevSmem);
+  cudaFuncSetAttribute(nn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_rev_blocks_per_sm, nn_rev_kernel, kRevThreads, kRevSmem);
   g_rev_blocks_per_sm = std::max(1, g_rev_blocks_per_sm);
 }
@@ -1144,9 +1675,17 @@ int launch_nn(const DevProblem& P, DevState& S, const NnPlan& plan, int grid, in
               cudaEvent_t ev_begin, cudaEvent_t ev_end, cudaEvent_t rev_done) {
   int n = 0;
   if (ev_begin) cudaEventRecord(ev_begin, st);
-  pdl_launch(nn_filter_kernel<kFwdQ>, dim3(grid), dim3(kNnThreads), kNnSmem, st, P, S, plan, 0);
-  ++n;
-  if (ev_end) cudaEventRecord(ev_end, st);
+  if (plan.use_tc) {
+    // Tensor-core filter (one CTA per SM) and its certification pass.
+    pdl_launch(nn_tc_kernel, dim3(refine_grid / 2), dim3(kTcThreads), kTcSmem, st, P, S, plan);
+    if (ev_end) cudaEventRecord(ev_end, st);
+    pdl_launch(nn_tc_window_kernel, dim3(4 * refine_grid), dim3(kTcM), 0, st, P, S, plan);
+    n += 2;
+  } else {
+    pdl_launch(nn_filter_kernel<kFwdQ>, dim3(grid), dim3(kNnThreads), kNnSmem, st, P, S, plan, 0);
+    ++n;
+    if (ev_end) cudaEventRecord(ev_end, st);
+  }
   if (!rev_done && plan.kind == 0) {
     // refine_grid is two CTAs per SM; the reverse grid fills every SM.
     pdl_launch(nn_rev_kernel, dim3(refine_grid / 2 * g_rev_blocks_per_sm), dim3(kRevThreads), kRevSmem, st, P, S,

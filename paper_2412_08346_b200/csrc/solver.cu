@@ -110,6 +110,12 @@ struct asicp_ctx {
   int nn_mode = 0;
   int use_graph = 1;
   int profile = 0;
+  // Forward / final NN filter on the tensor cores (nn.cu nn_tc_kernel);
+  // ASICP_NN_TC=1 selects it.
+  bool nn_tc = [] {
+    const char* e = std::getenv("ASICP_NN_TC");
+    return e && e[0] == '1';
+  }();
   int num_sms = 148;
   int nn_grid = 296;
   int max_chunks = 16;
@@ -147,7 +153,7 @@ struct asicp_ctx {
   DevState S{};
 
   // Device buffers.
-  Buf obj64, obj_meta, obj_cand, obj_cand4, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
+  Buf obj64, obj_meta, obj_cand, obj_cand4, obj_tc, tc_top, scene64, surf64, pre_surf_off, pre_tcp, pre_sdf, grids, sdf_values, part_pre_d,
       part_surf_off, part_pop, pop_off, pop_logk1, init_theta_d, scene32, sdf_coarse;
   // Collision clusters (collide.cu) and the scratch of their Morton sort.
   Buf scene_box, scene_code, scene_idx, scene_tmp, clusters, subclusters, scene_s32, scene_perm;
@@ -252,7 +258,7 @@ struct asicp_ctx {
     if (ev_rev_fork) cudaEventDestroy(ev_rev_fork);
     if (ev_rev_join) cudaEventDestroy(ev_rev_join);
     if (rev_side) cudaStreamDestroy(rev_side);
-    Buf* all[] = {&obj64, &obj_meta, &obj_cand, &obj_cand4, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
+    Buf* all[] = {&obj64, &obj_meta, &obj_cand, &obj_cand4, &obj_tc, &tc_top, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
                   &scene32, &sdf_coarse, &scene_box, &scene_code, &scene_idx, &scene_tmp, &clusters, &subclusters,
                   &scene_s32, &scene_perm, &theta,
@@ -398,6 +404,10 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->obj_cand4.ensure(static_cast<size_t>(c->n_obj_pad) * sizeof(float4));
   launch_object_prepare(c->obj64.as<double>(), c->n_obj, c->n_obj_pad, c->obj_meta.as<double>(),
                         c->obj_cand.as<float4>(), c->obj_cand4.as<float4>(), st);
+  if (c->nn_tc) {
+    c->obj_tc.ensure(static_cast<size_t>(c->n_obj) * 3 * sizeof(float4));
+    launch_obj_tc(c->obj_cand4.as<float4>(), c->n_obj, c->obj_tc.as<float4>(), st);
+  }
   upload(c, c->scene64, p.scene_cloud, 3 * p.n_scene, st);
   {
     // FP32 scene copy and the collision clusters, built on the device
@@ -644,6 +654,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   c->item_off.ensure(2 * (Jz + 1) * 4);
   c->item_counter.ensure(4 * 4);  // [0..1] item counters, [2..3] device split (nn_dyn)
   c->partials.ensure(fwd_slots * kNnQB * sizeof(NnPartial));
+  if (c->nn_tc) c->tc_top.ensure(fwd_slots * kNnQB * 2 * sizeof(float4));
   // Ambiguous windows: ~0.3 % of queries on cfg2, but up to ~15 % for dense
   // clouds matched from far (100k points, queries 25 cm out).  A (query,
   // split) allocates at most one block while the pool lasts, so a quarter of
@@ -692,6 +703,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   P.obj64 = c->obj64.as<double>();
   P.obj_cand = c->obj_cand.as<float4>();
   P.obj_cand4 = c->obj_cand4.as<float4>();
+  P.obj_tc = c->nn_tc ? c->obj_tc.as<float4>() : nullptr;
   P.scene64 = c->scene64.as<double>();
   P.scene32 = c->scene32.as<float4>();
   P.n_clusters = c->n_clusters;
@@ -784,6 +796,7 @@ void prepare(asicp_ctx* c, const asicp_problem& p) {
   S.item_counter = c->item_counter.as<int>();
   S.nn_dyn = c->item_counter.as<int>() + 2;
   S.partials = c->partials.as<NnPartial>();
+  S.tc_top = c->nn_tc ? c->tc_top.as<float4>() : nullptr;
   S.amb_pool = c->amb_pool.as<int2>();
   S.amb_n = c->amb_n.as<int>();
   S.amb_count = c->amb_count.as<int>();
@@ -866,6 +879,7 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   plan.item_overhead = item_overhead;
   plan.throughput = c->throughput;
   plan.max_ns = c->max_ns;
+  plan.use_tc = c->nn_tc && !plan.fp64_mode ? 1 : 0;
   return plan;
 }
 
