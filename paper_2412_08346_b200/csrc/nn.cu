@@ -1444,9 +1444,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_const
             b1 = fminf(b1, tm);
             s2 = lt1 ? s1 : (lt2 ? sid + h : s2);
             s1 = lt1 ? sid + h : s1;
-            if (lt2) {  // rare after the first tiles
+            if (__any_sync(0xffffffffu, lt2)) {  // warp-uniform branch; rare after the first tiles
               const unsigned m = tc_mask(h ? v1 : v0, __fadd_ru(tm, slack));
-              m2 = lt1 ? m1 : m;
+              m2 = lt1 ? m1 : (lt2 ? m : m2);
               m1 = lt1 ? m : m1;
             }
           }
