@@ -33,6 +33,7 @@ ASICP_OPT_PROFILE = 3
 ASICP_OPT_MAX_CHUNKS = 4
 ASICP_OPT_WINDOW_POOL = 5
 ASICP_OPT_THROUGHPUT = 6
+ASICP_OPT_NN_TC = 7
 ASICP_PRECOND_FIXED = 0
 ASICP_PRECOND_GAUSS_NEWTON_ROTATION = 1
 

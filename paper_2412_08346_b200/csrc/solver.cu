@@ -1279,6 +1279,10 @@ int asicp_set_option(asicp_ctx* ctx, int option, int64_t value) {
     case ASICP_OPT_PROFILE:
       ctx->profile = static_cast<int>(value);
       break;
+    case ASICP_OPT_NN_TC:
+      ctx->nn_tc = value != 0;
+      ctx->prepared = false;  // the TF32 candidate rows and the top-3 buffer are built at prepare
+      break;
     case ASICP_OPT_THROUGHPUT:
       ctx->throughput = value ? 1 : 0;
       ctx->P.throughput = ctx->throughput;  // a prepared problem keeps its buffers; the graph is re-captured

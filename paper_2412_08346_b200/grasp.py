@@ -377,7 +377,8 @@ class Solver:
     persist across calls.  `stream` may be a torch CUDA stream handle."""
 
     def __init__(self, device: int = 0, stream: int | None = None, nn_mode: int = 0, use_graph: bool = True,
-                 profile: bool = False, window_pool: int = 0, max_chunks: int = 0, throughput: bool = False):
+                 profile: bool = False, window_pool: int = 0, max_chunks: int = 0, throughput: bool = False,
+                 nn_tc: bool | None = None):
         self.lib = L.load()
         err = C.create_string_buffer(512)
         self.ctx = self.lib.asicp_create(device, C.c_void_p(stream) if stream else None, err, 512)
@@ -392,6 +393,8 @@ class Solver:
             self.lib.asicp_set_option(self.ctx, L.ASICP_OPT_MAX_CHUNKS, max_chunks)
         if throughput:  # the context shares the GPU with other solves (BatchSolver)
             self.lib.asicp_set_option(self.ctx, L.ASICP_OPT_THROUGHPUT, 1)
+        if nn_tc is not None:  # tensor-core NN filter (default: ASICP_NN_TC, else off)
+            self.lib.asicp_set_option(self.ctx, L.ASICP_OPT_NN_TC, 1 if nn_tc else 0)
         self._cp: CProblem | None = None
         self._bufs: SolutionBuffers | None = None
 

@@ -19,6 +19,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_2412_08346_b200 import Solver, fixtures, shard  # noqa: E402
 from paper_2412_08346_b200.batch import BatchSolver  # noqa: E402
+from paper_2412_08346_b200 import _lib as L  # noqa: E402
 from paper_2412_08346_b200.grasp import CProblem  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -28,7 +29,14 @@ ap.add_argument("--objects", type=int, default=11)
 ap.add_argument("--unit", type=int, default=0)
 ap.add_argument("--eager", action="store_true")
 ap.add_argument("--max-chunks", type=int, default=0, help="ASICP_OPT_MAX_CHUNKS of the batch contexts")
+ap.add_argument("--tc", type=int, default=0, help="NN filter on the tensor cores: 0 none, 1 every unit, K >= 2 every K-th")
 a = ap.parse_args()
+
+
+def tc_setup(i, s):
+    if a.tc:
+        s.lib.asicp_set_option(s.ctx, L.ASICP_OPT_NN_TC, 1 if (a.tc == 1 or i % a.tc == 0) else 0)
+
 
 problems = [fixtures.config(4, seed=o).problem() for o in range(a.objects)]
 units = shard.units_of(problems)
@@ -71,7 +79,7 @@ if a.mode == "subset":
     # Device time of a batch of the first U units (the per-rank share of the
     # cfg4 plan at 8 / 4 / 2 ranks is 4 / 8 / 16 whole units + a slice).
     for u in [int(x) for x in a.units.split(",")]:
-        b = BatchSolver(subs[:u])
+        b = BatchSolver(subs[:u], setup=tc_setup)
         b.run()
         ts = []
         for _ in range(5):
@@ -92,7 +100,7 @@ for i, p in enumerate(subs):
     s.close()
 print("isolated unit solve ms:", " ".join(f"{t:.2f}" for t in iso))
 print(f"sum of isolated unit solves: {sum(iso):.1f} ms  (mean {sum(iso) / len(iso):.2f} ms)")
-b = BatchSolver(subs, max_chunks=a.max_chunks)
+b = BatchSolver(subs, max_chunks=a.max_chunks, setup=tc_setup)
 b.run()
 ts = []
 for _ in range(5):
