@@ -1135,6 +1135,19 @@ __device__ __forceinline__ float tf32_rna(float x) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Wait with the thread suspended in hardware until the phase completes (the
+// time hint only bounds a single try), so idle roles do not poll the issue
+// slots the epilogue needs.
+__device__ __forceinline__ void mbar_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!done);
+}
 __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
@@ -1307,7 +1320,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < kPer; ++i) rows[i] = rows_next[i];
         if (t + 1 < ntiles) load_rows(t + 1, rows_next);
-        mbar_wait(empty + s, ph ^ 1);
+        mbar_sleep(empty + s, ph ^ 1);
         const uint32_t bs = sB_s + static_cast<uint32_t>(s) * kTcBBytes;
         float* bg = sB + s * (kTcBBytes / 4);
 #pragma unroll
@@ -1351,7 +1364,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_const
         qv[i] = r < U.nq ? qs[r] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       const int ua = n & 1;
-      mbar_wait(aempty + ua, ((n >> 1) & 1) ^ 1);
+      mbar_sleep(aempty + ua, ((n >> 1) & 1) ^ 1);
       float* a = sA + ua * (kTcABytes / 4);
 #pragma unroll
       for (int i = 0; i < kTcM / 32; ++i) {
@@ -1377,14 +1390,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_const
         if (U.nq == 0) continue;
         const int nc = S.items[0][U.item].nc;
         const int ua = n & 1;
-        mbar_wait(afull + ua, (n >> 1) & 1);
+        mbar_sleep(afull + ua, (n >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t as = sA_s + static_cast<uint32_t>(ua) * kTcABytes;
         const int ntiles = ceil_div(nc, kTcN);
         for (int t = 0; t < ntiles; ++t) {
-          mbar_wait(full + s, ph);
+          mbar_sleep(full + s, ph);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the gathered rows -> tensor core
-          mbar_wait(acce + b, aph ^ 1);
+          mbar_sleep(acce + b, aph ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t bs = sB_s + static_cast<uint32_t>(s) * kTcBBytes;
 #pragma unroll
@@ -1422,7 +1435,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) nn_tc_kernel(const __grid_const
       const float slack = row < U.nq ? tc_slack(w.q[U.qt * kTcM + row], Bo) : 0.0f;
       const int ntiles = ceil_div(w.nc, kTcN);
       for (int t = 0; t < ntiles; ++t) {
-        mbar_wait(accf + b, aph);
+        mbar_sleep(accf + b, aph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t t0 = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + b * kTcN + half * (kTcN / 2);
 #pragma unroll
