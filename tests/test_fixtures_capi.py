@@ -51,6 +51,17 @@ def test_library_exports_every_declared_symbol():
     assert not [n for n in sorted(fx_names) if not hasattr(fx, n)]
 
 
+def test_python_constants_mirror_the_header():
+    """Every ASICP_OPT_* / status define of asicp.h has the same value in the
+    ctypes layer (_lib.py), so Solver options reach the right switch."""
+    text = (ROOT / "include" / "asicp.h").read_text()
+    defines = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(ASICP_\w+)\s+(-?\d+)", text)}
+    opts = {k: v for k, v in defines.items() if k.startswith("ASICP_OPT_")}
+    assert {"ASICP_OPT_NN_MODE", "ASICP_OPT_THROUGHPUT", "ASICP_OPT_NN_TC"} <= set(opts)
+    for k, v in opts.items():
+        assert getattr(L, k) == v, k
+
+
 def test_schedule_kats():
     """test_spatial_index.cpp:153-184 / test_acceptance.cpp:633-657."""
     assert minibatch_schedule(13, 40, 900) == 439
