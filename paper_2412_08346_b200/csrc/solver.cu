@@ -176,7 +176,7 @@ struct asicp_ctx {
   cudaStream_t side = nullptr;  // forked work inside an iteration (median bandwidth)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t rev_side = nullptr;  // the reverse match beside the minibatch draw / forward filter
-  cudaEvent_t ev_rev_fork = nullptr, ev_rev_join = nullptr;
+  cudaEvent_t ev_rev_fork = nullptr, ev_rev_join = nullptr, ev_fill = nullptr;
   bool fork_rev = [] {  // ASICP_FORK_REV=0: the reverse match in line
     const char* e = std::getenv("ASICP_FORK_REV");
     return !(e && e[0] == '0');
@@ -257,6 +257,7 @@ struct asicp_ctx {
     if (side) cudaStreamDestroy(side);
     if (ev_rev_fork) cudaEventDestroy(ev_rev_fork);
     if (ev_rev_join) cudaEventDestroy(ev_rev_join);
+    if (ev_fill) cudaEventDestroy(ev_fill);
     if (rev_side) cudaStreamDestroy(rev_side);
     Buf* all[] = {&obj64, &obj_meta, &obj_cand, &obj_cand4, &obj_tc, &tc_top, &scene64, &surf64, &pre_surf_off, &pre_tcp, &pre_sdf, &grids, &sdf_values,
                   &part_pre_d, &part_surf_off, &part_pop, &pop_off, &pop_logk1, &init_theta_d,
@@ -888,20 +889,34 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
 // (the roofline kernel of bench.py).
 void enqueue_nn(asicp_ctx* c, const NnPlan& plan, int minibatch_m, bool capture) {
   cudaStream_t st = c->stream;
-  launch_nn_plan(c->P, c->S, plan, st);
   // The reverse match (colliding particles) needs neither the minibatch pools
   // nor the forward filter: fork it so it fills the SMs the draw leaves idle.
+  // The item fill (both lists) depends only on the collision test, so it
+  // goes on the fork too, ahead of the reverse match, and the forward filter
+  // waits for it after the draw.
   const bool fork_rev = plan.kind == 0 && c->fork_rev && !c->profile;
-  if (fork_rev) {
+  const bool fork_fill = fork_rev && minibatch_m > 0;
+  if (fork_fill) {
     CUDA_OK(cudaEventRecord(c->ev_rev_fork, st));
     CUDA_OK(cudaStreamWaitEvent(c->rev_side, c->ev_rev_fork, 0));
-    launch_nn_rev(c->P, c->S, plan, 2 * c->num_sms, c->rev_side);
-    CUDA_OK(cudaEventRecord(c->ev_rev_join, c->rev_side));
+    launch_nn_plan(c->P, c->S, plan, c->rev_side);
+    CUDA_OK(cudaEventRecord(c->ev_fill, c->rev_side));
+  } else {
+    launch_nn_plan(c->P, c->S, plan, st);
   }
   int mb_launches = 0;
   if (minibatch_m > 0) {
     StageTimer t(c, asicp_ctx::kStMinibatch, capture);
     mb_launches = launch_minibatch(c->P, c->S, minibatch_m, st);
+  }
+  if (fork_rev) {
+    if (!fork_fill) {  // the fill ran on the main stream: fork after it
+      CUDA_OK(cudaEventRecord(c->ev_rev_fork, st));
+      CUDA_OK(cudaStreamWaitEvent(c->rev_side, c->ev_rev_fork, 0));
+    }
+    launch_nn_rev(c->P, c->S, plan, 2 * c->num_sms, c->rev_side);
+    CUDA_OK(cudaEventRecord(c->ev_rev_join, c->rev_side));
+    if (fork_fill) CUDA_OK(cudaStreamWaitEvent(st, c->ev_fill, 0));
   }
   asicp_ctx::ProfEvent e{asicp_ctx::kStNn, nullptr, nullptr};
   if (c->profile && !capture) {
@@ -1249,6 +1264,7 @@ asicp_ctx* asicp_create(int device, void* stream, char* err, size_t errlen) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->rev_side, cudaStreamNonBlocking));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_rev_fork, cudaEventDisableTiming));
     CUDA_OK(cudaEventCreateWithFlags(&c->ev_rev_join, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->ev_fill, cudaEventDisableTiming));
     c->nn_grid = c->num_sms * std::max(1, nn_blocks_per_sm());
   });
   if (rc != ASICP_OK) {
