@@ -61,3 +61,17 @@ def test_tensor_core_filter_full_cfg2(tc_solver):
     _same(got, want)
     st = tc_solver.raw_stats()
     assert st[2] > 0 and st[12] > 0  # the filter ran (queries, forward pairs)
+
+
+def test_tensor_core_filter_through_the_context_option():
+    """The same path selected per context (ASICP_OPT_NN_TC, Solver(nn_tc=True))
+    next to a default context: both bit-identical to the reference."""
+    ref = _ref()
+    fx = fixtures.config(4, seed=3, particles_per_preshape=8).set(k_max=12, k_stein=6, anneal_period_total=12)
+    want = ref.optimize_grasp(fx)
+    for tc in (True, False):
+        s = Solver(nn_tc=tc)
+        try:
+            _same(s.optimize(fx), want)
+        finally:
+            s.close()

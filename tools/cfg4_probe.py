@@ -29,6 +29,7 @@ ap.add_argument("--objects", type=int, default=11)
 ap.add_argument("--unit", type=int, default=0)
 ap.add_argument("--eager", action="store_true")
 ap.add_argument("--max-chunks", type=int, default=0, help="ASICP_OPT_MAX_CHUNKS of the batch contexts")
+ap.add_argument("--latency", action="store_true", help="subset: batch contexts in latency mode (no ASICP_OPT_THROUGHPUT)")
 ap.add_argument("--tc", type=int, default=0, help="NN filter on the tensor cores: 0 none, 1 every unit, K >= 2 every K-th")
 a = ap.parse_args()
 
@@ -79,7 +80,7 @@ if a.mode == "subset":
     # Device time of a batch of the first U units (the per-rank share of the
     # cfg4 plan at 8 / 4 / 2 ranks is 4 / 8 / 16 whole units + a slice).
     for u in [int(x) for x in a.units.split(",")]:
-        b = BatchSolver(subs[:u], setup=tc_setup)
+        b = BatchSolver(subs[:u], setup=tc_setup, throughput=not a.latency)
         b.run()
         ts = []
         for _ in range(5):
