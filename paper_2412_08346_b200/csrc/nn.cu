@@ -42,8 +42,8 @@ constexpr int kNnSmem = kNnStages * kNnTile * 16;
 constexpr int kMinChunk = 2 * kNnTile;       // smallest candidate split
 
 // ---------------------------------------------------------------------------
-// Work planning: per particle counts -> exclusive scans (nn_plan_kernel, one
-// CTA) -> item lists (nn_fill_kernel).
+// Work planning: per particle counts -> exclusive scans -> item lists, all
+// in nn_fill_kernel.
 // Forward: count = query blocks; the split factor is chosen on the device
 // from the total T so that T x splits ~ plan.target_items (few matching
 // particles -> many splits per particle), capped by plan.nchunks and by
@@ -1608,57 +1608,6 @@ __global__ void __launch_bounds__(kTcM) nn_tc_window_kernel(DevProblem P, DevSta
 // ---------------------------------------------------------------------------
 // Host launchers
 // ---------------------------------------------------------------------------
-// Counts, exclusive scans and the per-round counter resets in one CTA (one
-// launch instead of a count kernel, two device scans and three memsets):
-// each thread owns a contiguous range of particles.
-constexpr int kPlanThreads = 1024;
-
-__global__ void __launch_bounds__(kPlanThreads) nn_plan_kernel(DevProblem P, DevState S, NnPlan plan) {
-  __shared__ int sf[kPlanThreads], sr[kPlanThreads];
-  const int tid = threadIdx.x;
-  const int per = ceil_div(P.J, kPlanThreads);
-  const int j0 = min(P.J, tid * per), j1 = min(P.J, j0 + per);
-  int cf = 0, cr = 0;
-  for (int j = j0; j < j1; ++j) {
-    int fwd = 0, rev = 0;
-    if (plan.kind == 2 || S.active[j]) {
-      if (plan.kind != 2 && S.n_col[j] > 0)
-        rev = ceil_div(S.n_col[j], kRevWQ);
-      else
-        fwd = ceil_div(surf_count(P, j), kFwdQB);
-    }
-    S.item_count[0][j] = fwd;
-    S.item_count[1][j] = rev;
-    cf += fwd;
-    cr += rev;
-  }
-  sf[tid] = cf;
-  sr[tid] = cr;
-  __syncthreads();
-  for (int off = 1; off < kPlanThreads; off <<= 1) {  // inclusive scans of the range sums
-    const int vf = tid >= off ? sf[tid - off] : 0, vr = tid >= off ? sr[tid - off] : 0;
-    __syncthreads();
-    sf[tid] += vf;
-    sr[tid] += vr;
-    __syncthreads();
-  }
-  int of = tid ? sf[tid - 1] : 0, orr = tid ? sr[tid - 1] : 0;
-  for (int j = j0; j < j1; ++j) {
-    S.item_off[0][j] = of;
-    S.item_off[1][j] = orr;
-    of += S.item_count[0][j];
-    orr += S.item_count[1][j];
-  }
-  if (tid == 0) {
-    S.item_off[0][P.J] = sf[kPlanThreads - 1];
-    S.item_off[1][P.J] = sr[kPlanThreads - 1];
-    S.item_count[0][P.J] = S.item_count[1][P.J] = 0;
-    S.item_counter[0] = S.item_counter[1] = 0;
-    *S.refine_count = 0;
-    *S.amb_count = 0;
-  }
-}
-
 void launch_nn_plan(const DevProblem& P, DevState& S, const NnPlan& plan, cudaStream_t st) {
   pdl_launch(nn_fill_kernel, dim3((P.J + kFillThreads - 1) / kFillThreads), dim3(kFillThreads), 0, st, P, S, plan);
 }
