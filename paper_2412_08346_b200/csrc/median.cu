@@ -252,7 +252,6 @@ __global__ void __cluster_dims__(kMedCl, 1, 1) __launch_bounds__(kMedThreads)
     }
   };
   const int shifts[6] = {52, 40, 28, 16, 4, 0}, widths[6] = {12, 12, 12, 12, 12, 4};
-  bool gathered = false;
   for (int pass = 0; pass < 6; ++pass) {
     const int shift = shifts[pass];
     const unsigned int dmask = (1u << widths[pass]) - 1u;
@@ -339,11 +338,9 @@ __global__ void __cluster_dims__(kMedCl, 1, 1) __launch_bounds__(kMedThreads)
         block_bitonic_sort(gath, n2);
         prefix = gath[rank];
       }
-      gathered = true;
       break;
     }
   }
-  (void)gathered;
   if (crank == 0 && tid == 0) {
     const double median = __longlong_as_double(static_cast<long long>(prefix));
     const double h = median / P.pop_logk1[pop];
