@@ -299,41 +299,26 @@ __global__ void __launch_bounds__(kCostThreads) cost_kernel(DevProblem P, DevSta
   const int* pmap = final_pass ? nullptr : S.pool_map;
   for (int c0 = 0; c0 < npairs; c0 += kCostChunk) {
     const int n = min(kCostChunk, npairs - c0);
-    // A thread's kCostU pairs of the chunk: each dependent level of gathers
-    // (match index -> pool map -> FP64 rows) is issued for all of them at
-    // once, so a chunk costs three L2 round trips, not three per pair.
-    constexpr int kCostU = kCostChunk / kCostHalf;
-    int idx[kCostU];
-    int64_t rrow[kCostU];
-#pragma unroll
-    for (int u = 0; u < kCostU; ++u) {
-      const int i = c0 + min(tid + u * kCostHalf, n - 1);
-      idx[u] = reverse ? S.res_rev[row + i] : S.res_fwd[so + i];
-      rrow[u] = reverse ? S.col_idx[row + i] : 0;
-    }
-    if (!reverse) {
-#pragma unroll
-      for (int u = 0; u < kCostU; ++u)
-        rrow[u] = pmap ? pmap[static_cast<int64_t>(j) * P.n_obj_pad + idx[u]] : idx[u];
-    }
-    V3 src[kCostU], tr[kCostU], ref[kCostU];
-#pragma unroll
-    for (int u = 0; u < kCostU; ++u) {
-      const int i = c0 + min(tid + u * kCostHalf, n - 1);
-      const int si = reverse ? idx[u] : i;  // surface row of the pair
-      src[u] = load3(P.surf64, s0 + si);
-      tr[u] = load3(S.S64, so + si);
-      ref[u] = load3(reverse ? P.scene64 : P.obj64, rrow[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kCostU; ++u) {
-      const int e = tid + u * kCostHalf;
-      if (e >= n) continue;
-      const V3 res = sub(tr[u], ref[u]);
+    for (int e = tid; e < n; e += kCostHalf) {
+      const int i = c0 + e;
+      V3 src, tr, ref;
+      if (reverse) {
+        const int sidx = S.res_rev[row + i];
+        src = load3(P.surf64, s0 + sidx);
+        tr = load3(S.S64, so + sidx);
+        ref = load3(P.scene64, S.col_idx[row + i]);
+      } else {
+        src = load3(P.surf64, s0 + i);
+        tr = load3(S.S64, so + i);
+        const int pos = S.res_fwd[so + i];
+        const int64_t oi = pmap ? pmap[static_cast<int64_t>(j) * P.n_obj_pad + pos] : pos;
+        ref = load3(P.obj64, oi);
+      }
+      const V3 res = sub(tr, ref);
       cost_terms[0 * kCostRow + e] = res.x;
       cost_terms[1 * kCostRow + e] = res.y;
       cost_terms[2 * kCostRow + e] = res.z;
-      for (int jj = 0; jj < 4; ++jj) cost_terms[(3 + jj) * kCostRow + e] = dot(res, mul(dR[jj], src[u]));
+      for (int jj = 0; jj < 4; ++jj) cost_terms[(3 + jj) * kCostRow + e] = dot(res, mul(dR[jj], src));
       cost_terms[7 * kCostRow + e] = sqnorm(res);
     }
     half_sync();
