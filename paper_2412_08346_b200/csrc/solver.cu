@@ -16,6 +16,7 @@
 #include "register.cuh"
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -32,6 +33,16 @@
 namespace {
 
 using namespace asicp;
+
+// NVTX ranges on the host API (header-only NVTX 3: no cost without a tool
+// attached): prepare, capture / graph launch / eager enqueue, wait.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 
 constexpr int kSubRows = kSub;
 constexpr int kStats = 256;  // [0..15] NN counters, [16..255] full rescans per iteration
@@ -371,6 +382,7 @@ void validate(const asicp_problem& p) {
 }
 
 void prepare(asicp_ctx* c, const asicp_problem& p) {
+  NvtxRange range("asicp_prepare");
   // ASICP_PREPARE_TIMING=1: host-side section times to stderr (diagnostics).
   static const bool timing = std::getenv("ASICP_PREPARE_TIMING") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
@@ -1060,6 +1072,7 @@ void enqueue_solve(asicp_ctx* c, bool capture) {
 // Enqueue one solve (graph replay) plus the D2H of the particle summaries
 // into pinned staging; returns without waiting.
 void launch(asicp_ctx* c) {
+  NvtxRange range("asicp_run: launch");
   if (!c->prepared) throw InvalidArgument("asicp_run: no prepared problem");
   if (c->in_flight) throw InvalidArgument("asicp_run_async: a solve is already in flight (call asicp_wait)");
   CUDA_OK(cudaSetDevice(c->device));
@@ -1073,6 +1086,7 @@ void launch(asicp_ctx* c) {
   const bool graph = c->use_graph && !c->profile && (!c->xchg || c->xchg->capturable());
   if (graph) {
     if (!c->graph_valid) {
+      NvtxRange capture_range("asicp_run: capture the solve graph");
       cudaGraph_t g;
       CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
       try {
@@ -1088,6 +1102,7 @@ void launch(asicp_ctx* c) {
     }
     CUDA_OK(cudaGraphLaunch(c->graph_exec, st));
   } else {
+    NvtxRange eager_range("asicp_run: eager enqueue");
     enqueue_solve(c, false);
   }
   CUDA_OK(cudaEventRecord(c->ev1, st));
@@ -1111,6 +1126,7 @@ void launch(asicp_ctx* c) {
 
 // Wait for the launched solve and fill `out` (traces are copied here).
 void finish(asicp_ctx* c, asicp_solution* out) {
+  NvtxRange range("asicp_wait");
   if (!c->in_flight) throw InvalidArgument("asicp_wait: no solve in flight");
   cudaStream_t st = c->stream;
   c->in_flight = false;
