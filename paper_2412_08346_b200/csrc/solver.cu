@@ -887,7 +887,7 @@ NnPlan make_plan(const asicp_ctx* c, int kind, int64_t m, bool pooled) {
   plan.target_items = c->target_items;
   static const int item_overhead = [] {  // ASICP_NN_ITEM_OVERHEAD: split-model experiments
     const char* e = std::getenv("ASICP_NN_ITEM_OVERHEAD");
-    return e ? std::max(0, std::atoi(e)) : 512;
+    return e ? std::max(0, std::atoi(e)) : 1024;  // swept 128-2048: 1024 best on cfg2/cfg3/cfg4
   }();
   plan.item_overhead = item_overhead;
   plan.throughput = c->throughput;
